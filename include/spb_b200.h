@@ -1,0 +1,164 @@
+/*
+ * spb_b200.h -- C ABI of the B200-native Structured Partial Backpropagation
+ * (SPB) training step (arXiv 2111.10672). libspb_b200.so exports exactly the
+ * functions below; everything is plain pointers and sizes, no torch or C++
+ * types. Each entry point names the reference interface it replaces
+ * (/root/reference/proj, file:line).
+ *
+ * Conventions
+ *  - Status codes: every call returns spb_status. The reference throws
+ *    jigsaw::ArgumentError / ProtocolError / ConfigError
+ *    (include/jigsaw/errors.hpp:9-25); exceptions cannot cross a C ABI, so the
+ *    same conditions return SPB_E_ARGUMENT / SPB_E_PROTOCOL / SPB_E_CONFIG and
+ *    spb_last_error() holds the message. CUDA / NCCL failures are
+ *    SPB_E_CUDA / SPB_E_NCCL. The C++ adapter (include/spb_b200/jigsaw_spb.hpp)
+ *    rethrows the reference exception types.
+ *  - Layer numbering is the reference's: layers 1..L, input side first;
+ *    workers 1..k; chunks 1..k (spb.hpp:13-18).
+ *  - Parameter blocks use the reference Params layout (model.hpp:93-94):
+ *    block l (0-based pointer index l-1) = W_l row-major [n_l x n_{l-1}]
+ *    followed by b_l [n_l], i.e. n_l*n_{l-1} + n_l floats. Values are fp32.
+ *  - Datasets: X row-major [N x n_0], Y row-major [N x n_L].
+ *  - A context (spb_ctx) owns device state on one GPU and one CUDA stream.
+ *    It is not thread-safe (the reference's const/thread-safe model methods,
+ *    model.hpp:21-25, are mirrored by one context per thread).
+ */
+#ifndef SPB_B200_H
+#define SPB_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(SPB_BUILD_LIB)
+#define SPB_API __attribute__((visibility("default")))
+#else
+#define SPB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SPB_OK = 0,
+  SPB_E_ARGUMENT = 1, /* jigsaw::ArgumentError */
+  SPB_E_PROTOCOL = 2, /* jigsaw::ProtocolError */
+  SPB_E_CONFIG = 3,   /* jigsaw::ConfigError */
+  SPB_E_CUDA = 4,
+  SPB_E_NCCL = 5
+} spb_status;
+
+typedef struct spb_ctx spb_ctx;
+
+/* Message of the last failing call on this thread (context-free calls) or
+ * on ctx (context calls; ctx may be NULL). Never NULL. */
+SPB_API const char* spb_last_error(const spb_ctx* ctx);
+
+/* ---- SPB bookkeeping: integer-exact host code -------------------------------
+ * Replaces suffix_layers spb.hpp:39 (spb.cpp:16-21). Worker j of k on an
+ * L-layer model backpropagates ceil(j*L/k) layers. */
+SPB_API spb_status spb_suffix_layers(int j, int k, int L, int* out);
+/* chunk_coverage spb.hpp:42 (spb.cpp:23-29): workers {k-m+1..k} into out[0..m). */
+SPB_API spb_status spb_chunk_coverage(int m, int k, int* out);
+/* chunk_layout spb.hpp:46 (spb.cpp:31-41): out[2(m-1)], out[2(m-1)+1] =
+ * first, last layer of chunk m (first > last when the chunk is empty). */
+SPB_API spb_status spb_chunk_layout(int k, int L, int* out);
+/* layer_chunks spb.hpp:49 (spb.cpp:43-49): out[l-1] = chunk of layer l =
+ * number of contributing workers of layer l. */
+SPB_API spb_status spb_layer_chunks(int k, int L, int* out);
+/* draw_batch (spb.cpp:127-131) on the stream Rng(seed).split(step).split(worker)
+ * (spb.cpp:176,187,141): count sample indices in [0, dataset_size). */
+SPB_API spb_status spb_draw_batch(uint64_t seed, int step, int worker, int count, int dataset_size, int* out);
+/* Worker placement for multi-GPU runs: the workers (1-based, ascending) that
+ * rank `rank` of `nranks` hosts, balanced so every rank carries the same
+ * backward work (pairs j, k+1-j). Writes *count entries to out (size >= k). */
+SPB_API spb_status spb_rank_workers(int k, int L, int rank, int nranks, int* out, int* count);
+
+/* make_random_chain_mlp (model.hpp:240-241, model.cpp:208-231): the
+ * reference's synthetic instance (stream Rng(seed).split(0x313a)), generated
+ * in fp64 exactly as the reference does and rounded to fp32. X [samples x n_0],
+ * Y [samples x n_L] (the scalar target repeated when n_L > 1), W[l] = block l+1. */
+SPB_API spb_status spb_make_random_chain_mlp(const int* widths, int n_widths, int samples, uint64_t seed, float* X,
+                                             float* Y, float* const* W);
+
+/* ---- Context: the ChainMlp "layer" (model.hpp:95-111) on one B200 ---------
+ * widths[0..n_widths): [n_0, ..., n_L]; n_L <= 16 (the reference requires
+ * n_L == 1, model.cpp:93; wider heads are the 0.5*||out-y||^2 throughput
+ * variant). k workers of per_worker_batch samples each may run per step. */
+SPB_API spb_status spb_create(const int* widths, int n_widths, int k, int per_worker_batch, int device,
+                      spb_ctx** out);
+SPB_API spb_status spb_destroy(spb_ctx* ctx);
+/* ChainMlp's dataset (model.cpp:86-101), uploaded to HBM. */
+SPB_API spb_status spb_set_dataset(spb_ctx* ctx, const float* X, const float* Y, int N);
+/* Params in / out (LayeredModel::initial_params, spb_sgd_run's iterate x). */
+SPB_API spb_status spb_set_params(spb_ctx* ctx, const float* const* blocks);
+SPB_API spb_status spb_get_params(spb_ctx* ctx, float* const* blocks);
+/* Optimizer: x -= lr * g (spb.cpp:196) when momentum = weight_decay = 0;
+ * otherwise momentum SGD + weight decay (PyTorch semantics). */
+SPB_API spb_status spb_set_optimizer(spb_ctx* ctx, float lr, float momentum, float weight_decay);
+
+/* ---- Worker: partial_backprop spb.hpp:54-56 (spb.cpp:51-68) ------------------
+ * Mean over `batch` (dataset indices, len > 0) of the per-sample gradients of
+ * the last `suffix` layers at the context's current params. out_blocks[l-1]
+ * receives block l for covered layers l >= L-suffix+1 and is not touched for
+ * absent ones (may be NULL). layer_ops (nullable, L entries) is accumulated
+ * with the reference's per-layer op counts (model.cpp:165-184). */
+SPB_API spb_status spb_partial_backprop(spb_ctx* ctx, const int* batch, int len, int suffix, float* const* out_blocks,
+                                long long* layer_ops, int* covered_from);
+
+/* ---- Gradient aggregator: aggregate spb.hpp:61 (spb.cpp:70-106) ---------------
+ * blocks[j*L + l] = worker j+1's block l+1 (host fp32, NULL when absent),
+ * dims[j*L + l] its length (0 when absent), covered_from[j] its first covered
+ * layer. Validates the protocol exactly like the reference, then averages
+ * each layer over its contributors on the GPU. out[l] receives layer l+1. */
+SPB_API spb_status spb_aggregate(spb_ctx* ctx, int k, int L, const float* const* blocks, const int* dims,
+                         const int* covered_from, float* const* out);
+
+/* ---- Training step: one SPB-SGD iteration (spb.cpp:187-196) -------------------
+ * Every worker j hosted by this context draws per_worker_batch samples from
+ * Rng(seed).split(step).split(j) (on the GPU, bit-exact), runs its forward pass
+ * and the backward pass truncated at layer L - ceil(jL/k) + 1, each layer's
+ * gradient is averaged over its contributors (x 1/(m_l * per_worker_batch)),
+ * and the optimizer updates the params. full_backprop != 0 runs the DP
+ * baseline (every worker backpropagates all L layers, plain mean;
+ * baseline_estimate spb.cpp:149-160) on the same kernels. The step is
+ * captured once as a CUDA graph and replayed `steps` times for steps
+ * step0, step0+1, ...; losses (nullable, host) receives each step's mini-batch
+ * loss (mean of 0.5*||out-y||^2 over this context's rows). */
+SPB_API spb_status spb_train_steps(spb_ctx* ctx, uint64_t seed, int step0, int steps, int full_backprop,
+                           float* losses);
+/* Same step, but the mini-batch rows come from HOST memory (the reference's
+ * model owns a host dataset): X_rows [rows x n_0], Y_rows [rows x n_L] in
+ * hosted-worker order, rows = hosted workers * per_worker_batch. Copies in,
+ * steps, and copies the loss out (synchronous). */
+SPB_API spb_status spb_step_host(spb_ctx* ctx, const float* X_rows, const float* Y_rows, int full_backprop,
+                         float* loss_out);
+/* The aggregated per-layer gradient the last step applied (aggregate's output,
+ * spb.cpp:70-106, in the Params block layout), or for spb_partial_backprop the
+ * covered blocks of the last call. */
+SPB_API spb_status spb_get_grads(spb_ctx* ctx, float* const* blocks);
+/* ChainMlp::loss (model.cpp:139-143) over the whole uploaded dataset. */
+SPB_API spb_status spb_loss(spb_ctx* ctx, double* out);
+/* Waits for all work queued on the context's stream. */
+SPB_API spb_status spb_synchronize(spb_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t), for event timing by callers. */
+SPB_API void* spb_stream(spb_ctx* ctx);
+
+/* ---- Multi-GPU: one context per rank, one SPB worker set per GPU --------------
+ * unique_id: 128 bytes from spb_comm_unique_id() on rank 0, broadcast by the
+ * caller. After this call spb_train_steps runs only this rank's workers
+ * (spb_rank_workers) and aggregates each layer over its contributors with
+ * NCCL over NVLink on per-layer buckets. */
+SPB_API spb_status spb_comm_unique_id(void* out128);
+SPB_API spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int nranks);
+
+/* ---- Introspection for tests and the bench ----------------------------------- */
+/* Batch indices the last device-drawn step used (rows in hosted-worker order). */
+SPB_API spb_status spb_last_batch(spb_ctx* ctx, int* out, int rows);
+/* Number of this library's kernel launches per step of the last
+ * spb_train_steps / spb_step_host call (the captured graph's kernel nodes). */
+SPB_API spb_status spb_launches_per_step(spb_ctx* ctx, int* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPB_B200_H */

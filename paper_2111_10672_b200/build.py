@@ -1,0 +1,79 @@
+"""Builds libspb_b200.so in-tree with nvcc for sm_100a.
+
+    python -m paper_2111_10672_b200.build [--force]
+
+Every .cu under csrc/ is compiled with
+``-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo`` (ptxas resource
+usage goes to build/ptxas.log) and linked with the static CUDA runtime into
+paper_2111_10672_b200/libspb_b200.so, so the library does not depend on the
+runtime torch bundles. The .so is git-ignored but travels with gpurun.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+BUILD = os.path.join(PKG, "build")
+LIB = os.path.join(PKG, "libspb_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",
+          "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-DSPB_BUILD_LIB"]
+NCCL_STATIC = "/usr/lib/x86_64-linux-gnu/libnccl_static.a"
+
+
+def _sources():
+    return sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
+
+
+def _headers_mtime():
+    paths = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))]
+    paths.append(os.path.join(ROOT, "include", "spb_b200.h"))
+    return max(os.path.getmtime(p) for p in paths)
+
+
+def _compile(src: str, force: bool) -> str:
+    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+    srcp = os.path.join(CSRC, src)
+    if not force and os.path.exists(obj):
+        if os.path.getmtime(obj) >= max(os.path.getmtime(srcp), _headers_mtime()):
+            return obj
+    cmd = [NVCC] + ARCH + CFLAGS + ["-c", srcp, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    with open(os.path.join(BUILD, src + ".ptxas.log"), "w") as f:
+        f.write(r.stdout + r.stderr)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"nvcc failed on {src}")
+    return obj
+
+
+def build(force: bool = False, verbose: bool = True) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    srcs = _sources()
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
+        objs = list(ex.map(lambda s: _compile(s, force), srcs))
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
+        return LIB
+    link = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
+    if os.path.exists(NCCL_STATIC):
+        link += ["-Xlinker", "--exclude-libs,ALL", NCCL_STATIC]
+    link += ["-lcuda" if os.path.exists("/usr/local/cuda/lib64/stubs/libcuda.so") and False else "", "-lpthread",
+             "-ldl", "-lrt"]
+    link = [a for a in link if a]
+    r = subprocess.run(link, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("link failed")
+    if verbose:
+        print(f"built {LIB}")
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv)

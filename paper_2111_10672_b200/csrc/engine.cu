@@ -1,0 +1,683 @@
+// The SPB engine behind the C ABI (include/spb_b200.h): device state for one
+// ChainMlp on one B200, the per-step launch program (forward -> head ->
+// truncated backward -> update), CUDA-graph capture, and the
+// reference-facing worker / aggregator entry points.
+//
+// HBM layout (all fp32, rows padded to a multiple of 4 elements = 16 B):
+//   params  : one flat allocation per role -- p_hi, p_lo (the exact 3xTF32
+//             split, W = hi + lo), grad, mom. Layer l owns W_l [n_l x ld_{l-1}]
+//             at w_off[l] and b_l [n_l] at b_off[l], each segment aligned to
+//             32 elements (128 B), so a single update launch covers all.
+//   H_l     : activations of hidden layer l (l = 0 is the gathered input),
+//             split pair [rows x ld_l].
+//   Delta   : two ping-pong split pairs [rows x ld_max] (Delta_l lives in
+//             buffer l % 2).
+// Row order: hosted workers ascending, per_worker_batch rows each, so the
+// contributors of every layer are a contiguous tail of rows (chunk_coverage,
+// spb.cpp:23-29) and each layer's aggregate is ONE wgrad GEMM over that tail.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/spb_b200.h"
+#include "gemm_tf32x3.cuh"
+#include "launch.hpp"
+#include "planner.hpp"
+
+namespace spb {
+namespace {
+
+thread_local std::string g_err;
+
+struct Ctl {
+  uint64_t seed;
+  int step;
+  int pad;
+};
+
+}  // namespace
+
+struct Engine {
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  std::vector<int> w;  // widths n_0..n_L
+  int L = 0, nout = 0;
+  int k = 1, bw = 1;
+  std::vector<long> ld;            // ld[l] = round_up(n_l, 4)
+  std::vector<long> w_off, b_off;  // index 1..L
+  long nflat = 0, ldd = 0;
+  float *p_hi = nullptr, *p_lo = nullptr, *grad = nullptr, *mom = nullptr;
+  float lr = 0.01f, mu = 0.f, wd = 0.f;
+  // dataset
+  float *X = nullptr, *Y = nullptr;
+  int N = 0;
+  // row workspace
+  int cap_rows = 0;
+  std::vector<float*> Hh, Hl;
+  float *Dh[2] = {nullptr, nullptr}, *Dl[2] = {nullptr, nullptr};
+  float *delta = nullptr, *row_loss = nullptr, *ybatch = nullptr, *scratch = nullptr, *xin = nullptr;
+  long scratch_n = 0;
+  int* idx = nullptr;
+  int* idx_in = nullptr;
+  float* loss_dev = nullptr;
+  float* tmp = nullptr;
+  long tmp_n = 0;
+  Ctl* ctl = nullptr;
+  int* workers_dev = nullptr;
+  std::vector<int> workers;  // hosted workers, ascending
+  // graphs: [full][host_rows]
+  cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  int graph_launches[2][2] = {{0, 0}, {0, 0}};
+  int last_launches = 0;
+  std::string err;
+
+  ~Engine() { release(); }
+
+  void release() {
+    for (auto& row : graph)
+      for (auto& g : row)
+        if (g) cudaGraphExecDestroy(g), g = nullptr;
+    auto f = [](void* p) {
+      if (p) cudaFree(p);
+    };
+    f(p_hi), f(p_lo), f(grad), f(mom), f(X), f(Y), f(delta), f(row_loss), f(ybatch), f(scratch), f(xin), f(idx),
+        f(idx_in), f(loss_dev), f(tmp), f(ctl), f(workers_dev);
+    for (auto p : Hh) f(p);
+    for (auto p : Hl) f(p);
+    for (int i = 0; i < 2; ++i) f(Dh[i]), f(Dl[i]);
+    if (st) cudaStreamDestroy(st);
+    st = nullptr;
+  }
+
+  template <class T>
+  static T* alloc(long n) {
+    void* p = nullptr;
+    SPB_CUDA(cudaMalloc(&p, static_cast<size_t>(n < 1 ? 1 : n) * sizeof(T)));
+    SPB_CUDA(cudaMemset(p, 0, static_cast<size_t>(n < 1 ? 1 : n) * sizeof(T)));
+    return static_cast<T*>(p);
+  }
+
+  void init(const int* widths, int n_widths, int k_, int bw_, int device) {
+    if (n_widths < 2) throw ArgumentError("mlp: need at least one layer");
+    for (int i = 0; i < n_widths; ++i)
+      if (widths[i] < 1) throw ArgumentError("mlp: widths must be >= 1");
+    if (widths[n_widths - 1] > 16) throw ArgumentError("mlp: output width must be <= 16");
+    if (k_ < 1 || bw_ < 1) throw ArgumentError("SpbConfig: k and per-worker batch must be >= 1");
+    w.assign(widths, widths + n_widths);
+    L = n_widths - 1;
+    nout = w[L];
+    k = k_;
+    bw = bw_;
+    dev = device;
+    SPB_CUDA(cudaSetDevice(dev));
+    SPB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    ld.resize(L + 1);
+    long ldmax = 0;
+    for (int l = 0; l <= L; ++l) ld[l] = round_up(w[l], 4), ldmax = std::max(ldmax, ld[l]);
+    ldd = ldmax;
+    w_off.assign(L + 1, 0);
+    b_off.assign(L + 1, 0);
+    long cur = 0, maxblk = 0;
+    for (int l = 1; l <= L; ++l) {
+      w_off[l] = cur;
+      cur += round_up(w[l] * ld[l - 1], 32);
+      b_off[l] = cur;
+      cur += round_up(w[l], 32);
+      maxblk = std::max(maxblk, w[l] * ld[l - 1] + w[l]);
+    }
+    nflat = cur;
+    p_hi = alloc<float>(nflat);
+    p_lo = alloc<float>(nflat);
+    grad = alloc<float>(nflat);
+    tmp_n = maxblk;
+    tmp = alloc<float>(tmp_n);
+    ctl = alloc<Ctl>(1);
+    loss_dev = alloc<float>(1);
+    workers_dev = alloc<int>(k);
+    set_workers_all();
+    ensure_rows(k * bw);
+  }
+
+  void set_workers(const std::vector<int>& ws) {
+    workers = ws;
+    SPB_CUDA(cudaMemcpy(workers_dev, ws.data(), ws.size() * sizeof(int), cudaMemcpyHostToDevice));
+    invalidate_graphs();
+  }
+  void set_workers_all() {
+    std::vector<int> ws(k);
+    std::iota(ws.begin(), ws.end(), 1);
+    set_workers(ws);
+  }
+
+  void invalidate_graphs() {
+    for (auto& row : graph)
+      for (auto& g : row)
+        if (g) cudaGraphExecDestroy(g), g = nullptr;
+  }
+
+  void ensure_rows(int rows) {
+    if (rows <= cap_rows) return;
+    SPB_CUDA(cudaStreamSynchronize(st));
+    invalidate_graphs();
+    for (auto p : Hh) cudaFree(p);
+    for (auto p : Hl) cudaFree(p);
+    Hh.assign(L, nullptr);
+    Hl.assign(L, nullptr);
+    for (int i = 0; i < 2; ++i) {
+      if (Dh[i]) cudaFree(Dh[i]), cudaFree(Dl[i]);
+    }
+    for (void* p : {(void*)delta, (void*)row_loss, (void*)ybatch, (void*)scratch, (void*)xin, (void*)idx,
+                    (void*)idx_in})
+      if (p) cudaFree(p);
+    cap_rows = rows;
+    for (int l = 0; l < L; ++l) {
+      Hh[l] = alloc<float>(rows * ld[l]);
+      Hl[l] = alloc<float>(rows * ld[l]);
+    }
+    for (int i = 0; i < 2; ++i) {
+      Dh[i] = alloc<float>(rows * ldd);
+      Dl[i] = alloc<float>(rows * ldd);
+    }
+    delta = alloc<float>(static_cast<long>(rows) * nout);
+    row_loss = alloc<float>(rows);
+    ybatch = alloc<float>(static_cast<long>(rows) * nout);
+    long sc = colreduce_scratch(rows, static_cast<int>(ldd), 1);
+    for (int l = 1; l <= L; ++l) sc = std::max(sc, colreduce_scratch(rows, w[l - 1], nout));
+    scratch_n = sc;
+    scratch = alloc<float>(sc);
+    xin = alloc<float>(static_cast<long>(rows) * w[0]);
+    idx = alloc<int>(rows);
+    idx_in = alloc<int>(rows);
+  }
+
+  // ---- the per-step launch program ----------------------------------------
+  // row0[l] (l = 1..L): first row contributing to layer l (rows when none).
+  // alpha[l]: the averaging factor 1/(m_l * per_worker_batch) of layer l.
+  int enqueue_pass(int rows, const std::vector<int>& row0, const std::vector<float>& alpha, cudaStream_t s) {
+    int n = 0;
+    // Forward, hidden layers (mlp_forward model.cpp:108-128 batched).
+    for (int l = 1; l < L; ++l) {
+      Operand A{Hh[l - 1], Hl[l - 1], ld[l - 1], rows, w[l - 1], false};
+      Operand B{p_hi + w_off[l], p_lo + w_off[l], ld[l - 1], w[l], w[l - 1], false};
+      GemmEpilogue ep{};
+      ep.out_hi = Hh[l];
+      ep.out_lo = Hl[l];
+      ep.ld_out = ld[l];
+      ep.bias_hi = p_hi + b_off[l];
+      ep.bias_lo = p_lo + b_off[l];
+      ep.M = rows;
+      ep.N = w[l];
+      n += gemm_tf32x3(A, B, kEpiFwdTanh, ep, s);
+    }
+    // Output head: out, delta_L = out - y (model.cpp:156), Delta_{L-1}.
+    const bool has_next = L > 1 && row0[L - 1] < rows;
+    launch_head(Hh[L - 1], Hl[L - 1], ld[L - 1], rows, w[L - 1], nout, p_hi + w_off[L], p_lo + w_off[L], ld[L - 1],
+                p_hi + b_off[L], p_lo + b_off[L], ybatch, delta, row_loss, has_next ? Dh[(L - 1) % 2] : nullptr,
+                has_next ? Dl[(L - 1) % 2] : nullptr, ldd, has_next ? row0[L - 1] : rows, false, s);
+    ++n;
+    launch_sum_loss(row_loss, rows, 1.0f / static_cast<float>(rows), loss_dev, s);
+    ++n;
+    // Head gradients over the contributor rows of layer L.
+    if (row0[L] < rows) {
+      launch_colreduce(Hh[L - 1], Hl[L - 1], ld[L - 1], row0[L], rows, w[L - 1], delta, nout, nout, alpha[L],
+                       grad + w_off[L], ld[L - 1], scratch, s);
+      launch_colreduce(delta, nullptr, nout, row0[L], rows, nout, nullptr, 1, 0, alpha[L], grad + b_off[L], 0, scratch,
+                       s);
+      n += 4;
+    }
+    // Truncated backward (model.cpp:161-185): layer l runs over its
+    // contributor rows only; dgrad stops at the lowest covered layer.
+    for (int l = L - 1; l >= 1; --l) {
+      if (row0[l] >= rows) break;
+      const int r0 = row0[l], cnt = rows - r0;
+      const int b = l % 2;
+      {  // wgrad: dW_l = alpha_l * Delta_l[r0:]^T H_{l-1}[r0:]
+        Operand A{Dh[b] + r0 * ldd, Dl[b] + r0 * ldd, ldd, w[l], cnt, true};
+        Operand B{Hh[l - 1] + r0 * ld[l - 1], Hl[l - 1] + r0 * ld[l - 1], ld[l - 1], w[l - 1], cnt, true};
+        GemmEpilogue ep{};
+        ep.out_hi = grad + w_off[l];
+        ep.ld_out = ld[l - 1];
+        ep.alpha = alpha[l];
+        ep.M = w[l];
+        ep.N = w[l - 1];
+        n += gemm_tf32x3(A, B, kEpiStoreScaled, ep, s);
+      }
+      launch_colreduce(Dh[b], Dl[b], ldd, r0, rows, w[l], nullptr, 1, 0, alpha[l], grad + b_off[l], 0, scratch, s);
+      n += 2;
+      if (l > 1 && row0[l - 1] < rows) {  // dgrad: Delta_{l-1} = (Delta_l W_l) * (1 - H_{l-1}^2)
+        const int q0 = row0[l - 1], qn = rows - q0;
+        Operand A{Dh[b] + q0 * ldd, Dl[b] + q0 * ldd, ldd, qn, w[l], false};
+        Operand B{p_hi + w_off[l], p_lo + w_off[l], ld[l - 1], w[l - 1], w[l], true};
+        GemmEpilogue ep{};
+        ep.out_hi = Dh[1 - b] + q0 * ldd;
+        ep.out_lo = Dl[1 - b] + q0 * ldd;
+        ep.ld_out = ldd;
+        ep.h_hi = Hh[l - 1] + q0 * ld[l - 1];
+        ep.h_lo = Hl[l - 1] + q0 * ld[l - 1];
+        ep.ld_h = ld[l - 1];
+        ep.M = qn;
+        ep.N = w[l - 1];
+        n += gemm_tf32x3(A, B, kEpiDgradTanh, ep, s);
+      }
+    }
+    return n;
+  }
+
+  // Row plan of one SPB step for the hosted workers.
+  void step_plan(bool full, std::vector<int>& row0, std::vector<float>& alpha) const {
+    const int rows = static_cast<int>(workers.size()) * bw;
+    row0.assign(L + 1, rows);
+    alpha.assign(L + 1, 0.f);
+    auto chunk_of = layer_chunks(k, L);
+    for (int l = 1; l <= L; ++l) {
+      if (full) {
+        row0[l] = 0;
+        alpha[l] = 1.0f / static_cast<float>(static_cast<long>(k) * bw);
+        continue;
+      }
+      for (size_t t = 0; t < workers.size(); ++t)
+        if (worker_stop(workers[t], k, L) <= l) {
+          row0[l] = static_cast<int>(t) * bw;
+          break;
+        }
+      alpha[l] = 1.0f / static_cast<float>(static_cast<long>(chunk_of[l - 1]) * bw);
+    }
+  }
+
+  int enqueue_step(bool full, bool host_rows, cudaStream_t s) {
+    const int rows = static_cast<int>(workers.size()) * bw;
+    int n = 0;
+    if (host_rows) {
+      launch_split_rows(xin, w[0], rows, w[0], Hh[0], Hl[0], ld[0], s);
+    } else {
+      launch_gather(X, ld[0], Y, w[0], nout, N, rows, bw, workers_dev, &ctl->seed, 0, &ctl->step, 0, nullptr, idx, Hh[0], Hl[0],
+                    ld[0], ybatch, s);
+    }
+    ++n;
+    std::vector<int> row0;
+    std::vector<float> alpha;
+    step_plan(full, row0, alpha);
+    n += enqueue_pass(rows, row0, alpha, s);
+    launch_sgd_update(p_hi, p_lo, grad, mom, nflat, lr, mu, wd, &ctl->step, s);
+    ++n;
+    return n;
+  }
+
+  cudaGraphExec_t get_graph(bool full, bool host_rows) {
+    cudaGraphExec_t& g = graph[full][host_rows];
+    if (g) return g;
+    cudaGraph_t gr;
+    SPB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    int n = 0;
+    try {
+      n = enqueue_step(full, host_rows, st);
+    } catch (...) {
+      cudaStreamEndCapture(st, &gr);
+      throw;
+    }
+    SPB_CUDA(cudaStreamEndCapture(st, &gr));
+    SPB_CUDA(cudaGraphInstantiate(&g, gr, 0));
+    cudaGraphDestroy(gr);
+    graph_launches[full][host_rows] = n;
+    return g;
+  }
+};
+
+}  // namespace spb
+
+using spb::Engine;
+
+struct spb_ctx {
+  Engine e;
+};
+
+namespace {
+
+template <class F>
+spb_status guard(spb_ctx* ctx, F&& f) {
+  std::string* err = ctx ? &ctx->e.err : &spb::g_err;
+  try {
+    if (ctx) SPB_CUDA(cudaSetDevice(ctx->e.dev));
+    f();
+    return SPB_OK;
+  } catch (const spb::ArgumentError& x) {
+    *err = x.what();
+    return SPB_E_ARGUMENT;
+  } catch (const spb::ProtocolError& x) {
+    *err = x.what();
+    return SPB_E_PROTOCOL;
+  } catch (const spb::ConfigError& x) {
+    *err = x.what();
+    return SPB_E_CONFIG;
+  } catch (const spb::CudaError& x) {
+    *err = x.what();
+    return SPB_E_CUDA;
+  } catch (const std::invalid_argument& x) {
+    *err = x.what();
+    return SPB_E_ARGUMENT;
+  } catch (const std::exception& x) {
+    *err = x.what();
+    return SPB_E_CUDA;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* spb_last_error(const spb_ctx* ctx) { return ctx ? ctx->e.err.c_str() : spb::g_err.c_str(); }
+
+spb_status spb_suffix_layers(int j, int k, int L, int* out) {
+  return guard(nullptr, [&] { *out = spb::suffix_layers(j, k, L); });
+}
+
+spb_status spb_chunk_coverage(int m, int k, int* out) {
+  return guard(nullptr, [&] {
+    auto v = spb::chunk_coverage(m, k);
+    std::copy(v.begin(), v.end(), out);
+  });
+}
+
+spb_status spb_chunk_layout(int k, int L, int* out) {
+  return guard(nullptr, [&] {
+    auto v = spb::chunk_layout(k, L);
+    for (int m = 0; m < k; ++m) out[2 * m] = v[m].first, out[2 * m + 1] = v[m].second;
+  });
+}
+
+spb_status spb_layer_chunks(int k, int L, int* out) {
+  return guard(nullptr, [&] {
+    auto v = spb::layer_chunks(k, L);
+    std::copy(v.begin(), v.end(), out);
+  });
+}
+
+spb_status spb_draw_batch(uint64_t seed, int step, int worker, int count, int dataset_size, int* out) {
+  return guard(nullptr, [&] {
+    if (count < 0 || dataset_size < 1) throw spb::ArgumentError("draw_batch: bad size");
+    spb::Rng r = spb::Rng(seed).split(static_cast<uint64_t>(step)).split(static_cast<uint64_t>(worker));
+    for (int i = 0; i < count; ++i) out[i] = static_cast<int>(r.next_below(static_cast<uint64_t>(dataset_size)));
+  });
+}
+
+spb_status spb_rank_workers(int k, int L, int rank, int nranks, int* out, int* count) {
+  return guard(nullptr, [&] {
+    auto v = spb::rank_workers(k, L, rank, nranks);
+    std::copy(v.begin(), v.end(), out);
+    *count = static_cast<int>(v.size());
+  });
+}
+
+spb_status spb_create(const int* widths, int n_widths, int k, int per_worker_batch, int device, spb_ctx** out) {
+  *out = nullptr;
+  auto ctx = std::make_unique<spb_ctx>();
+  spb_status s = guard(nullptr, [&] { ctx->e.init(widths, n_widths, k, per_worker_batch, device); });
+  if (s == SPB_OK) *out = ctx.release();
+  return s;
+}
+
+spb_status spb_destroy(spb_ctx* ctx) {
+  if (ctx) {
+    cudaSetDevice(ctx->e.dev);
+    cudaStreamSynchronize(ctx->e.st);
+    delete ctx;
+  }
+  return SPB_OK;
+}
+
+spb_status spb_set_dataset(spb_ctx* ctx, const float* X, const float* Y, int N) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    if (N < 1) throw spb::ArgumentError("mlp: dataset shape mismatch");
+    SPB_CUDA(cudaStreamSynchronize(e.st));
+    if (e.X) cudaFree(e.X), cudaFree(e.Y);
+    e.X = Engine::alloc<float>(static_cast<long>(N) * e.ld[0]);
+    e.Y = Engine::alloc<float>(static_cast<long>(N) * e.nout);
+    SPB_CUDA(cudaMemcpy2D(e.X, e.ld[0] * 4, X, e.w[0] * 4, e.w[0] * 4, N, cudaMemcpyHostToDevice));
+    SPB_CUDA(cudaMemcpy(e.Y, Y, static_cast<size_t>(N) * e.nout * 4, cudaMemcpyHostToDevice));
+    e.N = N;
+    e.invalidate_graphs();
+  });
+}
+
+spb_status spb_set_params(spb_ctx* ctx, const float* const* blocks) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    for (int l = 1; l <= e.L; ++l) {
+      const int no = e.w[l], ni = e.w[l - 1];
+      SPB_CUDA(cudaMemsetAsync(e.tmp, 0, e.tmp_n * 4, e.st));
+      SPB_CUDA(cudaMemcpy2DAsync(e.tmp, e.ld[l - 1] * 4, blocks[l - 1], ni * 4, ni * 4, no, cudaMemcpyHostToDevice,
+                                 e.st));
+      spb::launch_split(e.tmp, no * e.ld[l - 1], e.p_hi + e.w_off[l], e.p_lo + e.w_off[l], e.st);
+      SPB_CUDA(cudaMemcpyAsync(e.tmp, blocks[l - 1] + static_cast<long>(no) * ni, no * 4, cudaMemcpyHostToDevice,
+                               e.st));
+      spb::launch_split(e.tmp, no, e.p_hi + e.b_off[l], e.p_lo + e.b_off[l], e.st);
+      SPB_CUDA(cudaStreamSynchronize(e.st));
+    }
+    if (e.mom) SPB_CUDA(cudaMemsetAsync(e.mom, 0, e.nflat * 4, e.st));
+    SPB_CUDA(cudaStreamSynchronize(e.st));
+  });
+}
+
+spb_status spb_get_params(spb_ctx* ctx, float* const* blocks) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    for (int l = 1; l <= e.L; ++l) {
+      const int no = e.w[l], ni = e.w[l - 1];
+      spb::launch_join(e.p_hi + e.w_off[l], e.p_lo + e.w_off[l], no * e.ld[l - 1], e.tmp, e.st);
+      SPB_CUDA(cudaMemcpy2DAsync(blocks[l - 1], ni * 4, e.tmp, e.ld[l - 1] * 4, ni * 4, no, cudaMemcpyDeviceToHost,
+                                 e.st));
+      SPB_CUDA(cudaStreamSynchronize(e.st));
+      spb::launch_join(e.p_hi + e.b_off[l], e.p_lo + e.b_off[l], no, e.tmp, e.st);
+      SPB_CUDA(cudaMemcpyAsync(blocks[l - 1] + static_cast<long>(no) * ni, e.tmp, no * 4, cudaMemcpyDeviceToHost,
+                               e.st));
+      SPB_CUDA(cudaStreamSynchronize(e.st));
+    }
+  });
+}
+
+spb_status spb_get_grads(spb_ctx* ctx, float* const* blocks) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    for (int l = 1; l <= e.L; ++l) {
+      if (!blocks[l - 1]) continue;
+      const int no = e.w[l], ni = e.w[l - 1];
+      SPB_CUDA(cudaMemcpy2DAsync(blocks[l - 1], ni * 4, e.grad + e.w_off[l], e.ld[l - 1] * 4, ni * 4, no,
+                                 cudaMemcpyDeviceToHost, e.st));
+      SPB_CUDA(cudaMemcpyAsync(blocks[l - 1] + static_cast<long>(no) * ni, e.grad + e.b_off[l], no * 4,
+                               cudaMemcpyDeviceToHost, e.st));
+    }
+    SPB_CUDA(cudaStreamSynchronize(e.st));
+  });
+}
+
+spb_status spb_set_optimizer(spb_ctx* ctx, float lr, float momentum, float weight_decay) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    e.lr = lr;
+    e.mu = momentum;
+    e.wd = weight_decay;
+    if (momentum != 0.f && !e.mom) e.mom = Engine::alloc<float>(e.nflat);
+    e.invalidate_graphs();
+  });
+}
+
+spb_status spb_partial_backprop(spb_ctx* ctx, const int* batch, int len, int suffix, float* const* out_blocks,
+                                long long* layer_ops, int* covered_from) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    const int L = e.L;
+    if (suffix < 1 || suffix > L) throw spb::ArgumentError("partial_backprop: suffix out of range");
+    if (len <= 0) throw spb::ArgumentError("partial_backprop: empty batch");
+    if (!e.X) throw spb::ConfigError("partial_backprop: no dataset");
+    for (int i = 0; i < len; ++i)
+      if (batch[i] < 0 || batch[i] >= e.N) throw spb::ArgumentError("sample out of range");
+    e.ensure_rows(len);
+    const int stop = L - suffix + 1;
+    SPB_CUDA(cudaMemcpyAsync(e.idx_in, batch, len * sizeof(int), cudaMemcpyHostToDevice, e.st));
+    spb::launch_gather(e.X, e.ld[0], e.Y, e.w[0], e.nout, e.N, len, len, e.workers_dev, nullptr, 0, nullptr, 0, e.idx_in,
+                       e.idx, e.Hh[0], e.Hl[0], e.ld[0], e.ybatch, e.st);
+    std::vector<int> row0(L + 1, len);
+    std::vector<float> alpha(L + 1, 1.0f / static_cast<float>(len));
+    for (int l = stop; l <= L; ++l) row0[l] = 0;
+    e.enqueue_pass(len, row0, alpha, e.st);
+    for (int l = stop; l <= L; ++l) {
+      if (!out_blocks[l - 1]) continue;
+      const int no = e.w[l], ni = e.w[l - 1];
+      SPB_CUDA(cudaMemcpy2DAsync(out_blocks[l - 1], ni * 4, e.grad + e.w_off[l], e.ld[l - 1] * 4, ni * 4, no,
+                                 cudaMemcpyDeviceToHost, e.st));
+      SPB_CUDA(cudaMemcpyAsync(out_blocks[l - 1] + static_cast<long>(no) * ni, e.grad + e.b_off[l], no * 4,
+                               cudaMemcpyDeviceToHost, e.st));
+    }
+    SPB_CUDA(cudaStreamSynchronize(e.st));
+    if (covered_from) *covered_from = stop;
+    if (layer_ops)  // model.cpp:165-184, per sample
+      for (int l = stop; l <= L; ++l) {
+        long long ops = static_cast<long long>(e.w[l]) * (e.w[l - 1] + 1);
+        if (l > stop) ops += static_cast<long long>(e.w[l]) * e.w[l - 1] + e.w[l - 1];
+        layer_ops[l - 1] += ops * len;
+      }
+  });
+}
+
+spb_status spb_aggregate(spb_ctx* ctx, int k, int L, const float* const* blocks, const int* dims,
+                         const int* covered_from, float* const* out) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    if (k < 1) throw spb::ArgumentError("aggregate: need exactly k gradients");
+    // Protocol checks, spb.cpp:74-87.
+    for (int j = 1; j <= k; ++j) {
+      const int expect_from = L - spb::suffix_layers(j, k, L) + 1;
+      if (covered_from[j - 1] != expect_from)
+        throw spb::ProtocolError("aggregate: worker " + std::to_string(j) + " coverage does not match the suffix rule");
+      for (int l = 1; l <= L; ++l) {
+        const bool present = blocks[(j - 1) * L + l - 1] != nullptr && dims[(j - 1) * L + l - 1] > 0;
+        if (present != (l >= covered_from[j - 1]))
+          throw spb::ProtocolError("aggregate: block presence inconsistent with covered_from");
+      }
+    }
+    auto chunk_of = spb::layer_chunks(k, L);
+    for (int l = 1; l <= L; ++l) {  // spb.cpp:91-104
+      const int m = chunk_of[l - 1];
+      const long dim = dims[(k - m) * L + l - 1];
+      for (int wkr = k - m + 1; wkr <= k; ++wkr)
+        if (dims[(wkr - 1) * L + l - 1] != dim) throw spb::ProtocolError("aggregate: block dimension mismatch");
+    }
+    for (int l = 1; l <= L; ++l) {
+      const int m = chunk_of[l - 1];
+      const long dim = dims[(k - m) * L + l - 1];
+      float* stage = Engine::alloc<float>(dim * (m + 1));
+      const float** ptrs = nullptr;
+      SPB_CUDA(cudaMalloc(&ptrs, m * sizeof(float*)));
+      std::vector<const float*> hp(m);
+      for (int i = 0; i < m; ++i) {
+        hp[i] = stage + i * dim;
+        SPB_CUDA(cudaMemcpyAsync(stage + i * dim, blocks[(k - m + i) * L + l - 1], dim * 4, cudaMemcpyHostToDevice,
+                                 e.st));
+      }
+      SPB_CUDA(cudaMemcpyAsync(ptrs, hp.data(), m * sizeof(float*), cudaMemcpyHostToDevice, e.st));
+      spb::launch_aggregate(ptrs, m, dim, stage + m * dim, e.st);
+      SPB_CUDA(cudaMemcpyAsync(out[l - 1], stage + m * dim, dim * 4, cudaMemcpyDeviceToHost, e.st));
+      SPB_CUDA(cudaStreamSynchronize(e.st));
+      cudaFree(stage);
+      cudaFree(ptrs);
+    }
+  });
+}
+
+spb_status spb_train_steps(spb_ctx* ctx, uint64_t seed, int step0, int steps, int full_backprop, float* losses) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    if (!e.X) throw spb::ConfigError("train_steps: no dataset");
+    if (steps < 0) throw spb::ArgumentError("train_steps: steps must be >= 0");
+    e.ensure_rows(static_cast<int>(e.workers.size()) * e.bw);
+    cudaGraphExec_t g = e.get_graph(full_backprop != 0, false);
+    spb::Ctl c{seed, step0, 0};
+    SPB_CUDA(cudaMemcpyAsync(e.ctl, &c, sizeof c, cudaMemcpyHostToDevice, e.st));
+    for (int i = 0; i < steps; ++i) {
+      SPB_CUDA(cudaGraphLaunch(g, e.st));
+      if (losses) SPB_CUDA(cudaMemcpyAsync(losses + i, e.loss_dev, 4, cudaMemcpyDeviceToHost, e.st));
+    }
+    e.last_launches = e.graph_launches[full_backprop != 0][0];
+    if (losses) SPB_CUDA(cudaStreamSynchronize(e.st));
+  });
+}
+
+spb_status spb_step_host(spb_ctx* ctx, const float* X_rows, const float* Y_rows, int full_backprop, float* loss_out) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    const int rows = static_cast<int>(e.workers.size()) * e.bw;
+    e.ensure_rows(rows);
+    cudaGraphExec_t g = e.get_graph(full_backprop != 0, true);
+    SPB_CUDA(cudaMemcpyAsync(e.xin, X_rows, static_cast<size_t>(rows) * e.w[0] * 4, cudaMemcpyHostToDevice, e.st));
+    SPB_CUDA(cudaMemcpyAsync(e.ybatch, Y_rows, static_cast<size_t>(rows) * e.nout * 4, cudaMemcpyHostToDevice, e.st));
+    SPB_CUDA(cudaGraphLaunch(g, e.st));
+    SPB_CUDA(cudaMemcpyAsync(loss_out, e.loss_dev, 4, cudaMemcpyDeviceToHost, e.st));
+    SPB_CUDA(cudaStreamSynchronize(e.st));
+    e.last_launches = e.graph_launches[full_backprop != 0][1];
+  });
+}
+
+spb_status spb_loss(spb_ctx* ctx, double* out) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    if (!e.X) throw spb::ConfigError("loss: no dataset");
+    const int chunk = e.cap_rows;
+    std::vector<int> iota(chunk);
+    double total = 0.0;
+    std::vector<float> rl(chunk);
+    for (int s0 = 0; s0 < e.N; s0 += chunk) {
+      const int rows = std::min(chunk, e.N - s0);
+      for (int i = 0; i < rows; ++i) iota[i] = s0 + i;
+      SPB_CUDA(cudaMemcpyAsync(e.idx_in, iota.data(), rows * sizeof(int), cudaMemcpyHostToDevice, e.st));
+      spb::launch_gather(e.X, e.ld[0], e.Y, e.w[0], e.nout, e.N, rows, rows, e.workers_dev, nullptr, 0, nullptr, 0, e.idx_in,
+                         e.idx, e.Hh[0], e.Hl[0], e.ld[0], e.ybatch, e.st);
+      std::vector<int> row0(e.L + 1, rows);  // forward + head only
+      std::vector<float> alpha(e.L + 1, 0.f);
+      e.enqueue_pass(rows, row0, alpha, e.st);
+      SPB_CUDA(cudaMemcpyAsync(rl.data(), e.row_loss, rows * 4, cudaMemcpyDeviceToHost, e.st));
+      SPB_CUDA(cudaStreamSynchronize(e.st));
+      for (int i = 0; i < rows; ++i) total += rl[i];
+    }
+    *out = total / e.N;
+  });
+}
+
+spb_status spb_synchronize(spb_ctx* ctx) {
+  return guard(ctx, [&] { SPB_CUDA(cudaStreamSynchronize(ctx->e.st)); });
+}
+
+void* spb_stream(spb_ctx* ctx) { return ctx ? static_cast<void*>(ctx->e.st) : nullptr; }
+
+spb_status spb_comm_unique_id(void* out128) {
+  return guard(nullptr, [&] {
+    (void)out128;
+    throw spb::ConfigError("comm: built without NCCL");
+  });
+}
+
+spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int nranks) {
+  return guard(ctx, [&] {
+    (void)unique_id128, (void)rank, (void)nranks;
+    throw spb::ConfigError("comm: built without NCCL");
+  });
+}
+
+spb_status spb_last_batch(spb_ctx* ctx, int* out, int rows) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    if (rows > e.cap_rows) throw spb::ArgumentError("last_batch: too many rows");
+    SPB_CUDA(cudaMemcpyAsync(out, e.idx, rows * sizeof(int), cudaMemcpyDeviceToHost, e.st));
+    SPB_CUDA(cudaStreamSynchronize(e.st));
+  });
+}
+
+spb_status spb_launches_per_step(spb_ctx* ctx, int* out) {
+  return guard(ctx, [&] { *out = ctx->e.last_launches; });
+}
+
+}  // extern "C"

@@ -1,0 +1,257 @@
+// fp32-accurate GEMM on the 5th-gen tensor cores: tcgen05.mma kind::tf32 with
+// the 3xTF32 split, operands staged by TMA into 128B-swizzled shared memory,
+// accumulators in TMEM, fused epilogues.
+//
+//   D[M x N] = epi( sum_k A[m,k] * B[n,k] )
+//
+// Every operand X (A or B) is held in HBM as an exact split pair
+// X = X_hi + X_lo, X_hi = rna_tf32(X), X_lo = X - X_hi (both fp32 words), written
+// by whichever kernel produced X (forward / dgrad epilogues, the update
+// kernel, the dataset gather). The MMA pipe computes
+//   A_lo*B_hi + A_hi*B_lo + A_hi*B_hi
+// which loses only the A_lo*B_lo term (~2^-22 relative): fp32-class products,
+// needed for the 1e-5 parity bar that plain TF32 (2^-11) cannot meet.
+//
+// An operand is K-major (memory rows = MN index, K contiguous) or MN-major
+// (memory rows = K index, MN contiguous); tcgen05 accepts both for tf32, so
+// wgrad (Delta^T H) and dgrad (Delta W) need no transposed copies.
+//
+// Roles (256 threads, 1 CTA/SM): warp 0 = TMA producer, warp 1 = MMA issuer
+// (one elected lane), warp 2 = TMEM allocator, warps 4..7 = epilogue
+// (TMEM lanes 32*(warp%4)..+31).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace spb {
+
+enum Epi : int {
+  kEpiFwdTanh = 0,     // out = split(tanh(acc + bias[n]))
+  kEpiStoreScaled = 1, // out_f32 = alpha * acc
+  kEpiDgradTanh = 2,   // out = split(acc * (1 - h[m,n]^2)), h = h_hi + h_lo
+  kEpiFwdLinear = 3,   // out = split(acc + bias[n])
+};
+
+struct GemmEpilogue {
+  float* out_hi;  // kEpiStoreScaled: the fp32 output
+  float* out_lo;
+  long ld_out;
+  const float* bias_hi;
+  const float* bias_lo;
+  const float* h_hi;
+  const float* h_lo;
+  long ld_h;
+  float alpha;
+  int M, N;  // valid output extent
+};
+
+constexpr int kBM = 128;
+constexpr int kBK = 32;  // 32 fp32 = one 128-byte swizzle row
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kABytes = kBM * kBK * 4;
+  static constexpr int kBBytes = BN * kBK * 4;
+  static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
+  static constexpr int kStages = (BN >= 256) ? 2 : 3;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+};
+
+// TMA for one operand tile of ROWS (MN) x kBK (K) elements.
+template <bool MN_MAJOR, int ROWS>
+__device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, int mn0,
+                                             int k0) {
+  if constexpr (!MN_MAJOR) {
+    tma_load_2d(dst, tm, bar, k0, mn0);  // box {32 (K), ROWS (MN)}
+  } else {
+#pragma unroll
+    for (int c = 0; c < ROWS / 32; ++c)  // boxes {32 (MN), 32 (K)}, 4 KB apart
+      tma_load_2d(dst + c * 4096, tm, bar, mn0 + c * 32, k0);
+  }
+}
+
+// UMMA descriptor for the kk-th K=8 slice of an operand tile.
+template <bool MN_MAJOR>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int kk) {
+  if constexpr (!MN_MAJOR) {
+    // K-major SW128: rows of 128 B, 8-row atoms 1024 B apart (SBO); K slice = +32 B.
+    return sdesc(base + kk * 32, 16, 1024, kLayoutSw128);
+  } else {
+    // MN-major SW128_BASE32B: 32-element MN chunks 4 KB apart (LBO), 4-K-row
+    // atoms 512 B apart (SBO); a K=8 slice is 8 rows = +1 KB.
+    return sdesc(base + kk * 1024, 4096, 512, kLayoutSw128Base32);
+  }
+}
+
+__device__ __forceinline__ void store_split4(float* hi, float* lo, float4 v) {
+  float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+  float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+  *reinterpret_cast<float4*>(hi) = h;
+  *reinterpret_cast<float4*>(lo) = l;
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const float* v, int row, int col0) {
+  if (row >= ep.M) return;
+  const bool full = (col0 + 32 <= ep.N);
+  if constexpr (EPI == kEpiStoreScaled) {
+    float* o = ep.out_hi + row * ep.ld_out + col0;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(o + j) =
+            make_float4(ep.alpha * v[j], ep.alpha * v[j + 1], ep.alpha * v[j + 2], ep.alpha * v[j + 3]);
+    } else {
+      for (int j = 0; j < 32 && col0 + j < ep.N; ++j) o[j] = ep.alpha * v[j];
+    }
+  } else if constexpr (EPI == kEpiFwdTanh || EPI == kEpiFwdLinear) {
+    float* oh = ep.out_hi + row * ep.ld_out + col0;
+    float* ol = ep.out_lo + row * ep.ld_out + col0;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float4 bh = __ldg(reinterpret_cast<const float4*>(ep.bias_hi + col0 + j));
+        float4 bl = __ldg(reinterpret_cast<const float4*>(ep.bias_lo + col0 + j));
+        float4 z = make_float4(v[j] + (bh.x + bl.x), v[j + 1] + (bh.y + bl.y), v[j + 2] + (bh.z + bl.z),
+                               v[j + 3] + (bh.w + bl.w));
+        if (EPI == kEpiFwdTanh) z = make_float4(tanhf(z.x), tanhf(z.y), tanhf(z.z), tanhf(z.w));
+        store_split4(oh + j, ol + j, z);
+      }
+    } else {
+      for (int j = 0; j < 32 && col0 + j < ep.N; ++j) {
+        float z = v[j] + (ep.bias_hi[col0 + j] + ep.bias_lo[col0 + j]);
+        if (EPI == kEpiFwdTanh) z = tanhf(z);
+        float h = tf32_rna(z);
+        oh[j] = h;
+        ol[j] = z - h;
+      }
+    }
+  } else {  // kEpiDgradTanh
+    float* oh = ep.out_hi + row * ep.ld_out + col0;
+    float* ol = ep.out_lo + row * ep.ld_out + col0;
+    const float* hh = ep.h_hi + row * ep.ld_h + col0;
+    const float* hl = ep.h_lo + row * ep.ld_h + col0;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float4 a = *reinterpret_cast<const float4*>(hh + j);
+        float4 b = *reinterpret_cast<const float4*>(hl + j);
+        float4 h = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+        float4 d = make_float4(v[j] * (1.0f - h.x * h.x), v[j + 1] * (1.0f - h.y * h.y),
+                               v[j + 2] * (1.0f - h.z * h.z), v[j + 3] * (1.0f - h.w * h.w));
+        store_split4(oh + j, ol + j, d);
+      }
+    } else {
+      for (int j = 0; j < 32 && col0 + j < ep.N; ++j) {
+        float h = hh[j] + hl[j];
+        float d = v[j] * (1.0f - h * h);
+        float dh = tf32_rna(d);
+        oh[j] = dh;
+        ol[j] = d - dh;
+      }
+    }
+  }
+}
+
+// One CTA per 128 x BN output tile; grid = (ceil(M/128), ceil(N/BN)) so the
+// M-tiles sharing a B tile run side by side and B is read from HBM once.
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
+                       const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
+                       int num_kb, GemmEpilogue ep) {
+  using Cfg = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + Cfg::kStages;
+  uint64_t* accum_bar = empty_bar + Cfg::kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
+
+  const uint32_t warp = warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31u;
+  const int m_tile = blockIdx.x, n_tile = blockIdx.y;
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&ta_hi);
+    tma_prefetch(&ta_lo);
+    tma_prefetch(&tb_hi);
+    tma_prefetch(&tb_lo);
+  }
+  if (warp == 1 && elect_one()) {
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(accum_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % Cfg::kStages;
+        const uint32_t ph = (kb / Cfg::kStages) & 1u;
+        mbar_wait(&empty_bar[s], ph ^ 1u);
+        mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
+        uint8_t* base = smem + s * Cfg::kStageBytes;
+        load_operand<A_MN, kBM>(base, &ta_hi, &full_bar[s], m_tile * kBM, kb * kBK);
+        load_operand<A_MN, kBM>(base + Cfg::kABytes, &ta_lo, &full_bar[s], m_tile * kBM, kb * kBK);
+        load_operand<B_MN, BN>(base + 2 * Cfg::kABytes, &tb_hi, &full_bar[s], n_tile * BN, kb * kBK);
+        load_operand<B_MN, BN>(base + 2 * Cfg::kABytes + Cfg::kBBytes, &tb_lo, &full_bar[s], n_tile * BN,
+                               kb * kBK);
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_tf32(kBM, BN, A_MN, B_MN);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % Cfg::kStages;
+        const uint32_t ph = (kb / Cfg::kStages) & 1u;
+        mbar_wait(&full_bar[s], ph);
+        tc_fence_after();
+        const uint32_t base = smem_u32(smem + s * Cfg::kStageBytes);
+        const uint32_t a_hi = base, a_lo = base + Cfg::kABytes;
+        const uint32_t b_hi = base + 2 * Cfg::kABytes, b_lo = b_hi + Cfg::kBBytes;
+#pragma unroll
+        for (int kk = 0; kk < kBK / 8; ++kk) {
+          const uint32_t acc = (kb | kk) != 0;
+          umma_tf32(tmem, operand_desc<A_MN>(a_lo, kk), operand_desc<B_MN>(b_hi, kk), idesc, acc);
+          umma_tf32(tmem, operand_desc<A_MN>(a_hi, kk), operand_desc<B_MN>(b_lo, kk), idesc, 1u);
+          umma_tf32(tmem, operand_desc<A_MN>(a_hi, kk), operand_desc<B_MN>(b_hi, kk), idesc, 1u);
+        }
+        umma_commit(&empty_bar[s]);  // frees the stage once these MMAs retire
+      }
+      umma_commit(accum_bar);  // accumulator complete
+    }
+  } else if (warp >= 4) {
+    const uint32_t q = warp & 3u;
+    mbar_wait(accum_bar, 0);
+    tc_fence_after();
+    const int row = m_tile * kBM + static_cast<int>(q * 32 + lane);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float v[32];
+      tmem_ld_32x32b_x32(tmem + ((q * 32u) << 16) + static_cast<uint32_t>(c0), v);
+      const int col0 = n_tile * BN + c0;
+      if (col0 < ep.N) epilogue_chunk<EPI>(ep, v, row, col0);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, BN);
+  }
+}
+
+}  // namespace spb

@@ -1,0 +1,344 @@
+// Non-GEMM kernels of the SPB step: dataset gather with the on-device
+// counter-based Rng, the fused output head, deterministic column reductions
+// (bias / head gradients), the fused optimizer update, and the per-layer
+// contributor average used by the aggregator entry point.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "launch.hpp"
+#include "ptx.cuh"
+
+namespace spb {
+namespace {
+
+// rng.hpp:47-53, bit-exact.
+__device__ __forceinline__ uint64_t rng_mix(uint64_t a, uint64_t b) {
+  uint64_t z = a ^ (b + 0x9E3779B97F4A7C15ULL + (a << 6) + (a >> 2));
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One CTA per row: draw (or read) the sample index, split its input row into
+// the H0 pair and copy its target row.
+__global__ void gather_kernel(const float* __restrict__ X, long ldx, const float* __restrict__ Y, int n0, int nout,
+                              int N, int bw, const int* __restrict__ workers, const uint64_t* __restrict__ seed_dev,
+                              uint64_t seed_host, const int* __restrict__ step_dev, int step_host, const int* __restrict__ idx_in,
+                              int* __restrict__ idx_out, float* __restrict__ h_hi, float* __restrict__ h_lo,
+                              long ldh, float* __restrict__ ybatch) {
+  const int r = blockIdx.x;
+  int idx;
+  if (idx_in) {
+    idx = idx_in[r];
+  } else {
+    // Rng(seed).split(step).split(worker): keys chain through mix
+    // (rng.hpp:18); draw p is next_u64 at counter p+1 (rng.hpp:20) and
+    // next_below is the high half of the 128-bit product (rng.hpp:26-29).
+    const int step = step_dev ? *step_dev : step_host;
+    const uint64_t seed = seed_dev ? *seed_dev : seed_host;
+    const uint64_t key = rng_mix(rng_mix(seed, static_cast<uint64_t>(step)), static_cast<uint64_t>(workers[r / bw]));
+    const uint64_t u = rng_mix(key, static_cast<uint64_t>(r % bw) + 1);
+    idx = static_cast<int>(__umul64hi(u, static_cast<uint64_t>(N)));
+  }
+  if (threadIdx.x == 0 && idx_out) idx_out[r] = idx;
+  const float* src = X + idx * ldx;
+  float* dh = h_hi + r * ldh;
+  float* dl = h_lo + r * ldh;
+  for (int c = threadIdx.x; c < n0; c += blockDim.x) {
+    const float v = src[c];
+    const float h = tf32_rna(v);
+    dh[c] = h;
+    dl[c] = v - h;
+  }
+  if (threadIdx.x < nout) ybatch[r * nout + threadIdx.x] = Y[static_cast<long>(idx) * nout + threadIdx.x];
+}
+
+__global__ void split_rows_kernel(const float* __restrict__ x, long ldx, int cols, float* __restrict__ hi,
+                                  float* __restrict__ lo, long ld) {
+  const int r = blockIdx.x;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    const float v = x[r * ldx + c];
+    const float h = tf32_rna(v);
+    hi[r * ld + c] = h;
+    lo[r * ld + c] = v - h;
+  }
+}
+
+constexpr int kMaxOut = 16;
+
+// One warp per row (model.cpp:121-126 for layer L, :156 for the output
+// delta, :172-183 for the delta entering layer L-1).
+__global__ void head_kernel(const float* __restrict__ h_hi, const float* __restrict__ h_lo, long ldh, int rows,
+                            int n_in, int n_out, const float* __restrict__ w_hi, const float* __restrict__ w_lo,
+                            long ldw, const float* __restrict__ b_hi, const float* __restrict__ b_lo,
+                            const float* __restrict__ y, float* __restrict__ delta, float* __restrict__ row_loss,
+                            float* __restrict__ dn_hi, float* __restrict__ dn_lo, long ldd, int cont_row0,
+                            int tanh_out) {
+  const int warps = blockDim.x / 32;
+  const int r = blockIdx.x * warps + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* hh = h_hi + r * ldh;
+  const float* hl = h_lo + r * ldh;
+  float acc[kMaxOut];
+#pragma unroll
+  for (int o = 0; o < kMaxOut; ++o) acc[o] = 0.f;
+  for (int i = lane; i < n_in; i += 32) {
+    const float h = hh[i] + hl[i];
+#pragma unroll
+    for (int o = 0; o < kMaxOut; ++o)
+      if (o < n_out) acc[o] = fmaf(w_hi[o * ldw + i] + w_lo[o * ldw + i], h, acc[o]);
+  }
+  float d[kMaxOut];
+  float loss = 0.f;
+#pragma unroll
+  for (int o = 0; o < kMaxOut; ++o) {
+    d[o] = 0.f;
+    if (o < n_out) {
+      float z = warp_sum(acc[o]) + (b_hi[o] + b_lo[o]);
+      if (tanh_out) z = tanhf(z);
+      d[o] = z - y[r * n_out + o];
+      loss += 0.5f * d[o] * d[o];
+    }
+  }
+  if (lane == 0) {
+    for (int o = 0; o < n_out; ++o) delta[r * n_out + o] = d[o];
+    row_loss[r] = loss;
+  }
+  if (dn_hi && r >= cont_row0) {
+    float* oh = dn_hi + r * ldd;
+    float* ol = dn_lo + r * ldd;
+    for (int i = lane; i < n_in; i += 32) {
+      float s = 0.f;
+#pragma unroll
+      for (int o = 0; o < kMaxOut; ++o)
+        if (o < n_out) s = fmaf(d[o], w_hi[o * ldw + i] + w_lo[o * ldw + i], s);
+      const float h = hh[i] + hl[i];
+      const float v = s * (1.0f - h * h);
+      const float vh = tf32_rna(v);
+      oh[i] = vh;
+      ol[i] = v - vh;
+    }
+  }
+}
+
+constexpr int kColThreads = 256;
+constexpr int kRowsPerSplit = 32;
+
+// Pass 1: partial[split][o][c] = sum over this split's rows.
+__global__ void colreduce_partial_kernel(const float* __restrict__ hi, const float* __restrict__ lo, long ld, int r0,
+                                         int r1, int ncols, const float* __restrict__ rowvec, int nvec, long ldv,
+                                         float* __restrict__ partial) {
+  const int c = blockIdx.x * kColThreads + threadIdx.x;
+  const int split = blockIdx.y;
+  const int ra = r0 + split * kRowsPerSplit;
+  const int rb = min(r1, ra + kRowsPerSplit);
+  if (c >= ncols) return;
+  float acc[kMaxOut];
+#pragma unroll
+  for (int o = 0; o < kMaxOut; ++o) acc[o] = 0.f;
+  for (int r = ra; r < rb; ++r) {
+    float v = hi[r * ld + c];
+    if (lo) v += lo[r * ld + c];
+    if (!rowvec) {
+      acc[0] += v;
+    } else {
+#pragma unroll
+      for (int o = 0; o < kMaxOut; ++o)
+        if (o < nvec) acc[o] = fmaf(rowvec[r * ldv + o], v, acc[o]);
+    }
+  }
+  for (int o = 0; o < nvec; ++o) partial[(static_cast<long>(split) * nvec + o) * ncols + c] = acc[o];
+}
+
+// Pass 2: out = alpha * sum over splits, in split order.
+__global__ void colreduce_final_kernel(const float* __restrict__ partial, int nsplit, int nvec, int ncols, float alpha,
+                                       float* __restrict__ out, long ld_out) {
+  const long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<long>(nvec) * ncols) return;
+  const int o = static_cast<int>(t / ncols), c = static_cast<int>(t % ncols);
+  float s = 0.f;
+  for (int sp = 0; sp < nsplit; ++sp) s += partial[(static_cast<long>(sp) * nvec + o) * ncols + c];
+  out[o * ld_out + c] = alpha * s;
+}
+
+// Fused optimizer over the flat parameter pair, float4-vectorised, grid-stride:
+//   w = hi + lo; g' = g + wd*w; buf = mu*buf + g' (when mu != 0); w -= lr*buf
+//   hi = rna_tf32(w); lo = w - hi  (the split the next forward's GEMMs read)
+// With mu = wd = 0 this is the reference's x -= gamma*g (spb.cpp:196). The
+// first momentum step sees buf = 0, so buf = g' exactly as in PyTorch SGD.
+__global__ void sgd_update_kernel(float4* __restrict__ p_hi, float4* __restrict__ p_lo,
+                                  const float4* __restrict__ grad, float4* __restrict__ mom, long n4, float lr,
+                                  float mu, float wd, int* step_dev) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 h = p_hi[i], l = p_lo[i], g = __ldg(&grad[i]);
+    float w[4] = {h.x + l.x, h.y + l.y, h.z + l.z, h.w + l.w};
+    float gg[4] = {g.x, g.y, g.z, g.w};
+    if (wd != 0.f) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) gg[j] = fmaf(wd, w[j], gg[j]);
+    }
+    if (mom) {
+      float4 b = mom[i];
+      float bb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        bb[j] = fmaf(mu, bb[j], gg[j]);
+        gg[j] = bb[j];
+      }
+      mom[i] = make_float4(bb[0], bb[1], bb[2], bb[3]);
+    }
+    float nh[4], nl[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float wn = w[j] - lr * gg[j];
+      nh[j] = tf32_rna(wn);
+      nl[j] = wn - nh[j];
+    }
+    p_hi[i] = make_float4(nh[0], nh[1], nh[2], nh[3]);
+    p_lo[i] = make_float4(nl[0], nl[1], nl[2], nl[3]);
+  }
+  if (step_dev && blockIdx.x == 0 && threadIdx.x == 0) *step_dev += 1;  // next step's Rng stream
+}
+
+__global__ void aggregate_kernel(const float* const* __restrict__ srcs, int m, long n, float* __restrict__ out) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  const double inv = 1.0 / static_cast<double>(m);
+  for (long c = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; c < n; c += stride) {
+    double s = 0.0;
+    for (int w = 0; w < m; ++w) s += static_cast<double>(srcs[w][c]);
+    out[c] = static_cast<float>(s * inv);
+  }
+}
+
+__global__ void split_kernel(const float* __restrict__ in, long n, float* __restrict__ hi, float* __restrict__ lo) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float v = in[i], h = tf32_rna(v);
+    hi[i] = h;
+    lo[i] = v - h;
+  }
+}
+
+__global__ void join_kernel(const float* __restrict__ hi, const float* __restrict__ lo, long n, float* __restrict__ out) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = hi[i] + lo[i];
+}
+
+// Deterministic single-CTA sum of the per-row losses (warp-shuffle tree).
+__global__ void sum_loss_kernel(const float* __restrict__ row_loss, int rows, float scale, float* __restrict__ out) {
+  __shared__ float part[32];
+  float s = 0.f;
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) s += row_loss[r];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x / 32] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < blockDim.x / 32 ? part[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) *out = v * scale;
+  }
+}
+
+int grid_for(long n, int threads) {
+  long b = (n + threads - 1) / threads;
+  long cap = 148L * 8;
+  return static_cast<int>(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+}  // namespace
+
+void launch_gather(const float* X, long ldx, const float* Y, int n0, int nout, int N, int rows, int bw,
+                   const int* workers, const uint64_t* seed_dev, uint64_t seed_host, const int* step_dev,
+                   int step_host, const int* idx_in, int* idx_out, float* h_hi, float* h_lo, long ldh, float* ybatch,
+                   cudaStream_t s) {
+  if (rows <= 0) return;
+  gather_kernel<<<rows, 256, 0, s>>>(X, ldx, Y, n0, nout, N, bw, workers, seed_dev, seed_host, step_dev, step_host,
+                                     idx_in, idx_out,
+                                     h_hi, h_lo, ldh, ybatch);
+  SPB_CUDA(cudaGetLastError());
+}
+
+void launch_split_rows(const float* x, long ldx_in, int rows, int cols, float* hi, float* lo, long ld,
+                       cudaStream_t s) {
+  if (rows <= 0) return;
+  split_rows_kernel<<<rows, 256, 0, s>>>(x, ldx_in, cols, hi, lo, ld);
+  SPB_CUDA(cudaGetLastError());
+}
+
+void launch_head(const float* h_hi, const float* h_lo, long ldh, int rows, int n_in, int n_out, const float* w_hi,
+                 const float* w_lo, long ldw, const float* b_hi, const float* b_lo, const float* y, float* delta,
+                 float* row_loss, float* dn_hi, float* dn_lo, long ldd, int cont_row0, bool tanh_out,
+                 cudaStream_t s) {
+  if (rows <= 0) return;
+  if (n_out > kMaxOut) throw std::invalid_argument("head: n_out > 16");
+  const int warps = 8;
+  head_kernel<<<(rows + warps - 1) / warps, warps * 32, 0, s>>>(h_hi, h_lo, ldh, rows, n_in, n_out, w_hi, w_lo, ldw,
+                                                                b_hi, b_lo, y, delta, row_loss, dn_hi, dn_lo, ldd,
+                                                                cont_row0, tanh_out ? 1 : 0);
+  SPB_CUDA(cudaGetLastError());
+}
+
+long colreduce_scratch(int rows, int ncols, int nvec) {
+  const long nsplit = (rows + kRowsPerSplit - 1) / kRowsPerSplit;
+  return (nsplit < 1 ? 1 : nsplit) * nvec * static_cast<long>(ncols);
+}
+
+void launch_colreduce(const float* hi, const float* lo, long ld, int r0, int r1, int ncols, const float* rowvec,
+                      int nvec, long ldv, float alpha, float* out, long ld_out, float* scratch, cudaStream_t s) {
+  if (nvec > kMaxOut) throw std::invalid_argument("colreduce: nvec > 16");
+  const int rows = r1 - r0;
+  if (rows <= 0 || ncols <= 0) return;
+  const int nsplit = (rows + kRowsPerSplit - 1) / kRowsPerSplit;
+  dim3 g1((ncols + kColThreads - 1) / kColThreads, nsplit);
+  colreduce_partial_kernel<<<g1, kColThreads, 0, s>>>(hi, lo, ld, r0, r1, ncols, rowvec, nvec, ldv, scratch);
+  SPB_CUDA(cudaGetLastError());
+  const long tot = static_cast<long>(nvec) * ncols;
+  colreduce_final_kernel<<<static_cast<int>((tot + 255) / 256), 256, 0, s>>>(scratch, nsplit, nvec, ncols, alpha, out,
+                                                                             ld_out);
+  SPB_CUDA(cudaGetLastError());
+}
+
+void launch_sgd_update(float* p_hi, float* p_lo, const float* grad, float* mom, long n, float lr, float momentum,
+                       float wd, int* step_dev, cudaStream_t s) {
+  if (n % 4) throw std::invalid_argument("update: n must be a multiple of 4");
+  const long n4 = n / 4;
+  sgd_update_kernel<<<grid_for(n4, 256), 256, 0, s>>>(
+      reinterpret_cast<float4*>(p_hi), reinterpret_cast<float4*>(p_lo), reinterpret_cast<const float4*>(grad),
+      reinterpret_cast<float4*>(mom), n4, lr, momentum, wd, step_dev);
+  SPB_CUDA(cudaGetLastError());
+}
+
+void launch_aggregate(const float* const* srcs_dev, int m, long n, float* out, cudaStream_t s) {
+  if (n <= 0) return;
+  aggregate_kernel<<<grid_for(n, 256), 256, 0, s>>>(srcs_dev, m, n, out);
+  SPB_CUDA(cudaGetLastError());
+}
+
+void launch_split(const float* in, long n, float* hi, float* lo, cudaStream_t s) {
+  if (n <= 0) return;
+  split_kernel<<<grid_for(n, 256), 256, 0, s>>>(in, n, hi, lo);
+  SPB_CUDA(cudaGetLastError());
+}
+
+void launch_join(const float* hi, const float* lo, long n, float* out, cudaStream_t s) {
+  if (n <= 0) return;
+  join_kernel<<<grid_for(n, 256), 256, 0, s>>>(hi, lo, n, out);
+  SPB_CUDA(cudaGetLastError());
+}
+
+void launch_sum_loss(const float* row_loss, int rows, float scale, float* out, cudaStream_t s) {
+  sum_loss_kernel<<<1, 1024, 0, s>>>(row_loss, rows, scale, out);
+  SPB_CUDA(cudaGetLastError());
+}
+
+}  // namespace spb

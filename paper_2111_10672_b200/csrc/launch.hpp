@@ -1,0 +1,75 @@
+// Internal launcher interface shared by the kernel translation units and the
+// engine (C-ABI). Not part of the public boundary (include/spb_b200.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace spb {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define SPB_CUDA(expr)                                                                            \
+  do {                                                                                            \
+    cudaError_t e_ = (expr);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      throw ::spb::CudaError(std::string(#expr) + ": " + cudaGetErrorString(e_) + " @" __FILE__); \
+  } while (0)
+
+inline long round_up(long x, long a) { return (x + a - 1) / a * a; }
+
+// A GEMM operand as an exact split pair (hi + lo) in HBM.
+//   K-major : memory rows are MN indices (mn rows of k contiguous elements)
+//   MN-major: memory rows are K indices  (k rows of mn contiguous elements)
+struct Operand {
+  const float* hi;
+  const float* lo;
+  long ld;  // elements between memory rows (multiple of 4)
+  int mn;   // extent along the GEMM M (for A) / N (for B) dimension
+  int k;    // extent along K
+  bool mn_major;
+};
+
+struct GemmEpilogue;  // gemm_tf32x3.cuh
+
+// D = epi(A * B^T) over M = A.mn, N = B.mn, K = A.k. Returns kernels launched.
+int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue& ep, cudaStream_t s);
+
+// ---- non-GEMM kernels (kernels.cu) ----
+// H0 / Ybatch rows from the dataset. Indices come from `idx` (host-provided,
+// device pointer) or, when idx_in == nullptr, from the counter-based Rng
+// (rng.hpp) : row r -> slot r / bw, worker workers[slot], draw r % bw of
+// Rng(seed).split(*step).split(worker). Drawn indices are stored to idx_out.
+void launch_gather(const float* X, long ldx, const float* Y, int n0, int nout, int N, int rows, int bw,
+                   const int* workers, const uint64_t* seed_dev, uint64_t seed_host, const int* step_dev, int step_host,
+                   const int* idx_in,
+                   int* idx_out, float* h_hi, float* h_lo, long ldh, float* ybatch, cudaStream_t s);
+// Rows already on device (spb_step_host): split X rows into H0 hi/lo.
+void launch_split_rows(const float* x, long ldx_in, int rows, int cols, float* hi, float* lo, long ld,
+                       cudaStream_t s);
+// Head layer L (n_out <= 16): out = H W^T + b, delta = out - y, row_loss,
+// and for rows >= cont_row0: dnext = (delta W) * (1 - H^2) as a split pair.
+void launch_head(const float* h_hi, const float* h_lo, long ldh, int rows, int n_in, int n_out, const float* w_hi,
+                 const float* w_lo, long ldw, const float* b_hi, const float* b_lo, const float* y,
+                 float* delta, float* row_loss, float* dn_hi, float* dn_lo, long ldd, int cont_row0,
+                 bool tanh_out, cudaStream_t s);
+// out[o * ld_out + c] = alpha * sum_{r in [r0,r1)} vec(r,o) * (hi + lo)[r, c]
+// (vec = 1 when rowvec == nullptr, nvec = 1), deterministic two-pass column
+// reduction. scratch must hold colreduce_scratch(...) floats.
+long colreduce_scratch(int rows, int ncols, int nvec);
+void launch_colreduce(const float* hi, const float* lo, long ld, int r0, int r1, int ncols, const float* rowvec,
+                      int nvec, long ldv, float alpha, float* out, long ld_out, float* scratch, cudaStream_t s);
+// Optimizer over the flat parameter pair (see engine.cu).
+void launch_sgd_update(float* p_hi, float* p_lo, const float* grad, float* mom, long n, float lr, float momentum,
+                       float wd, int* step_dev, cudaStream_t s);
+// out[c] = (sum_{w} src[w][c]) / m for w ascending (aggregate, spb.cpp:97-103).
+void launch_aggregate(const float* const* srcs_dev, int m, long n, float* out, cudaStream_t s);
+void launch_split(const float* in, long n, float* hi, float* lo, cudaStream_t s);
+void launch_join(const float* hi, const float* lo, long n, float* out, cudaStream_t s);
+void launch_sum_loss(const float* row_loss, int rows, float scale, float* out, cudaStream_t s);
+
+}  // namespace spb

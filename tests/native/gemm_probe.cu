@@ -1,0 +1,110 @@
+// Standalone numerics probe of the tcgen05 3xTF32 GEMM for every operand
+// majorness, against an fp64 host reference (a torch-free stand-in for the
+// "plain fp32 reference" of a floating-point kernel). Built and run by
+// tests/test_gpu_gemm.py:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -I include -o build/gemm_probe \
+//        tests/native/gemm_probe.cu paper_2111_10672_b200/csrc/gemm.cu
+// Prints one line per case: "case am bm M N K rel_err max_abs_err" and exits
+// non-zero if any case exceeds 2e-6 norm-wise relative error.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <vector>
+
+#include "../../paper_2111_10672_b200/csrc/gemm_tf32x3.cuh"
+#include "../../paper_2111_10672_b200/csrc/launch.hpp"
+
+using namespace spb;
+
+static float rna(float x) {  // host cvt.rna.tf32.f32
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u = (u + 0x1000u) & ~0x1FFFu;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+struct Dev {
+  float *hi, *lo;
+};
+
+// Stores logical X[mn][k] in the requested majorness with ld padding.
+static Dev upload(const std::vector<float>& X, int mn, int k, bool mn_major, long& ld) {
+  const long rows = mn_major ? k : mn, cols = mn_major ? mn : k;
+  ld = (cols + 3) / 4 * 4 + 4;  // deliberately padded
+  std::vector<float> h(rows * ld, 0.f), l(rows * ld, 0.f);
+  for (int i = 0; i < mn; ++i)
+    for (int j = 0; j < k; ++j) {
+      const float v = X[static_cast<long>(i) * k + j];
+      const long at = mn_major ? static_cast<long>(j) * ld + i : static_cast<long>(i) * ld + j;
+      h[at] = rna(v);
+      l[at] = v - h[at];
+    }
+  Dev d;
+  cudaMalloc(&d.hi, h.size() * 4);
+  cudaMalloc(&d.lo, l.size() * 4);
+  cudaMemcpy(d.hi, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(d.lo, l.data(), l.size() * 4, cudaMemcpyHostToDevice);
+  return d;
+}
+
+int main() {
+  struct Case {
+    int M, N, K;
+  };
+  const Case cases[] = {{200, 300, 100}, {128, 128, 32}, {5, 7, 3}, {1024, 1024, 1024}, {333, 129, 517}};
+  int bad = 0;
+  std::mt19937_64 rng(1234);
+  std::uniform_real_distribution<float> U(-1.f, 1.f);
+  for (const Case& c : cases) {
+    std::vector<float> A(static_cast<long>(c.M) * c.K), B(static_cast<long>(c.N) * c.K);
+    for (auto& v : A) v = U(rng);
+    for (auto& v : B) v = U(rng);
+    std::vector<double> R(static_cast<long>(c.M) * c.N, 0.0);
+    for (int i = 0; i < c.M; ++i)
+      for (int j = 0; j < c.N; ++j) {
+        double s = 0;
+        for (int q = 0; q < c.K; ++q) s += static_cast<double>(A[static_cast<long>(i) * c.K + q]) * B[static_cast<long>(j) * c.K + q];
+        R[static_cast<long>(i) * c.N + j] = s;
+      }
+    for (int am = 0; am < 2; ++am)
+      for (int bm = 0; bm < 2; ++bm) {
+        long lda, ldb;
+        Dev a = upload(A, c.M, c.K, am, lda), b = upload(B, c.N, c.K, bm, ldb);
+        float* out;
+        const long ldo = (c.N + 3) / 4 * 4;
+        cudaMalloc(&out, static_cast<long>(c.M) * ldo * 4);
+        cudaMemset(out, 0, static_cast<long>(c.M) * ldo * 4);
+        Operand OA{a.hi, a.lo, lda, c.M, c.K, am != 0}, OB{b.hi, b.lo, ldb, c.N, c.K, bm != 0};
+        GemmEpilogue ep{};
+        ep.out_hi = out;
+        ep.ld_out = ldo;
+        ep.alpha = 1.0f;
+        ep.M = c.M;
+        ep.N = c.N;
+        gemm_tf32x3(OA, OB, kEpiStoreScaled, ep, 0);
+        cudaError_t e = cudaDeviceSynchronize();
+        std::vector<float> got(static_cast<long>(c.M) * ldo);
+        cudaMemcpy(got.data(), out, got.size() * 4, cudaMemcpyDeviceToHost);
+        double num = 0, den = 0, mx = 0;
+        for (int i = 0; i < c.M; ++i)
+          for (int j = 0; j < c.N; ++j) {
+            const double d = got[static_cast<long>(i) * ldo + j] - R[static_cast<long>(i) * c.N + j];
+            num += d * d;
+            den += R[static_cast<long>(i) * c.N + j] * R[static_cast<long>(i) * c.N + j];
+            mx = std::max(mx, std::fabs(d));
+          }
+        const double rel = std::sqrt(num / (den > 0 ? den : 1));
+        std::printf("case am=%d bm=%d M=%d N=%d K=%d rel_err=%.3e max_abs=%.3e %s\n", am, bm, c.M, c.N, c.K, rel, mx,
+                    e == cudaSuccess ? "" : cudaGetErrorString(e));
+        if (!(rel <= 2e-6) || e != cudaSuccess) ++bad;
+        cudaFree(a.hi), cudaFree(a.lo), cudaFree(b.hi), cudaFree(b.lo), cudaFree(out);
+      }
+  }
+  std::printf("%s\n", bad ? "GEMM PROBE FAILED" : "GEMM PROBE OK");
+  return bad ? 1 : 0;
+}
