@@ -158,6 +158,17 @@ SPB_API spb_status spb_last_batch(spb_ctx* ctx, int* out, int rows);
  * spb_train_steps / spb_step_host call (the captured graph's kernel nodes). */
 SPB_API spb_status spb_launches_per_step(spb_ctx* ctx, int* out);
 
+/* One SPB step run eagerly (not from the graph) with CUDA events around every
+ * launch. Per kernel class c (0 forward GEMM, 1 wgrad GEMM, 2 dgrad GEMM,
+ * 3 head, 4 bias/head-gradient reductions, 5 optimizer update, 6 gather,
+ * 7 collectives): ms[c] summed launch time, work[c] algorithmic work (GEMM
+ * FLOPs 2*M*N*K; update HBM bytes), launches[c]; step_ms the whole step. */
+SPB_API spb_status spb_profile_step(spb_ctx* ctx, uint64_t seed, int step, int full_backprop, int ncls, float* ms,
+                                    double* work, int* launches, float* step_ms);
+/* spb_train_steps timed with CUDA events on the context's stream (ms total). */
+SPB_API spb_status spb_time_train_steps(spb_ctx* ctx, uint64_t seed, int step0, int steps, int full_backprop,
+                                        float* ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -39,6 +39,9 @@ struct Ctl {
   int pad;
 };
 
+// Kernel classes of spb_profile_step (index into its output arrays).
+enum { kClsFwd = 0, kClsWgrad, kClsDgrad, kClsHead, kClsColred, kClsUpdate, kClsGather, kClsComm, kNumCls };
+
 }  // namespace
 
 struct Engine {
@@ -74,6 +77,28 @@ struct Engine {
   int graph_launches[2][2] = {{0, 0}, {0, 0}};
   int last_launches = 0;
   std::string err;
+
+  // Eager-mode instrumentation (spb_profile_step): CUDA events around every
+  // launch, tagged with a kernel class and its algorithmic work.
+  struct ProfRec {
+    int cls;
+    double work;
+    cudaEvent_t a, b;
+  };
+  std::vector<ProfRec>* prof = nullptr;
+  cudaEvent_t prof_a = nullptr;
+  void pbeg(cudaStream_t s) {
+    if (!prof) return;
+    SPB_CUDA(cudaEventCreate(&prof_a));
+    SPB_CUDA(cudaEventRecord(prof_a, s));
+  }
+  void pend(int cls, double work, cudaStream_t s) {
+    if (!prof) return;
+    cudaEvent_t b;
+    SPB_CUDA(cudaEventCreate(&b));
+    SPB_CUDA(cudaEventRecord(b, s));
+    prof->push_back({cls, work, prof_a, b});
+  }
 
   ~Engine() { release(); }
 
@@ -211,22 +236,27 @@ struct Engine {
       ep.bias_lo = p_lo + b_off[l];
       ep.M = rows;
       ep.N = w[l];
+      pbeg(s);
       n += gemm_tf32x3(A, B, kEpiFwdTanh, ep, s);
+      pend(kClsFwd, 2.0 * rows * w[l] * w[l - 1], s);
     }
     // Output head: out, delta_L = out - y (model.cpp:156), Delta_{L-1}.
     const bool has_next = L > 1 && row0[L - 1] < rows;
+    pbeg(s);
     launch_head(Hh[L - 1], Hl[L - 1], ld[L - 1], rows, w[L - 1], nout, p_hi + w_off[L], p_lo + w_off[L], ld[L - 1],
                 p_hi + b_off[L], p_lo + b_off[L], ybatch, delta, row_loss, has_next ? Dh[(L - 1) % 2] : nullptr,
                 has_next ? Dl[(L - 1) % 2] : nullptr, ldd, has_next ? row0[L - 1] : rows, false, s);
-    ++n;
     launch_sum_loss(row_loss, rows, 1.0f / static_cast<float>(rows), loss_dev, s);
-    ++n;
+    pend(kClsHead, 0, s);
+    n += 2;
     // Head gradients over the contributor rows of layer L.
     if (row0[L] < rows) {
+      pbeg(s);
       launch_colreduce(Hh[L - 1], Hl[L - 1], ld[L - 1], row0[L], rows, w[L - 1], delta, nout, nout, alpha[L],
                        grad + w_off[L], ld[L - 1], scratch, s);
       launch_colreduce(delta, nullptr, nout, row0[L], rows, nout, nullptr, 1, 0, alpha[L], grad + b_off[L], 0, scratch,
                        s);
+      pend(kClsColred, 0, s);
       n += 4;
     }
     // Truncated backward (model.cpp:161-185): layer l runs over its
@@ -244,9 +274,13 @@ struct Engine {
         ep.alpha = alpha[l];
         ep.M = w[l];
         ep.N = w[l - 1];
+        pbeg(s);
         n += gemm_tf32x3(A, B, kEpiStoreScaled, ep, s);
+        pend(kClsWgrad, 2.0 * cnt * w[l] * w[l - 1], s);
       }
+      pbeg(s);
       launch_colreduce(Dh[b], Dl[b], ldd, r0, rows, w[l], nullptr, 1, 0, alpha[l], grad + b_off[l], 0, scratch, s);
+      pend(kClsColred, 0, s);
       n += 2;
       if (l > 1 && row0[l - 1] < rows) {  // dgrad: Delta_{l-1} = (Delta_l W_l) * (1 - H_{l-1}^2)
         const int q0 = row0[l - 1], qn = rows - q0;
@@ -261,11 +295,17 @@ struct Engine {
         ep.ld_h = ld[l - 1];
         ep.M = qn;
         ep.N = w[l - 1];
+        pbeg(s);
         n += gemm_tf32x3(A, B, kEpiDgradTanh, ep, s);
+        pend(kClsDgrad, 2.0 * qn * w[l] * w[l - 1], s);
       }
     }
     return n;
   }
+
+  // HBM bytes one update launch must move: read hi, lo, grad (+ mom), write
+  // hi, lo (+ mom), 4 B each.
+  double update_bytes() const { return static_cast<double>(nflat) * 4.0 * (mom ? 7 : 5); }
 
   // Row plan of one SPB step for the hosted workers.
   void step_plan(bool full, std::vector<int>& row0, std::vector<float>& alpha) const {
@@ -291,18 +331,22 @@ struct Engine {
   int enqueue_step(bool full, bool host_rows, cudaStream_t s) {
     const int rows = static_cast<int>(workers.size()) * bw;
     int n = 0;
+    pbeg(s);
     if (host_rows) {
       launch_split_rows(xin, w[0], rows, w[0], Hh[0], Hl[0], ld[0], s);
     } else {
       launch_gather(X, ld[0], Y, w[0], nout, N, rows, bw, workers_dev, &ctl->seed, 0, &ctl->step, 0, nullptr, idx, Hh[0], Hl[0],
                     ld[0], ybatch, s);
     }
+    pend(kClsGather, 0, s);
     ++n;
     std::vector<int> row0;
     std::vector<float> alpha;
     step_plan(full, row0, alpha);
     n += enqueue_pass(rows, row0, alpha, s);
+    pbeg(s);
     launch_sgd_update(p_hi, p_lo, grad, mom, nflat, lr, mu, wd, &ctl->step, s);
+    pend(kClsUpdate, update_bytes(), s);
     ++n;
     return n;
   }
@@ -664,6 +708,66 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
   return guard(ctx, [&] {
     (void)unique_id128, (void)rank, (void)nranks;
     throw spb::ConfigError("comm: built without NCCL");
+  });
+}
+
+spb_status spb_profile_step(spb_ctx* ctx, uint64_t seed, int step, int full_backprop, int ncls, float* ms,
+                            double* work, int* launches, float* step_ms) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    if (!e.X) throw spb::ConfigError("profile_step: no dataset");
+    if (ncls < spb::kNumCls) throw spb::ArgumentError("profile_step: ncls too small");
+    std::vector<Engine::ProfRec> recs;
+    spb::Ctl c{seed, step, 0};
+    SPB_CUDA(cudaMemcpyAsync(e.ctl, &c, sizeof c, cudaMemcpyHostToDevice, e.st));
+    cudaEvent_t a, b;
+    SPB_CUDA(cudaEventCreate(&a));
+    SPB_CUDA(cudaEventCreate(&b));
+    e.prof = &recs;
+    SPB_CUDA(cudaEventRecord(a, e.st));
+    try {
+      e.enqueue_step(full_backprop != 0, false, e.st);
+    } catch (...) {
+      e.prof = nullptr;
+      throw;
+    }
+    SPB_CUDA(cudaEventRecord(b, e.st));
+    e.prof = nullptr;
+    SPB_CUDA(cudaStreamSynchronize(e.st));
+    for (int i = 0; i < ncls; ++i) ms[i] = 0.f, work[i] = 0.0, launches[i] = 0;
+    for (auto& r : recs) {
+      float t = 0.f;
+      SPB_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+      ms[r.cls] += t;
+      work[r.cls] += r.work;
+      launches[r.cls] += 1;
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    SPB_CUDA(cudaEventElapsedTime(step_ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  });
+}
+
+spb_status spb_time_train_steps(spb_ctx* ctx, uint64_t seed, int step0, int steps, int full_backprop, float* ms) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    if (!e.X) throw spb::ConfigError("train_steps: no dataset");
+    cudaGraphExec_t g = e.get_graph(full_backprop != 0, false);
+    spb::Ctl c{seed, step0, 0};
+    SPB_CUDA(cudaMemcpyAsync(e.ctl, &c, sizeof c, cudaMemcpyHostToDevice, e.st));
+    cudaEvent_t a, b;
+    SPB_CUDA(cudaEventCreate(&a));
+    SPB_CUDA(cudaEventCreate(&b));
+    SPB_CUDA(cudaEventRecord(a, e.st));
+    for (int i = 0; i < steps; ++i) SPB_CUDA(cudaGraphLaunch(g, e.st));
+    SPB_CUDA(cudaEventRecord(b, e.st));
+    SPB_CUDA(cudaEventSynchronize(b));
+    SPB_CUDA(cudaEventElapsedTime(ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    e.last_launches = e.graph_launches[full_backprop != 0][0];
   });
 }
 

@@ -40,6 +40,16 @@ CUtensorMap tmap2d(const float* base, long inner, long outer, long ld, int box_i
   return m;
 }
 
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    SPB_CUDA(cudaGetDevice(&dev));
+    SPB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
 CUtensorMap operand_map(const Operand& X, const float* base, int tile_rows) {
   if (!X.mn_major) return tmap2d(base, X.k, X.mn, X.ld, kBK, tile_rows, CU_TENSOR_MAP_SWIZZLE_128B);
   return tmap2d(base, X.mn, X.k, X.ld, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
@@ -57,8 +67,10 @@ void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cud
   CUtensorMap ah = operand_map(A, A.hi, kBM), al = operand_map(A, A.lo, kBM);
   CUtensorMap bh = operand_map(B, B.hi, BN), bl = operand_map(B, B.lo, BN);
   const int num_kb = (A.k + kBK - 1) / kBK;
-  dim3 grid((A.mn + kBM - 1) / kBM, (B.mn + BN - 1) / BN);
-  kern<<<grid, 256, smem, s>>>(ah, al, bh, bl, num_kb, ep);
+  const int num_m = (A.mn + kBM - 1) / kBM, num_n = (B.mn + BN - 1) / BN;
+  const int tiles = num_m * num_n;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, 256, smem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, ep);
   SPB_CUDA(cudaGetLastError());
 }
 

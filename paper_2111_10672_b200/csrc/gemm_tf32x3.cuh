@@ -106,7 +106,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
         *reinterpret_cast<float4*>(o + j) =
             make_float4(ep.alpha * v[j], ep.alpha * v[j + 1], ep.alpha * v[j + 2], ep.alpha * v[j + 3]);
     } else {
-      for (int j = 0; j < 32 && col0 + j < ep.N; ++j) o[j] = ep.alpha * v[j];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < ep.N) o[j] = ep.alpha * v[j];
     }
   } else if constexpr (EPI == kEpiFwdTanh || EPI == kEpiFwdLinear) {
     float* oh = ep.out_hi + row * ep.ld_out + col0;
@@ -122,7 +124,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
         store_split4(oh + j, ol + j, z);
       }
     } else {
-      for (int j = 0; j < 32 && col0 + j < ep.N; ++j) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (col0 + j >= ep.N) continue;
         float z = v[j] + (ep.bias_hi[col0 + j] + ep.bias_lo[col0 + j]);
         if (EPI == kEpiFwdTanh) z = tanhf(z);
         float h = tf32_rna(z);
@@ -146,7 +150,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
         store_split4(oh + j, ol + j, d);
       }
     } else {
-      for (int j = 0; j < 32 && col0 + j < ep.N; ++j) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (col0 + j >= ep.N) continue;
         float h = hh[j] + hl[j];
         float d = v[j] * (1.0f - h * h);
         float dh = tf32_rna(d);
@@ -157,24 +163,35 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
   }
 }
 
-// One CTA per 128 x BN output tile; grid = (ceil(M/128), ceil(N/BN)) so the
-// M-tiles sharing a B tile run side by side and B is read from HBM once.
+// Persistent CTAs (grid <= #SMs) walk the output tiles m-fastest, so the
+// CTAs running side by side share one B tile (read from HBM once).
+//
+// fp32-faithful accumulation: the tensor core rounds its fp32 accumulator
+// toward zero after every tcgen05.mma, so a single TMEM accumulator drifts by
+// ~(3K/8) * 2^-25 relative over K (7e-6 at K=1024, measured). The MMA warp
+// therefore accumulates only kChunkKb k-blocks (K = 32*kChunkKb) per TMEM
+// buffer; the epilogue warps drain each chunk into fp32 registers
+// (round-to-nearest adds) while the MMA warp fills the other buffer. The error
+// is then bounded independently of K.
+constexpr int kChunkKb = 4;  // 128 of K per TMEM chunk
+
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(256, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                        const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
-                       int num_kb, GemmEpilogue ep) {
+                       int num_kb, int num_m_tiles, int num_tiles, GemmEpilogue ep) {
   using Cfg = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
   uint64_t* empty_bar = full_bar + Cfg::kStages;
-  uint64_t* accum_bar = empty_bar + Cfg::kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
+  uint64_t* tfull_bar = empty_bar + Cfg::kStages;  // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31u;
-  const int m_tile = blockIdx.x, n_tile = blockIdx.y;
+  const int num_chunks = (num_kb + kChunkKb - 1) / kChunkKb;
 
   if (warp == 0 && elect_one()) {
     tma_prefetch(&ta_hi);
@@ -187,10 +204,13 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(accum_bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 4);  // one arrive per epilogue warp
+    }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, BN);
+  if (warp == 2) tmem_alloc(tmem_slot, 2 * BN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -198,59 +218,89 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % Cfg::kStages;
-        const uint32_t ph = (kb / Cfg::kStages) & 1u;
-        mbar_wait(&empty_bar[s], ph ^ 1u);
-        mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
-        uint8_t* base = smem + s * Cfg::kStageBytes;
-        load_operand<A_MN, kBM>(base, &ta_hi, &full_bar[s], m_tile * kBM, kb * kBK);
-        load_operand<A_MN, kBM>(base + Cfg::kABytes, &ta_lo, &full_bar[s], m_tile * kBM, kb * kBK);
-        load_operand<B_MN, BN>(base + 2 * Cfg::kABytes, &tb_hi, &full_bar[s], n_tile * BN, kb * kBK);
-        load_operand<B_MN, BN>(base + 2 * Cfg::kABytes + Cfg::kBBytes, &tb_lo, &full_bar[s], n_tile * BN,
-                               kb * kBK);
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int m0 = (t % num_m_tiles) * kBM, n0 = (t / num_m_tiles) * BN;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % Cfg::kStages;
+          const uint32_t ph = (it / Cfg::kStages) & 1u;
+          mbar_wait(&empty_bar[s], ph ^ 1u);
+          mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
+          uint8_t* base = smem + s * Cfg::kStageBytes;
+          load_operand<A_MN, kBM>(base, &ta_hi, &full_bar[s], m0, kb * kBK);
+          load_operand<A_MN, kBM>(base + Cfg::kABytes, &ta_lo, &full_bar[s], m0, kb * kBK);
+          load_operand<B_MN, BN>(base + 2 * Cfg::kABytes, &tb_hi, &full_bar[s], n0, kb * kBK);
+          load_operand<B_MN, BN>(base + 2 * Cfg::kABytes + Cfg::kBBytes, &tb_lo, &full_bar[s], n0, kb * kBK);
+        }
       }
     }
   } else if (warp == 1) {
     if (elect_one()) {
       constexpr uint32_t idesc = idesc_tf32(kBM, BN, A_MN, B_MN);
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % Cfg::kStages;
-        const uint32_t ph = (kb / Cfg::kStages) & 1u;
-        mbar_wait(&full_bar[s], ph);
-        tc_fence_after();
-        const uint32_t base = smem_u32(smem + s * Cfg::kStageBytes);
-        const uint32_t a_hi = base, a_lo = base + Cfg::kABytes;
-        const uint32_t b_hi = base + 2 * Cfg::kABytes, b_lo = b_hi + Cfg::kBBytes;
+      int it = 0, g = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        for (int c = 0; c < num_chunks; ++c, ++g) {
+          const uint32_t b = g & 1, tph = (g >> 1) & 1;
+          mbar_wait(&tempty_bar[b], tph ^ 1u);  // epilogue drained this buffer
+          tc_fence_after();
+          const uint32_t acc_addr = tmem + b * BN;
+          const int kb_end = min(num_kb, (c + 1) * kChunkKb);
+          for (int kb = c * kChunkKb; kb < kb_end; ++kb, ++it) {
+            const int s = it % Cfg::kStages;
+            const uint32_t ph = (it / Cfg::kStages) & 1u;
+            mbar_wait(&full_bar[s], ph);
+            tc_fence_after();
+            const uint32_t base = smem_u32(smem + s * Cfg::kStageBytes);
+            const uint32_t a_hi = base, a_lo = base + Cfg::kABytes;
+            const uint32_t b_hi = base + 2 * Cfg::kABytes, b_lo = b_hi + Cfg::kBBytes;
 #pragma unroll
-        for (int kk = 0; kk < kBK / 8; ++kk) {
-          const uint32_t acc = (kb | kk) != 0;
-          umma_tf32(tmem, operand_desc<A_MN>(a_lo, kk), operand_desc<B_MN>(b_hi, kk), idesc, acc);
-          umma_tf32(tmem, operand_desc<A_MN>(a_hi, kk), operand_desc<B_MN>(b_lo, kk), idesc, 1u);
-          umma_tf32(tmem, operand_desc<A_MN>(a_hi, kk), operand_desc<B_MN>(b_hi, kk), idesc, 1u);
+            for (int kk = 0; kk < kBK / 8; ++kk) {
+              const uint32_t acc = (kb != c * kChunkKb) || kk != 0;
+              umma_tf32(acc_addr, operand_desc<A_MN>(a_lo, kk), operand_desc<B_MN>(b_hi, kk), idesc, acc);
+              umma_tf32(acc_addr, operand_desc<A_MN>(a_hi, kk), operand_desc<B_MN>(b_lo, kk), idesc, 1u);
+              umma_tf32(acc_addr, operand_desc<A_MN>(a_hi, kk), operand_desc<B_MN>(b_hi, kk), idesc, 1u);
+            }
+            umma_commit(&empty_bar[s]);  // frees the smem stage once these MMAs retire
+          }
+          umma_commit(&tfull_bar[b]);  // chunk accumulated
         }
-        umma_commit(&empty_bar[s]);  // frees the stage once these MMAs retire
       }
-      umma_commit(accum_bar);  // accumulator complete
     }
   } else if (warp >= 4) {
     const uint32_t q = warp & 3u;
-    mbar_wait(accum_bar, 0);
-    tc_fence_after();
-    const int row = m_tile * kBM + static_cast<int>(q * 32 + lane);
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      float v[32];
-      tmem_ld_32x32b_x32(tmem + ((q * 32u) << 16) + static_cast<uint32_t>(c0), v);
-      const int col0 = n_tile * BN + c0;
-      if (col0 < ep.N) epilogue_chunk<EPI>(ep, v, row, col0);
+    const uint32_t lane_addr = (q * 32u) << 16;
+    int g = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int m0 = (t % num_m_tiles) * kBM, n0 = (t / num_m_tiles) * BN;
+      float acc[BN];
+#pragma unroll
+      for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+      for (int c = 0; c < num_chunks; ++c, ++g) {
+        const uint32_t b = g & 1, tph = (g >> 1) & 1;
+        mbar_wait(&tfull_bar[b], tph);
+        tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          tmem_ld_32x32b_x32(tmem + lane_addr + b * BN + c0, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[c0 + j] += v[j];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[b]);
+      }
+      const int row = m0 + static_cast<int>(q * 32 + lane);
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 32)
+        if (n0 + c0 < ep.N) epilogue_chunk<EPI>(ep, acc + c0, row, n0 + c0);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, BN);
+    tmem_dealloc(tmem, 2 * BN);
   }
 }
 

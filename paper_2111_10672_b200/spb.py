@@ -91,6 +91,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "spb_launches_per_step": (i, [vp, ip]),
         "spb_make_random_chain_mlp": (i, [ip, i, i, u64, fp, fp, vp]),
         "spb_get_grads": (i, [vp, vp]),
+        "spb_profile_step": (i, [vp, u64, i, i, i, fp, C.POINTER(C.c_double), ip, fp]),
+        "spb_time_train_steps": (i, [vp, u64, i, i, i, fp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -105,8 +107,10 @@ EXPORTED = [
     "spb_get_params", "spb_set_optimizer", "spb_partial_backprop", "spb_aggregate", "spb_train_steps",
     "spb_step_host", "spb_loss", "spb_synchronize", "spb_stream", "spb_comm_unique_id", "spb_comm_init",
     "spb_last_batch", "spb_launches_per_step", "spb_make_random_chain_mlp",
-    "spb_get_grads",
+    "spb_get_grads", "spb_profile_step", "spb_time_train_steps",
 ]
+
+PROFILE_CLASSES = ["gemm_fwd", "gemm_wgrad", "gemm_dgrad", "head", "colreduce", "update", "gather", "comm"]
 
 
 def _check(st: int, ctx=None):
@@ -322,6 +326,25 @@ class ChainMlp:
         _check(load_library().spb_step_host(self._ctx, _fp(X_rows), _fp(Y_rows), int(full_backprop), _fp(loss)),
                self._ctx)
         return float(loss[0])
+
+    def profile_step(self, seed: int, step: int, full_backprop: bool = False):
+        """One eager step with per-class CUDA-event timings (see spb_profile_step)."""
+        n = len(PROFILE_CLASSES)
+        ms = np.zeros(n, dtype=np.float32)
+        work = np.zeros(n, dtype=np.float64)
+        launches = np.zeros(n, dtype=np.int32)
+        step_ms = np.zeros(1, dtype=np.float32)
+        _check(load_library().spb_profile_step(self._ctx, seed, step, int(full_backprop), n, _fp(ms),
+                                               work.ctypes.data_as(C.POINTER(C.c_double)), _ip(launches),
+                                               _fp(step_ms)), self._ctx)
+        return {c: dict(ms=float(ms[i]), work=float(work[i]), launches=int(launches[i]))
+                for i, c in enumerate(PROFILE_CLASSES)}, float(step_ms[0])
+
+    def time_train_steps(self, seed: int, step0: int, steps: int, full_backprop: bool = False) -> float:
+        ms = np.zeros(1, dtype=np.float32)
+        _check(load_library().spb_time_train_steps(self._ctx, seed, step0, steps, int(full_backprop), _fp(ms)),
+               self._ctx)
+        return float(ms[0])
 
     def last_batch(self, rows: int) -> np.ndarray:
         out = np.zeros(rows, dtype=np.int32)

@@ -56,7 +56,7 @@ int main() {
   struct Case {
     int M, N, K;
   };
-  const Case cases[] = {{200, 300, 100}, {128, 128, 32}, {5, 7, 3}, {1024, 1024, 1024}, {333, 129, 517}};
+  const Case cases[] = {{200, 300, 100}, {128, 128, 32}, {5, 7, 3}, {1024, 1024, 1024}, {333, 129, 517}, {256, 384, 4096}, {130, 260, 8192}};
   int bad = 0;
   std::mt19937_64 rng(1234);
   std::uniform_real_distribution<float> U(-1.f, 1.f);
