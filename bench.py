@@ -323,6 +323,8 @@ def run_b200(args, world, rank, local, dist):
         "phase_ms_full_backprop": {c: round(prof_full[c]["ms"], 3) for c in prof_full},
         "eager_step_ms": round(prof_step_ms, 3),
     }
+    barrier(dist)
+    m.close()
     del m
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, kind, cores, sample = cpu_reference(cfg, 1, 0, REF_BW)

@@ -150,6 +150,12 @@ SPB_API void* spb_stream(spb_ctx* ctx);
  * NCCL over NVLink on per-layer buckets. */
 SPB_API spb_status spb_comm_unique_id(void* out128);
 SPB_API spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int nranks);
+/* The per-layer bucket protocol spb_comm_init sets up (host-only, no GPU):
+ * for layer l (index l-1): kind 0 = all-reduce over all ranks (ranks without
+ * contributor rows add zeros), 1 = broadcast from root (a single contributing
+ * rank); rank_mask = bit r set when rank r hosts a contributor of layer l. */
+SPB_API spb_status spb_bucket_plan(int k, int L, int nranks, int full_backprop, int* kind, int* root,
+                                   int* rank_mask);
 
 /* ---- Introspection for tests and the bench ----------------------------------- */
 /* Batch indices the last device-drawn step used (rows in hosted-worker order). */

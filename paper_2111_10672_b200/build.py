@@ -24,7 +24,6 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",
           "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-DSPB_BUILD_LIB"]
-NCCL_STATIC = "/usr/lib/x86_64-linux-gnu/libnccl_static.a"
 
 
 def _sources():
@@ -61,11 +60,9 @@ def build(force: bool = False, verbose: bool = True) -> str:
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
         return LIB
     link = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
-    if os.path.exists(NCCL_STATIC):
-        link += ["-Xlinker", "--exclude-libs,ALL", NCCL_STATIC]
-    link += ["-lcuda" if os.path.exists("/usr/local/cuda/lib64/stubs/libcuda.so") and False else "", "-lpthread",
-             "-ldl", "-lrt"]
-    link = [a for a in link if a]
+    # NCCL is linked dynamically (libnccl.so.2, SONAME-compatible with the one
+    # torch may already have loaded into the process); everything else static.
+    link += ["-lnccl", "-lpthread", "-ldl", "-lrt"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

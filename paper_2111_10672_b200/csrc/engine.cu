@@ -16,8 +16,10 @@
 // contributors of every layer are a contiguous tail of rows (chunk_coverage,
 // spb.cpp:23-29) and each layer's aggregate is ONE wgrad GEMM over that tail.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -77,6 +79,12 @@ struct Engine {
   int graph_launches[2][2] = {{0, 0}, {0, 0}};
   int last_launches = 0;
   std::string err;
+  // multi-GPU
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  cudaStream_t cst = nullptr;  // collectives
+  std::vector<Bucket> buckets[2];  // [full]
+  std::vector<cudaEvent_t> evs;    // fork/join events (reused)
 
   // Eager-mode instrumentation (spb_profile_step): CUDA events around every
   // launch, tagged with a kernel class and its algorithmic work.
@@ -103,9 +111,25 @@ struct Engine {
   ~Engine() { release(); }
 
   void release() {
+    // Order matters: graphs that captured NCCL collectives hold references to
+    // the communicator, so they go first; then the communicator is finalized
+    // (flushes outstanding work) before it is destroyed.
+    if (st) cudaStreamSynchronize(st);
+    if (cst) cudaStreamSynchronize(cst);
     for (auto& row : graph)
       for (auto& g : row)
         if (g) cudaGraphExecDestroy(g), g = nullptr;
+    if (comm) {
+      ncclCommFinalize(comm);
+      ncclResult_t state = ncclInProgress;
+      while (ncclCommGetAsyncError(comm, &state) == ncclSuccess && state == ncclInProgress) {
+      }
+      ncclCommDestroy(comm);
+      comm = nullptr;
+    }
+    if (cst) cudaStreamDestroy(cst), cst = nullptr;
+    for (auto ev : evs) cudaEventDestroy(ev);
+    evs.clear();
     auto f = [](void* p) {
       if (p) cudaFree(p);
     };
@@ -222,7 +246,10 @@ struct Engine {
   // ---- the per-step launch program ----------------------------------------
   // row0[l] (l = 1..L): first row contributing to layer l (rows when none).
   // alpha[l]: the averaging factor 1/(m_l * per_worker_batch) of layer l.
-  int enqueue_pass(int rows, const std::vector<int>& row0, const std::vector<float>& alpha, cudaStream_t s) {
+  // on_grad(l) runs after layer l's gradient is final on this rank (for every
+  // layer, top down, including layers with no local contributor rows).
+  int enqueue_pass(int rows, const std::vector<int>& row0, const std::vector<float>& alpha, cudaStream_t s,
+                   const std::function<int(int)>& on_grad = nullptr) {
     int n = 0;
     // Forward, hidden layers (mlp_forward model.cpp:108-128 batched).
     for (int l = 1; l < L; ++l) {
@@ -259,9 +286,11 @@ struct Engine {
       pend(kClsColred, 0, s);
       n += 4;
     }
+    if (on_grad) n += on_grad(L);
     // Truncated backward (model.cpp:161-185): layer l runs over its
     // contributor rows only; dgrad stops at the lowest covered layer.
-    for (int l = L - 1; l >= 1; --l) {
+    int l = L - 1;
+    for (; l >= 1; --l) {
       if (row0[l] >= rows) break;
       const int r0 = row0[l], cnt = rows - r0;
       const int b = l % 2;
@@ -299,8 +328,44 @@ struct Engine {
         n += gemm_tf32x3(A, B, kEpiDgradTanh, ep, s);
         pend(kClsDgrad, 2.0 * qn * w[l] * w[l - 1], s);
       }
+      if (on_grad) n += on_grad(l);
     }
+    for (; l >= 1 && on_grad; --l) n += on_grad(l);  // no local rows below here
     return n;
+  }
+
+  cudaEvent_t ev(size_t i) {
+    while (evs.size() <= i) {
+      cudaEvent_t e;
+      SPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      evs.push_back(e);
+    }
+    return evs[i];
+  }
+
+  // Layer l's bucket collective on the comm stream, after the main stream has
+  // produced the layer's local gradient (grad[w_off[l] .. b_off[l] + n_l)).
+  int enqueue_bucket(int l, bool full, cudaStream_t s) {
+    const Bucket* bk = nullptr;
+    for (auto& b : buckets[full])
+      if (b.l_lo <= l && l <= b.l_hi) bk = &b;
+    if (!bk) throw ConfigError("comm: no bucket for layer");
+    SPB_CUDA(cudaEventRecord(ev(2 + l), s));
+    SPB_CUDA(cudaStreamWaitEvent(cst, ev(2 + l), 0));
+    float* base = grad + w_off[l];
+    const size_t count = static_cast<size_t>(b_off[l] + w[l] - w_off[l]);
+    const bool mine = std::find(bk->ranks.begin(), bk->ranks.end(), rank) != bk->ranks.end();
+    pbeg(cst);
+    ncclResult_t r;
+    if (bk->kind == 1) {
+      r = ncclBroadcast(base, base, count, ncclFloat32, bk->root, comm, cst);
+    } else {
+      if (!mine) SPB_CUDA(cudaMemsetAsync(base, 0, count * sizeof(float), cst));
+      r = ncclAllReduce(base, base, count, ncclFloat32, ncclSum, comm, cst);
+    }
+    if (r != ncclSuccess) throw std::runtime_error(std::string("nccl: ") + ncclGetErrorString(r));
+    pend(kClsComm, static_cast<double>(count) * 4.0, cst);
+    return 0;
   }
 
   // HBM bytes one update launch must move: read hi, lo, grad (+ mom), write
@@ -343,7 +408,16 @@ struct Engine {
     std::vector<int> row0;
     std::vector<float> alpha;
     step_plan(full, row0, alpha);
-    n += enqueue_pass(rows, row0, alpha, s);
+    if (comm) {
+      // Fork the comm stream into this stream's (captured) work.
+      SPB_CUDA(cudaEventRecord(ev(0), s));
+      SPB_CUDA(cudaStreamWaitEvent(cst, ev(0), 0));
+      n += enqueue_pass(rows, row0, alpha, s, [&](int l) { return enqueue_bucket(l, full, s); });
+      SPB_CUDA(cudaEventRecord(ev(1), cst));  // join before the update
+      SPB_CUDA(cudaStreamWaitEvent(s, ev(1), 0));
+    } else {
+      n += enqueue_pass(rows, row0, alpha, s);
+    }
     pbeg(s);
     launch_sgd_update(p_hi, p_lo, grad, mom, nflat, lr, mu, wd, &ctl->step, s);
     pend(kClsUpdate, update_bytes(), s);
@@ -699,15 +773,48 @@ void* spb_stream(spb_ctx* ctx) { return ctx ? static_cast<void*>(ctx->e.st) : nu
 
 spb_status spb_comm_unique_id(void* out128) {
   return guard(nullptr, [&] {
-    (void)out128;
-    throw spb::ConfigError("comm: built without NCCL");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) throw std::runtime_error(std::string("nccl: ") + ncclGetErrorString(r));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof id);
   });
 }
 
 spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int nranks) {
-  return guard(ctx, [&] {
-    (void)unique_id128, (void)rank, (void)nranks;
-    throw spb::ConfigError("comm: built without NCCL");
+  spb_status st = guard(ctx, [&] {
+    auto& e = ctx->e;
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw spb::ArgumentError("comm: bad rank");
+    if (nranks > e.k) throw spb::ArgumentError("comm: more ranks than SPB workers");
+    if (e.comm) throw spb::ConfigError("comm: already initialised");
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id128, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&e.comm, nranks, id, rank);
+    if (r != ncclSuccess) throw std::runtime_error(std::string("nccl: ") + ncclGetErrorString(r));
+    e.rank = rank;
+    e.nranks = nranks;
+    SPB_CUDA(cudaStreamCreateWithFlags(&e.cst, cudaStreamNonBlocking));
+    e.buckets[0] = spb::bucket_plan(e.k, e.L, nranks, false);
+    e.buckets[1] = spb::bucket_plan(e.k, e.L, nranks, true);
+    e.set_workers(spb::rank_workers(e.k, e.L, rank, nranks));
+    e.ensure_rows(static_cast<int>(e.workers.size()) * e.bw);
+  });
+  if (st != SPB_OK && ctx && ctx->e.err.rfind("nccl", 0) == 0) return SPB_E_NCCL;
+  return st;
+}
+
+spb_status spb_bucket_plan(int k, int L, int nranks, int full_backprop, int* kind, int* root, int* rank_mask) {
+  return guard(nullptr, [&] {
+    if (nranks > 31) throw spb::ArgumentError("bucket_plan: at most 31 ranks");
+    auto b = spb::bucket_plan(k, L, nranks, full_backprop != 0);
+    for (auto& x : b) {
+      const int l = x.l_hi;
+      kind[l - 1] = x.kind;
+      root[l - 1] = x.root;
+      int mask = 0;
+      for (int r : x.ranks) mask |= 1 << r;
+      rank_mask[l - 1] = mask;
+    }
   });
 }
 

@@ -128,4 +128,40 @@ inline std::vector<int> rank_workers(int k, int L, int rank, int nranks) {
   return w;
 }
 
+// Per-layer gradient buckets for the multi-GPU step (issued as soon as the
+// backward pass has produced that layer, so the collectives overlap the rest
+// of the backward). Layer l's contributor RANKS are the ranks hosting a
+// worker j with stop_j <= l (every rank when `full`). A bucket with a single
+// contributing rank is BROADCAST from it (the others have nothing to add);
+// any other bucket is ALL-REDUCED over all ranks, non-contributors adding
+// zeros. For ring collectives this is the per-rank-byte-optimal choice: a
+// sub-group all-reduce followed by a broadcast costs 2(s-1)/s + 1 > 2(N-1)/N
+// bucket sizes whenever s >= 2.
+struct Bucket {
+  int l_lo, l_hi;          // 1-based layer range [l_lo, l_hi]
+  std::vector<int> ranks;  // contributing ranks, ascending
+  int kind;                // 0 = all-reduce, 1 = broadcast from root
+  int root;
+};
+
+inline std::vector<Bucket> bucket_plan(int k, int L, int nranks, bool full) {
+  std::vector<std::vector<int>> owned(nranks);
+  for (int r = 0; r < nranks; ++r) owned[r] = rank_workers(k, L, r, nranks);
+  std::vector<std::vector<int>> per_layer(L + 1);
+  for (int l = 1; l <= L; ++l)
+    for (int r = 0; r < nranks; ++r)
+      for (int j : owned[r])
+        if (full || worker_stop(j, k, L) <= l) {
+          per_layer[l].push_back(r);
+          break;
+        }
+  std::vector<Bucket> out;
+  for (int l = L; l >= 1; --l) {
+    Bucket b{l, l, per_layer[l], 0, 0};
+    if (b.ranks.size() == 1) b.kind = 1, b.root = b.ranks[0];
+    out.push_back(b);
+  }
+  return out;  // top (layer L) bucket first: the order backward produces them
+}
+
 }  // namespace spb

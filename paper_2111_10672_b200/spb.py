@@ -93,6 +93,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "spb_get_grads": (i, [vp, vp]),
         "spb_profile_step": (i, [vp, u64, i, i, i, fp, C.POINTER(C.c_double), ip, fp]),
         "spb_time_train_steps": (i, [vp, u64, i, i, i, fp]),
+        "spb_bucket_plan": (i, [i, i, i, i, ip, ip, ip]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -107,7 +108,7 @@ EXPORTED = [
     "spb_get_params", "spb_set_optimizer", "spb_partial_backprop", "spb_aggregate", "spb_train_steps",
     "spb_step_host", "spb_loss", "spb_synchronize", "spb_stream", "spb_comm_unique_id", "spb_comm_init",
     "spb_last_batch", "spb_launches_per_step", "spb_make_random_chain_mlp",
-    "spb_get_grads", "spb_profile_step", "spb_time_train_steps",
+    "spb_get_grads", "spb_profile_step", "spb_time_train_steps", "spb_bucket_plan",
 ]
 
 PROFILE_CLASSES = ["gemm_fwd", "gemm_wgrad", "gemm_dgrad", "head", "colreduce", "update", "gather", "comm"]
@@ -172,6 +173,22 @@ def rank_workers(k: int, L: int, rank: int, nranks: int) -> List[int]:
     n = C.c_int()
     _check(load_library().spb_rank_workers(k, L, rank, nranks, _ip(out), C.byref(n)))
     return out[: n.value].tolist()
+
+
+def bucket_plan(k: int, L: int, nranks: int, full_backprop: bool = False):
+    """Per layer (index l-1): (kind, root, contributing ranks) of the
+    multi-GPU gradient protocol; kind 0 = all-reduce, 1 = broadcast."""
+    kind = np.zeros(L, dtype=np.int32)
+    root = np.zeros(L, dtype=np.int32)
+    mask = np.zeros(L, dtype=np.int32)
+    _check(load_library().spb_bucket_plan(k, L, nranks, int(full_backprop), _ip(kind), _ip(root), _ip(mask)))
+    return [(int(kind[l]), int(root[l]), [r for r in range(nranks) if (int(mask[l]) >> r) & 1]) for l in range(L)]
+
+
+def comm_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(load_library().spb_comm_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
 
 
 def block_dims(widths: Sequence[int]) -> List[int]:
@@ -257,11 +274,15 @@ class ChainMlp:
         self._initial = [np.asarray(b, dtype=np.float32).copy() for b in weights]
         self.set_params(self._initial)
 
-    def __del__(self):
+    def close(self):
+        """Releases the device state (and the NCCL communicator, if any)."""
         ctx = getattr(self, "_ctx", None)
         if ctx is not None and _lib is not None:
             _lib.spb_destroy(ctx)
-            self._ctx = None
+        self._ctx = None
+
+    def __del__(self):
+        self.close()
 
     # LayeredModel accessors (model.hpp:32-36)
     def layer_count(self) -> int:
@@ -345,6 +366,18 @@ class ChainMlp:
         _check(load_library().spb_time_train_steps(self._ctx, seed, step0, steps, int(full_backprop), _fp(ms)),
                self._ctx)
         return float(ms[0])
+
+    def comm_init(self, unique_id: bytes, rank: int, nranks: int):
+        """Joins the NCCL clique; the context then runs only this rank's workers."""
+        buf = (C.c_char * 128).from_buffer_copy(unique_id)
+        _check(load_library().spb_comm_init(self._ctx, C.cast(buf, C.c_void_p), rank, nranks), self._ctx)
+        self.rank, self.nranks = rank, nranks
+
+    def comm_init_torch(self, dist, rank: int, nranks: int):
+        """Rendezvous through an initialised torch.distributed group (plumbing only)."""
+        obj = [comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        self.comm_init(obj[0], rank, nranks)
 
     def last_batch(self, rows: int) -> np.ndarray:
         out = np.zeros(rows, dtype=np.int32)

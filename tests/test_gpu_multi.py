@@ -1,0 +1,87 @@
+"""Multi-GPU SPB step over NCCL (needs >= 2 GPUs; skipped otherwise).
+
+Each rank runs its balanced worker set on its own B200, per-layer buckets are
+reduced with NCCL (broadcast from a sole contributor, else all-reduce), and
+every rank applies the same update. Weights after 3 steps must equal the
+single-process CPU oracle's SPB-SGD iterates (1e-4) and be bit-identical
+across ranks; batch indices must be bit-exact.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpus():
+    try:
+        import torch
+
+        return torch.cuda.device_count()
+    except Exception:  # noqa: BLE001
+        return 0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+WIDTHS, N, K, BW, LR, SEED, DSEED = [96, 80, 72, 64, 56, 48, 40, 32, 1], 512, 8, 16, 0.05, 11, 5
+
+
+def _rank(rank, world, port, out_dir, full):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+
+    from paper_2111_10672_b200 import spb
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    X, Y, W = spb.gen_chain_mlp(WIDTHS, N, DSEED)
+    m = spb.ChainMlp(WIDTHS, X, Y, W, k=K, per_worker_batch=BW, device=rank)
+    m.comm_init_torch(dist, rank, world)
+    m.set_optimizer(LR)
+    m.train_steps(SEED, 1, 1, full_backprop=full)
+    idx = m.last_batch(len(spb.rank_workers(K, len(WIDTHS) - 1, rank, world)) * BW)
+    m.train_steps(SEED, 2, 2, full_backprop=full)
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), idx, *m.get_params())
+    dist.barrier()
+    m.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("full", [False, True])
+def test_multi_gpu_step_matches_oracle(tmp_path, orc, full):
+    world = min(_gpus(), 4)
+    if world < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import torch.multiprocessing as mp
+
+    from paper_2111_10672_b200 import spb
+
+    mp.start_processes(_rank, args=(world, _free_port(), str(tmp_path), full), nprocs=world, start_method="spawn")
+    L = len(WIDTHS) - 1
+    X, Y, W = orc.gen_chain_mlp(WIDTHS, N, DSEED)
+    Xf, Yf, Wf = spb.gen_chain_mlp(WIDTHS, N, DSEED)
+    X, Y, P = Xf.astype(np.float64), Yf.astype(np.float64), [b.astype(np.float64) for b in Wf]
+    for s in range(1, 4):
+        orc.spb_step(WIDTHS, X, Y, P, K, K * BW, LR, SEED, s, full=full)
+    outs = [np.load(os.path.join(tmp_path, f"r{r}.npz")) for r in range(world)]
+    for r in range(world):
+        ws = spb.rank_workers(K, L, r, world)
+        want = np.concatenate([orc.draw_batch(SEED, 1, j, BW, N) for j in ws])
+        assert np.array_equal(outs[r]["arr_0"], want)
+        for l in range(L):
+            got = outs[r][f"arr_{l + 1}"]
+            assert np.linalg.norm(got - P[l]) / np.linalg.norm(P[l]) <= 1e-4
+            assert np.array_equal(got, outs[0][f"arr_{l + 1}"])
