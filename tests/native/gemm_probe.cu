@@ -1,9 +1,8 @@
 // Standalone numerics probe of the tcgen05 3xTF32 GEMM for every operand
 // majorness, against an fp64 host reference (a torch-free stand-in for the
 // "plain fp32 reference" of a floating-point kernel). Built and run by
-// tests/test_gpu_gemm.py:
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -I include -o build/gemm_probe \
-//        tests/native/gemm_probe.cu paper_2111_10672_b200/csrc/gemm.cu
+// tests/test_native.py (nvcc -gencode arch=compute_100a,code=sm_100a with
+// paper_2111_10672_b200/csrc/gemm.cu).
 // Prints one line per case: "case am bm M N K rel_err max_abs_err" and exits
 // non-zero if any case exceeds 2e-6 norm-wise relative error.
 #include <cuda_runtime.h>

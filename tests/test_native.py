@@ -1,0 +1,56 @@
+"""Native (C/C++/CUDA) test programs: the GEMM numerics probe and the C++
+drop-in adapter test. Compiling them needs no GPU (CPU tests); running them
+does (gpu tests)."""
+import os
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+BUILD = os.path.join(ROOT, "build")
+NVCC = "/usr/local/cuda/bin/nvcc"
+
+
+def _build_probe():
+    os.makedirs(BUILD, exist_ok=True)
+    out = os.path.join(BUILD, "gemm_probe")
+    subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-std=c++17", "-I",
+                    os.path.join(ROOT, "include"), "-o", out, os.path.join(ROOT, "tests/native/gemm_probe.cu"),
+                    os.path.join(ROOT, "paper_2111_10672_b200/csrc/gemm.cu")], check=True, capture_output=True)
+    return out
+
+
+def _build_adapter():
+    from paper_2111_10672_b200 import spb
+
+    spb.load_library()
+    os.makedirs(BUILD, exist_ok=True)
+    out = os.path.join(BUILD, "test_adapter")
+    libdir = os.path.join(ROOT, "paper_2111_10672_b200")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests/native/test_adapter.cpp"), "-L", libdir, "-l:libspb_b200.so",
+                    f"-Wl,-rpath,{libdir}", "-o", out], check=True, capture_output=True)
+    return out
+
+
+def test_adapter_compiles_against_the_c_abi():
+    assert os.path.exists(_build_adapter())
+
+
+def test_gemm_probe_compiles():
+    assert os.path.exists(_build_probe())
+
+
+@pytest.mark.gpu
+def test_gemm_probe_numerics():
+    r = subprocess.run([_build_probe()], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "GEMM PROBE OK" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_adapter_on_gpu():
+    r = subprocess.run([_build_adapter()], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
