@@ -92,6 +92,12 @@ SPB_API spb_status spb_set_dataset(spb_ctx* ctx, const float* X, const float* Y,
 /* Params in / out (LayeredModel::initial_params, spb_sgd_run's iterate x). */
 SPB_API spb_status spb_set_params(spb_ctx* ctx, const float* const* blocks);
 SPB_API spb_status spb_get_params(spb_ctx* ctx, float* const* blocks);
+/* fused = 1: single-GPU steps apply the optimizer inside the backward pass
+ * (the wgrad GEMM epilogue updates W in place; the aggregated gradient is then
+ * not materialised). fused = 0 (default): aggregate into the gradient buffer,
+ * readable with spb_get_grads, then one fused update kernel over all params.
+ * Multi-GPU steps are always unfused (buckets are reduced first). */
+SPB_API spb_status spb_set_fused_update(spb_ctx* ctx, int fused);
 /* Optimizer: x -= lr * g (spb.cpp:196) when momentum = weight_decay = 0;
  * otherwise momentum SGD + weight decay (PyTorch semantics). */
 SPB_API spb_status spb_set_optimizer(spb_ctx* ctx, float lr, float momentum, float weight_decay);
@@ -132,9 +138,9 @@ SPB_API spb_status spb_train_steps(spb_ctx* ctx, uint64_t seed, int step0, int s
  * steps, and copies the loss out (synchronous). */
 SPB_API spb_status spb_step_host(spb_ctx* ctx, const float* X_rows, const float* Y_rows, int full_backprop,
                          float* loss_out);
-/* The aggregated per-layer gradient the last step applied (aggregate's output,
- * spb.cpp:70-106, in the Params block layout), or for spb_partial_backprop the
- * covered blocks of the last call. */
+/* The aggregated per-layer gradient the last unfused step applied
+ * (aggregate's output, spb.cpp:70-106, in the Params block layout), or for
+ * spb_partial_backprop the covered blocks of the last call. */
 SPB_API spb_status spb_get_grads(spb_ctx* ctx, float* const* blocks);
 /* ChainMlp::loss (model.cpp:139-143) over the whole uploaded dataset. */
 SPB_API spb_status spb_loss(spb_ctx* ctx, double* out);

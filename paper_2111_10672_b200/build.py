@@ -60,9 +60,8 @@ def build(force: bool = False, verbose: bool = True) -> str:
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
         return LIB
     link = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
-    # NCCL is linked dynamically (libnccl.so.2, SONAME-compatible with the one
-    # torch may already have loaded into the process); everything else static.
-    link += ["-lnccl", "-lpthread", "-ldl", "-lrt"]
+    # NCCL is dlopen'ed at first use (engine.cu); everything else is static.
+    link += ["-lpthread", "-ldl", "-lrt"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

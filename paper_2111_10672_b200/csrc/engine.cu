@@ -16,8 +16,10 @@
 // contributors of every layer are a contiguous tail of rows (chunk_coverage,
 // spb.cpp:23-29) and each layer's aggregate is ONE wgrad GEMM over that tail.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -35,11 +37,66 @@ namespace {
 
 thread_local std::string g_err;
 
+// NCCL is resolved at first use with dlopen, never at library load: the
+// process may also host torch's own NCCL (a newer libnccl.so.2), and binding
+// the system one at load time would shadow it. SPB_NCCL_LIB (set by the
+// Python front-end to torch's bundled copy when present) wins; otherwise the
+// already-loaded or system libnccl.so.2 is used.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*CommFinalize)(ncclComm_t);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*);
+  const char* (*GetErrorString)(ncclResult_t);
+};
+
+const NcclApi& nccl() {
+  static NcclApi api{};
+  static std::string fail;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = nullptr;
+    if (const char* p = std::getenv("SPB_NCCL_LIB")) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      fail = std::string("comm: cannot load libnccl.so.2: ") + dlerror();
+      return;
+    }
+    auto sym = [&](const char* n) {
+      void* f = dlsym(h, n);
+      if (!f && fail.empty()) fail = std::string("comm: missing NCCL symbol ") + n;
+      return f;
+    };
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+    api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
+    api.CommFinalize = reinterpret_cast<decltype(api.CommFinalize)>(sym("ncclCommFinalize"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.CommGetAsyncError = reinterpret_cast<decltype(api.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  });
+  if (!fail.empty()) throw std::runtime_error(fail);
+  return api;
+}
+
+void nccl_check(ncclResult_t r) {
+  if (r != ncclSuccess) throw std::runtime_error(std::string("nccl: ") + nccl().GetErrorString(r));
+}
+
 struct Ctl {
   uint64_t seed;
   int step;
   int pad;
 };
+
+// Event slots (Engine::ev): fork/join of the step, per-layer backward and
+// per-layer bucket events.
+enum { kEvStepFork = 0, kEvStepJoin = 1, kEvFork = 2, kEvJoin = 3, kEvUpdFork = 4, kEvUpdJoin = 5, kEvBucket = 8,
+       kEvLayer = 8 + 1024, kEvUpd = 8 + 3072 };
 
 // Kernel classes of spb_profile_step (index into its output arrays).
 enum { kClsFwd = 0, kClsWgrad, kClsDgrad, kClsHead, kClsColred, kClsUpdate, kClsGather, kClsComm, kNumCls };
@@ -64,7 +121,8 @@ struct Engine {
   int cap_rows = 0;
   std::vector<float*> Hh, Hl;
   float *Dh[2] = {nullptr, nullptr}, *Dl[2] = {nullptr, nullptr};
-  float *delta = nullptr, *row_loss = nullptr, *ybatch = nullptr, *scratch = nullptr, *xin = nullptr;
+  float *delta = nullptr, *row_loss = nullptr, *ybatch = nullptr, *scratch = nullptr, *scratch2 = nullptr,
+        *xin = nullptr;
   long scratch_n = 0;
   int* idx = nullptr;
   int* idx_in = nullptr;
@@ -83,8 +141,12 @@ struct Engine {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
   cudaStream_t cst = nullptr;  // collectives
+  cudaStream_t s2 = nullptr;   // wgrad branch of the backward (runs beside dgrad)
+  cudaStream_t s3 = nullptr;   // per-layer optimizer updates (run beside the backward GEMMs)
   std::vector<Bucket> buckets[2];  // [full]
   std::vector<cudaEvent_t> evs;    // fork/join events (reused)
+  bool fused_update = false;       // single-GPU: optimizer inside the wgrad epilogue (opt-in)
+  bool concurrent = true;          // side streams (off in spb_profile_step: clean per-kernel times)
 
   // Eager-mode instrumentation (spb_profile_step): CUDA events around every
   // launch, tagged with a kernel class and its algorithmic work.
@@ -120,20 +182,23 @@ struct Engine {
       for (auto& g : row)
         if (g) cudaGraphExecDestroy(g), g = nullptr;
     if (comm) {
-      ncclCommFinalize(comm);
+      const NcclApi& api = nccl();
+      api.CommFinalize(comm);
       ncclResult_t state = ncclInProgress;
-      while (ncclCommGetAsyncError(comm, &state) == ncclSuccess && state == ncclInProgress) {
+      while (api.CommGetAsyncError(comm, &state) == ncclSuccess && state == ncclInProgress) {
       }
-      ncclCommDestroy(comm);
+      api.CommDestroy(comm);
       comm = nullptr;
     }
     if (cst) cudaStreamDestroy(cst), cst = nullptr;
+    if (s2) cudaStreamDestroy(s2), s2 = nullptr;
+    if (s3) cudaStreamDestroy(s3), s3 = nullptr;
     for (auto ev : evs) cudaEventDestroy(ev);
     evs.clear();
     auto f = [](void* p) {
       if (p) cudaFree(p);
     };
-    f(p_hi), f(p_lo), f(grad), f(mom), f(X), f(Y), f(delta), f(row_loss), f(ybatch), f(scratch), f(xin), f(idx),
+    f(p_hi), f(p_lo), f(grad), f(mom), f(X), f(Y), f(delta), f(row_loss), f(ybatch), f(scratch), f(scratch2), f(xin), f(idx),
         f(idx_in), f(loss_dev), f(tmp), f(ctl), f(workers_dev);
     for (auto p : Hh) f(p);
     for (auto p : Hl) f(p);
@@ -164,6 +229,8 @@ struct Engine {
     dev = device;
     SPB_CUDA(cudaSetDevice(dev));
     SPB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    SPB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    SPB_CUDA(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
     ld.resize(L + 1);
     long ldmax = 0;
     for (int l = 0; l <= L; ++l) ld[l] = round_up(w[l], 4), ldmax = std::max(ldmax, ld[l]);
@@ -219,7 +286,7 @@ struct Engine {
     for (int i = 0; i < 2; ++i) {
       if (Dh[i]) cudaFree(Dh[i]), cudaFree(Dl[i]);
     }
-    for (void* p : {(void*)delta, (void*)row_loss, (void*)ybatch, (void*)scratch, (void*)xin, (void*)idx,
+    for (void* p : {(void*)delta, (void*)row_loss, (void*)ybatch, (void*)scratch, (void*)scratch2, (void*)xin, (void*)idx,
                     (void*)idx_in})
       if (p) cudaFree(p);
     cap_rows = rows;
@@ -238,6 +305,7 @@ struct Engine {
     for (int l = 1; l <= L; ++l) sc = std::max(sc, colreduce_scratch(rows, w[l - 1], nout));
     scratch_n = sc;
     scratch = alloc<float>(sc);
+    scratch2 = alloc<float>(sc);
     xin = alloc<float>(static_cast<long>(rows) * w[0]);
     idx = alloc<int>(rows);
     idx_in = alloc<int>(rows);
@@ -248,8 +316,14 @@ struct Engine {
   // alpha[l]: the averaging factor 1/(m_l * per_worker_batch) of layer l.
   // on_grad(l) runs after layer l's gradient is final on this rank (for every
   // layer, top down, including layers with no local contributor rows).
+  // fused: apply the optimizer inside the backward (single-GPU step): the
+  // wgrad GEMM epilogue updates W_l in place and the bias / head reductions
+  // update b_l / W_L, so the gradient never round-trips through HBM. dgrad_l
+  // then runs before wgrad_l, because it reads the pre-update W_l.
+  // step_dev (nullable) is advanced once the gather has consumed it.
   int enqueue_pass(int rows, const std::vector<int>& row0, const std::vector<float>& alpha, cudaStream_t s,
-                   const std::function<int(int)>& on_grad = nullptr) {
+                   const std::function<int(int, cudaStream_t)>& on_grad = nullptr, bool fused = false,
+                   int* step_dev = nullptr, const std::function<void(int, cudaStream_t)>& on_layer = nullptr) {
     int n = 0;
     // Forward, hidden layers (mlp_forward model.cpp:108-128 batched).
     for (int l = 1; l < L; ++l) {
@@ -273,45 +347,44 @@ struct Engine {
     launch_head(Hh[L - 1], Hl[L - 1], ld[L - 1], rows, w[L - 1], nout, p_hi + w_off[L], p_lo + w_off[L], ld[L - 1],
                 p_hi + b_off[L], p_lo + b_off[L], ybatch, delta, row_loss, has_next ? Dh[(L - 1) % 2] : nullptr,
                 has_next ? Dl[(L - 1) % 2] : nullptr, ldd, has_next ? row0[L - 1] : rows, false, s);
-    launch_sum_loss(row_loss, rows, 1.0f / static_cast<float>(rows), loss_dev, s);
+    launch_sum_loss(row_loss, rows, 1.0f / static_cast<float>(rows), loss_dev, step_dev, s);
     pend(kClsHead, 0, s);
     n += 2;
+    auto col_upd = [&](long off) {
+      return ColUpdate{p_lo + off, mom ? mom + off : nullptr, lr, mu, wd};
+    };
     // Head gradients over the contributor rows of layer L.
     if (row0[L] < rows) {
       pbeg(s);
+      ColUpdate uw = col_upd(w_off[L]), ub = col_upd(b_off[L]);
       launch_colreduce(Hh[L - 1], Hl[L - 1], ld[L - 1], row0[L], rows, w[L - 1], delta, nout, nout, alpha[L],
-                       grad + w_off[L], ld[L - 1], scratch, s);
-      launch_colreduce(delta, nullptr, nout, row0[L], rows, nout, nullptr, 1, 0, alpha[L], grad + b_off[L], 0, scratch,
-                       s);
+                       fused ? p_hi + w_off[L] : grad + w_off[L], ld[L - 1], scratch, s, fused ? &uw : nullptr);
+      launch_colreduce(delta, nullptr, nout, row0[L], rows, nout, nullptr, 1, 0, alpha[L],
+                       fused ? p_hi + b_off[L] : grad + b_off[L], 0, scratch, s, fused ? &ub : nullptr);
       pend(kClsColred, 0, s);
       n += 4;
     }
-    if (on_grad) n += on_grad(L);
+    if (on_grad) n += on_grad(L, s);
+    if (on_layer) on_layer(L, s);  // W_L: read by the head only
     // Truncated backward (model.cpp:161-185): layer l runs over its
     // contributor rows only; dgrad stops at the lowest covered layer.
+    // Unfused: wgrad_l (+ bias) runs on the side stream s2 beside dgrad_l
+    // (both only read Delta_l); dgrad_l waits for wgrad_{l+1}, which was the
+    // last reader of the Delta buffer it overwrites. Collectives and the final
+    // update wait on s2.
+    const bool two = !fused && concurrent;
+    if (two) {
+      SPB_CUDA(cudaEventRecord(ev(kEvFork), s));
+      SPB_CUDA(cudaStreamWaitEvent(s2, ev(kEvFork), 0));
+    }
+    cudaStream_t sw = two ? s2 : s;
     int l = L - 1;
     for (; l >= 1; --l) {
       if (row0[l] >= rows) break;
       const int r0 = row0[l], cnt = rows - r0;
       const int b = l % 2;
-      {  // wgrad: dW_l = alpha_l * Delta_l[r0:]^T H_{l-1}[r0:]
-        Operand A{Dh[b] + r0 * ldd, Dl[b] + r0 * ldd, ldd, w[l], cnt, true};
-        Operand B{Hh[l - 1] + r0 * ld[l - 1], Hl[l - 1] + r0 * ld[l - 1], ld[l - 1], w[l - 1], cnt, true};
-        GemmEpilogue ep{};
-        ep.out_hi = grad + w_off[l];
-        ep.ld_out = ld[l - 1];
-        ep.alpha = alpha[l];
-        ep.M = w[l];
-        ep.N = w[l - 1];
-        pbeg(s);
-        n += gemm_tf32x3(A, B, kEpiStoreScaled, ep, s);
-        pend(kClsWgrad, 2.0 * cnt * w[l] * w[l - 1], s);
-      }
-      pbeg(s);
-      launch_colreduce(Dh[b], Dl[b], ldd, r0, rows, w[l], nullptr, 1, 0, alpha[l], grad + b_off[l], 0, scratch, s);
-      pend(kClsColred, 0, s);
-      n += 2;
-      if (l > 1 && row0[l - 1] < rows) {  // dgrad: Delta_{l-1} = (Delta_l W_l) * (1 - H_{l-1}^2)
+      auto dgrad = [&] {  // Delta_{l-1} = (Delta_l W_l) * (1 - H_{l-1}^2)
+        if (!(l > 1 && row0[l - 1] < rows)) return;
         const int q0 = row0[l - 1], qn = rows - q0;
         Operand A{Dh[b] + q0 * ldd, Dl[b] + q0 * ldd, ldd, qn, w[l], false};
         Operand B{p_hi + w_off[l], p_lo + w_off[l], ld[l - 1], w[l - 1], w[l], true};
@@ -327,10 +400,57 @@ struct Engine {
         pbeg(s);
         n += gemm_tf32x3(A, B, kEpiDgradTanh, ep, s);
         pend(kClsDgrad, 2.0 * qn * w[l] * w[l - 1], s);
+      };
+      if (fused) dgrad();
+      if (two) {  // Delta_l is ready on s (head or dgrad_{l+1})
+        SPB_CUDA(cudaEventRecord(ev(kEvLayer + 2 * l), s));
+        SPB_CUDA(cudaStreamWaitEvent(s2, ev(kEvLayer + 2 * l), 0));
       }
-      if (on_grad) n += on_grad(l);
+      {  // wgrad: dW_l = alpha_l * Delta_l[r0:]^T H_{l-1}[r0:] (or the fused update of W_l)
+        Operand A{Dh[b] + r0 * ldd, Dl[b] + r0 * ldd, ldd, w[l], cnt, true};
+        Operand B{Hh[l - 1] + r0 * ld[l - 1], Hl[l - 1] + r0 * ld[l - 1], ld[l - 1], w[l - 1], cnt, true};
+        GemmEpilogue ep{};
+        ep.ld_out = ld[l - 1];
+        ep.alpha = alpha[l];
+        ep.M = w[l];
+        ep.N = w[l - 1];
+        if (fused) {
+          ep.out_hi = p_hi + w_off[l];
+          ep.out_lo = p_lo + w_off[l];
+          ep.mom = mom ? mom + w_off[l] : nullptr;
+          ep.lr = lr;
+          ep.mu = mu;
+          ep.wd = wd;
+        } else {
+          ep.out_hi = grad + w_off[l];
+        }
+        pbeg(sw);
+        n += gemm_tf32x3(A, B, fused ? kEpiWgradUpdate : kEpiStoreScaled, ep, sw);
+        pend(kClsWgrad, 2.0 * cnt * w[l] * w[l - 1], sw);
+      }
+      pbeg(sw);
+      ColUpdate ub = col_upd(b_off[l]);
+      launch_colreduce(Dh[b], Dl[b], ldd, r0, rows, w[l], nullptr, 1, 0, alpha[l],
+                       fused ? p_hi + b_off[l] : grad + b_off[l], 0, scratch2, sw, fused ? &ub : nullptr);
+      pend(kClsColred, 0, sw);
+      n += 2;
+      if (two) {
+        SPB_CUDA(cudaEventRecord(ev(kEvLayer + 2 * l + 1), s2));  // wgrad_l done
+        // dgrad_l overwrites the Delta buffer that wgrad_{l+1} read: wait for it.
+        if (l + 1 <= L - 1) SPB_CUDA(cudaStreamWaitEvent(s, ev(kEvLayer + 2 * (l + 1) + 1), 0));
+      }
+      if (!fused) dgrad();
+      if (on_grad) n += on_grad(l, two ? s2 : s);
+      if (on_layer) on_layer(l, two ? s2 : s);  // grad of layer l final there; dgrad_l (last W_l reader) on s
     }
-    for (; l >= 1 && on_grad; --l) n += on_grad(l);  // no local rows below here
+    if (two) {  // join the side stream
+      SPB_CUDA(cudaEventRecord(ev(kEvJoin), s2));
+      SPB_CUDA(cudaStreamWaitEvent(s, ev(kEvJoin), 0));
+    }
+    for (; l >= 1 && on_grad; --l) {  // no local rows below here
+      n += on_grad(l, s);
+      if (on_layer) on_layer(l, s);
+    }
     return n;
   }
 
@@ -345,25 +465,23 @@ struct Engine {
 
   // Layer l's bucket collective on the comm stream, after the main stream has
   // produced the layer's local gradient (grad[w_off[l] .. b_off[l] + n_l)).
-  int enqueue_bucket(int l, bool full, cudaStream_t s) {
+  int enqueue_bucket(int l, bool full, cudaStream_t s) {  // s: the stream that produced layer l's gradient
     const Bucket* bk = nullptr;
     for (auto& b : buckets[full])
       if (b.l_lo <= l && l <= b.l_hi) bk = &b;
     if (!bk) throw ConfigError("comm: no bucket for layer");
-    SPB_CUDA(cudaEventRecord(ev(2 + l), s));
-    SPB_CUDA(cudaStreamWaitEvent(cst, ev(2 + l), 0));
+    SPB_CUDA(cudaEventRecord(ev(kEvBucket + l), s));
+    SPB_CUDA(cudaStreamWaitEvent(cst, ev(kEvBucket + l), 0));
     float* base = grad + w_off[l];
     const size_t count = static_cast<size_t>(b_off[l] + w[l] - w_off[l]);
     const bool mine = std::find(bk->ranks.begin(), bk->ranks.end(), rank) != bk->ranks.end();
     pbeg(cst);
-    ncclResult_t r;
     if (bk->kind == 1) {
-      r = ncclBroadcast(base, base, count, ncclFloat32, bk->root, comm, cst);
+      nccl_check(nccl().Broadcast(base, base, count, ncclFloat32, bk->root, comm, cst));
     } else {
       if (!mine) SPB_CUDA(cudaMemsetAsync(base, 0, count * sizeof(float), cst));
-      r = ncclAllReduce(base, base, count, ncclFloat32, ncclSum, comm, cst);
+      nccl_check(nccl().AllReduce(base, base, count, ncclFloat32, ncclSum, comm, cst));
     }
-    if (r != ncclSuccess) throw std::runtime_error(std::string("nccl: ") + ncclGetErrorString(r));
     pend(kClsComm, static_cast<double>(count) * 4.0, cst);
     return 0;
   }
@@ -408,20 +526,45 @@ struct Engine {
     std::vector<int> row0;
     std::vector<float> alpha;
     step_plan(full, row0, alpha);
+    // Unfused optimizer: one update launch per layer on s3, issued as soon as
+    // the layer's gradient is final (wgrad on s2, or its NCCL bucket on cst)
+    // and its last reader dgrad_l (on s) is done, so the HBM-bound update
+    // runs beside the remaining backward GEMMs instead of after them.
+    const bool per_layer = comm || !fused_update;
+    cudaStream_t us = concurrent ? s3 : s;
+    auto fork = [&](cudaStream_t to, int e) {
+      SPB_CUDA(cudaEventRecord(ev(e), s));
+      SPB_CUDA(cudaStreamWaitEvent(to, ev(e), 0));
+    };
+    auto join = [&](cudaStream_t from, int e) {
+      SPB_CUDA(cudaEventRecord(ev(e), from));
+      SPB_CUDA(cudaStreamWaitEvent(s, ev(e), 0));
+    };
+    if (comm) fork(cst, kEvStepFork);
+    if (per_layer && concurrent) fork(s3, kEvUpdFork);
+    static const bool skip_update = std::getenv("SPB_DEBUG_SKIP_UPDATE") != nullptr;  // timing experiments only
+    auto on_layer = [&](int l, cudaStream_t grad_stream) {
+      if (skip_update) return;
+      cudaStream_t src = comm ? cst : grad_stream;
+      SPB_CUDA(cudaEventRecord(ev(kEvUpd + 2 * l), s));  // dgrad_l issued before this point on s
+      SPB_CUDA(cudaEventRecord(ev(kEvUpd + 2 * l + 1), src));
+      SPB_CUDA(cudaStreamWaitEvent(us, ev(kEvUpd + 2 * l), 0));
+      SPB_CUDA(cudaStreamWaitEvent(us, ev(kEvUpd + 2 * l + 1), 0));
+      const long off = w_off[l], cnt = b_off[l] + round_up(w[l], 32) - w_off[l];
+      pbeg(us);
+      launch_sgd_update(p_hi + off, p_lo + off, grad + off, mom ? mom + off : nullptr, cnt, lr, mu, wd, us);
+      pend(kClsUpdate, static_cast<double>(cnt) * 4.0 * (mom ? 7 : 5), us);
+      ++n;
+    };
     if (comm) {
-      // Fork the comm stream into this stream's (captured) work.
-      SPB_CUDA(cudaEventRecord(ev(0), s));
-      SPB_CUDA(cudaStreamWaitEvent(cst, ev(0), 0));
-      n += enqueue_pass(rows, row0, alpha, s, [&](int l) { return enqueue_bucket(l, full, s); });
-      SPB_CUDA(cudaEventRecord(ev(1), cst));  // join before the update
-      SPB_CUDA(cudaStreamWaitEvent(s, ev(1), 0));
+      n += enqueue_pass(rows, row0, alpha, s, [&](int l, cudaStream_t from) { return enqueue_bucket(l, full, from); },
+                        false, &ctl->step, on_layer);
+      join(cst, kEvStepJoin);
     } else {
-      n += enqueue_pass(rows, row0, alpha, s);
+      n += enqueue_pass(rows, row0, alpha, s, nullptr, fused_update, &ctl->step,
+                        per_layer ? std::function<void(int, cudaStream_t)>(on_layer) : nullptr);
     }
-    pbeg(s);
-    launch_sgd_update(p_hi, p_lo, grad, mom, nflat, lr, mu, wd, &ctl->step, s);
-    pend(kClsUpdate, update_bytes(), s);
-    ++n;
+    if (per_layer && concurrent) join(s3, kEvUpdJoin);
     return n;
   }
 
@@ -613,6 +756,13 @@ spb_status spb_get_grads(spb_ctx* ctx, float* const* blocks) {
   });
 }
 
+spb_status spb_set_fused_update(spb_ctx* ctx, int fused) {
+  return guard(ctx, [&] {
+    ctx->e.fused_update = fused != 0;
+    ctx->e.invalidate_graphs();
+  });
+}
+
 spb_status spb_set_optimizer(spb_ctx* ctx, float lr, float momentum, float weight_decay) {
   return guard(ctx, [&] {
     auto& e = ctx->e;
@@ -774,8 +924,7 @@ void* spb_stream(spb_ctx* ctx) { return ctx ? static_cast<void*>(ctx->e.st) : nu
 spb_status spb_comm_unique_id(void* out128) {
   return guard(nullptr, [&] {
     ncclUniqueId id;
-    ncclResult_t r = ncclGetUniqueId(&id);
-    if (r != ncclSuccess) throw std::runtime_error(std::string("nccl: ") + ncclGetErrorString(r));
+    spb::nccl_check(spb::nccl().GetUniqueId(&id));
     static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
     std::memcpy(out128, &id, sizeof id);
   });
@@ -789,8 +938,7 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     if (e.comm) throw spb::ConfigError("comm: already initialised");
     ncclUniqueId id;
     std::memcpy(&id, unique_id128, sizeof id);
-    ncclResult_t r = ncclCommInitRank(&e.comm, nranks, id, rank);
-    if (r != ncclSuccess) throw std::runtime_error(std::string("nccl: ") + ncclGetErrorString(r));
+    spb::nccl_check(spb::nccl().CommInitRank(&e.comm, nranks, id, rank));
     e.rank = rank;
     e.nranks = nranks;
     SPB_CUDA(cudaStreamCreateWithFlags(&e.cst, cudaStreamNonBlocking));
@@ -799,7 +947,8 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     e.set_workers(spb::rank_workers(e.k, e.L, rank, nranks));
     e.ensure_rows(static_cast<int>(e.workers.size()) * e.bw);
   });
-  if (st != SPB_OK && ctx && ctx->e.err.rfind("nccl", 0) == 0) return SPB_E_NCCL;
+  if (st != SPB_OK && ctx && (ctx->e.err.rfind("nccl", 0) == 0 || ctx->e.err.rfind("comm: ", 0) == 0))
+    return SPB_E_NCCL;
   return st;
 }
 
@@ -831,15 +980,18 @@ spb_status spb_profile_step(spb_ctx* ctx, uint64_t seed, int step, int full_back
     SPB_CUDA(cudaEventCreate(&a));
     SPB_CUDA(cudaEventCreate(&b));
     e.prof = &recs;
+    e.concurrent = false;  // serialise so each launch's events time it alone
     SPB_CUDA(cudaEventRecord(a, e.st));
     try {
       e.enqueue_step(full_backprop != 0, false, e.st);
     } catch (...) {
       e.prof = nullptr;
+      e.concurrent = true;
       throw;
     }
     SPB_CUDA(cudaEventRecord(b, e.st));
     e.prof = nullptr;
+    e.concurrent = true;
     SPB_CUDA(cudaStreamSynchronize(e.st));
     for (int i = 0; i < ncls; ++i) ms[i] = 0.f, work[i] = 0.0, launches[i] = 0;
     for (auto& r : recs) {

@@ -5,6 +5,9 @@
 
 #include <mutex>
 
+#include <cstdlib>
+
+#include "gemm_2sm.cuh"
 #include "gemm_tf32x3.cuh"
 #include "launch.hpp"
 
@@ -74,6 +77,52 @@ void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cud
   SPB_CUDA(cudaGetLastError());
 }
 
+template <bool AM, bool BM_, int EPI>
+void launch_2sm(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
+  using Cfg = Gemm2smCfg;
+  auto kern = gemm_tf32x3_2sm_kernel<AM, BM_, EPI>;
+  static bool configured = false;
+  if (!configured) {
+    SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
+    configured = true;
+  }
+  CUtensorMap ah = operand_map(A, A.hi, Cfg::kRowsA), al = operand_map(A, A.lo, Cfg::kRowsA);
+  CUtensorMap bh = operand_map(B, B.hi, Cfg::kRowsB), bl = operand_map(B, B.lo, Cfg::kRowsB);
+  const int num_kb = (A.k + kBK - 1) / kBK;
+  const int num_m = (A.mn + 255) / 256, num_n = (B.mn + Cfg::kPairN - 1) / Cfg::kPairN;
+  const int tiles = num_m * num_n;
+  const int pairs = num_sms() / 2;
+  const int clusters = tiles < pairs ? tiles : pairs;
+  kern<<<2 * clusters, Cfg::kThreads, Cfg::kSmem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, ep);
+  SPB_CUDA(cudaGetLastError());
+}
+
+template <int EPI>
+void dispatch_2sm(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
+  if (!A.mn_major && !B.mn_major) launch_2sm<false, false, EPI>(A, B, ep, s);
+  else if (!A.mn_major && B.mn_major) launch_2sm<false, true, EPI>(A, B, ep, s);
+  else if (A.mn_major && !B.mn_major) launch_2sm<true, false, EPI>(A, B, ep, s);
+  else launch_2sm<true, true, EPI>(A, B, ep, s);
+}
+
+int g_force_variant = -1;  // -1 auto, 0 = 1-CTA 128x128, 1 = CTA pair 256x256
+
+// Wave-quantised cost of each variant, in units of one 1-CTA 128x128 tile.
+// A pair tile is 4 such tiles on 2 SMs at kPairSpeedup x the per-SM rate.
+bool use_2sm(int M, int N) {
+  if (g_force_variant >= 0) return g_force_variant == 1;
+  static const double ratio = [] {
+    const char* e = std::getenv("SPB_2SM_COST");
+    return e ? std::atof(e) : 0.7;
+  }();
+  const int sms = num_sms();
+  const long t1 = static_cast<long>((M + 127) / 128) * ((N + 127) / 128);
+  const long t2 = static_cast<long>((M + 255) / 256) * ((N + 255) / 256);
+  const double c1 = static_cast<double>((t1 + sms - 1) / sms);
+  const double c2 = static_cast<double>((t2 + sms / 2 - 1) / (sms / 2)) * 2.0 * ratio;
+  return c2 < c1;
+}
+
 template <int BN, int EPI>
 void dispatch_major(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
   if (!A.mn_major && !B.mn_major) launch_inst<BN, false, false, EPI>(A, B, ep, s);
@@ -84,16 +133,31 @@ void dispatch_major(const Operand& A, const Operand& B, const GemmEpilogue& ep, 
 
 }  // namespace
 
+void gemm_force_variant(int v) { g_force_variant = v; }
+
 int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue& ep, cudaStream_t s) {
   if (A.k != B.k) throw std::invalid_argument("gemm: K mismatch");
+  if (epi == kEpiWgradUpdate && !(A.mn_major && B.mn_major)) throw std::invalid_argument("gemm: wgrad-update is MN/MN");
   if (A.mn <= 0 || B.mn <= 0 || A.k <= 0) return 0;
   if ((A.ld % 4) || (B.ld % 4)) throw std::invalid_argument("gemm: ld must be a multiple of 4");
   constexpr int BN = 128;
+  if (use_2sm(A.mn, B.mn)) {
+    switch (epi) {
+      case kEpiFwdTanh: dispatch_2sm<kEpiFwdTanh>(A, B, ep, s); break;
+      case kEpiStoreScaled: dispatch_2sm<kEpiStoreScaled>(A, B, ep, s); break;
+      case kEpiDgradTanh: dispatch_2sm<kEpiDgradTanh>(A, B, ep, s); break;
+      case kEpiFwdLinear: dispatch_2sm<kEpiFwdLinear>(A, B, ep, s); break;
+      case kEpiWgradUpdate: launch_2sm<true, true, kEpiWgradUpdate>(A, B, ep, s); break;
+      default: throw std::invalid_argument("gemm: bad epilogue");
+    }
+    return 1;
+  }
   switch (epi) {
     case kEpiFwdTanh: dispatch_major<BN, kEpiFwdTanh>(A, B, ep, s); break;
     case kEpiStoreScaled: dispatch_major<BN, kEpiStoreScaled>(A, B, ep, s); break;
     case kEpiDgradTanh: dispatch_major<BN, kEpiDgradTanh>(A, B, ep, s); break;
     case kEpiFwdLinear: dispatch_major<BN, kEpiFwdLinear>(A, B, ep, s); break;
+    case kEpiWgradUpdate: launch_inst<BN, true, true, kEpiWgradUpdate>(A, B, ep, s); break;
     default: throw std::invalid_argument("gemm: bad epilogue");
   }
   return 1;

@@ -1,0 +1,186 @@
+// CTA-pair (cta_group::2) variant of the 3xTF32 GEMM: one 256 x 256 output
+// tile per SM pair. Each CTA stages its 128 rows of A and its 128 rows of B
+// (hi + lo, 64 KB per k-block) and the leader CTA issues
+// tcgen05.mma.cta_group::2 M=256 N=256 K=8, which reads A from each CTA's own
+// smem and B from both halves. Per SM this moves half the shared-memory and
+// L2 bytes per FLOP of the 1-CTA 128 x 128 tile, which is what bounds the
+// 1-CTA kernel (tensor pipe ~60% active, profiles/r01_*).
+//
+// Roles (384 threads = 3 warpgroups, 1 CTA/SM): warp 0 TMA producer (both
+// CTAs), warp 1 MMA issuer (leader only), warp 2 TMEM allocator, warp 3
+// idle; warps 4..11 epilogue: warp w drains TMEM lanes 32*(w%4)..+31 and
+// columns 128*((w-4)/4)..+127 of its CTA's 128 x 256 accumulator.
+// Accumulation is chunked exactly as in gemm_tf32x3.cuh (kChunkKb k-blocks
+// per TMEM buffer, drained into fp32 registers), so numerics match.
+#pragma once
+#include "gemm_tf32x3.cuh"
+
+namespace spb {
+
+struct Gemm2smCfg {
+  static constexpr int kRowsA = 128;  // per CTA
+  static constexpr int kRowsB = 128;  // per CTA (pair N = 256)
+  static constexpr int kPairN = 256;
+  static constexpr int kABytes = kRowsA * kBK * 4;
+  static constexpr int kBBytes = kRowsB * kBK * 4;
+  static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;  // 64 KB
+  static constexpr int kStages = 3;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kThreads = 384;
+  static constexpr int kEpiWarps = 8;
+};
+
+template <bool MN_MAJOR, int ROWS>
+__device__ __forceinline__ void load_operand_2sm(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, int mn0,
+                                                 int k0) {
+  if constexpr (!MN_MAJOR) {
+    tma_load_2d_2sm(dst, tm, bar, k0, mn0);
+  } else {
+#pragma unroll
+    for (int c = 0; c < ROWS / 32; ++c) tma_load_2d_2sm(dst + c * 4096, tm, bar, mn0 + c * 32, k0);
+  }
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    gemm_tf32x3_2sm_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
+                           const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
+                           int num_kb, int num_m_pairs, int num_tiles, GemmEpilogue ep) {
+  using Cfg = Gemm2smCfg;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + Cfg::kStages;
+  uint64_t* tfull_bar = empty_bar + Cfg::kStages;  // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;            // [2], leader's copy is the live one
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t cta = cluster_ctarank();
+  const bool leader = cta == 0;
+  const int cluster_id = static_cast<int>(blockIdx.x >> 1), nclusters = static_cast<int>(gridDim.x >> 1);
+  const int num_chunks = (num_kb + kChunkKb - 1) / kChunkKb;
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&ta_hi);
+    tma_prefetch(&ta_lo);
+    tma_prefetch(&tb_hi);
+    tma_prefetch(&tb_lo);
+  }
+  if (warp == 1 && elect_one()) {
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 2 * Cfg::kEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    regs_dealloc<56>();
+    if (warp == 0) {
+      if (elect_one()) {
+        int it = 0;
+        for (int t = cluster_id; t < num_tiles; t += nclusters) {
+          const int m0 = (t % num_m_pairs) * 256 + static_cast<int>(cta) * Cfg::kRowsA;
+          const int n0 = (t / num_m_pairs) * Cfg::kPairN + static_cast<int>(cta) * Cfg::kRowsB;
+          for (int kb = 0; kb < num_kb; ++kb, ++it) {
+            const int s = it % Cfg::kStages;
+            const uint32_t ph = (it / Cfg::kStages) & 1u;
+            mbar_wait(&empty_bar[s], ph ^ 1u);
+            if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * Cfg::kStageBytes);
+            uint8_t* base = smem + s * Cfg::kStageBytes;
+            load_operand_2sm<A_MN, Cfg::kRowsA>(base, &ta_hi, &full_bar[s], m0, kb * kBK);
+            load_operand_2sm<A_MN, Cfg::kRowsA>(base + Cfg::kABytes, &ta_lo, &full_bar[s], m0, kb * kBK);
+            load_operand_2sm<B_MN, Cfg::kRowsB>(base + 2 * Cfg::kABytes, &tb_hi, &full_bar[s], n0, kb * kBK);
+            load_operand_2sm<B_MN, Cfg::kRowsB>(base + 2 * Cfg::kABytes + Cfg::kBBytes, &tb_lo, &full_bar[s], n0,
+                                                kb * kBK);
+          }
+        }
+      }
+    } else if (warp == 1 && leader) {
+      if (elect_one()) {
+        constexpr uint32_t idesc = idesc_tf32(256, Cfg::kPairN, A_MN, B_MN);
+        int it = 0, g = 0;
+        for (int t = cluster_id; t < num_tiles; t += nclusters) {
+          for (int c = 0; c < num_chunks; ++c, ++g) {
+            const uint32_t b = g & 1, tph = (g >> 1) & 1;
+            mbar_wait(&tempty_bar[b], tph ^ 1u);  // both CTAs' epilogues drained buffer b
+            tc_fence_after();
+            const uint32_t acc_addr = tmem + b * Cfg::kPairN;
+            const int kb_end = min(num_kb, (c + 1) * kChunkKb);
+            for (int kb = c * kChunkKb; kb < kb_end; ++kb, ++it) {
+              const int s = it % Cfg::kStages;
+              const uint32_t ph = (it / Cfg::kStages) & 1u;
+              mbar_wait(&full_bar[s], ph);
+              tc_fence_after();
+              const uint32_t base = smem_u32(smem + s * Cfg::kStageBytes);
+              const uint32_t a_hi = base, a_lo = base + Cfg::kABytes;
+              const uint32_t b_hi = base + 2 * Cfg::kABytes, b_lo = b_hi + Cfg::kBBytes;
+#pragma unroll
+              for (int kk = 0; kk < kBK / 8; ++kk) {
+                const uint32_t acc = (kb != c * kChunkKb) || kk != 0;
+                umma_tf32_2sm(acc_addr, operand_desc<A_MN>(a_lo, kk), operand_desc<B_MN>(b_hi, kk), idesc, acc);
+                umma_tf32_2sm(acc_addr, operand_desc<A_MN>(a_hi, kk), operand_desc<B_MN>(b_lo, kk), idesc, 1u);
+                umma_tf32_2sm(acc_addr, operand_desc<A_MN>(a_hi, kk), operand_desc<B_MN>(b_hi, kk), idesc, 1u);
+              }
+              umma_commit_2sm(&empty_bar[s], 0x3);  // frees this stage in both CTAs
+            }
+            umma_commit_2sm(&tfull_bar[b], 0x3);  // chunk ready in both CTAs' TMEM
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    regs_alloc<200>();
+    const uint32_t q = warp & 3u;
+    const int colbase = static_cast<int>((warp - 4) >> 2) * 128;
+    const uint32_t lane_addr = (q * 32u) << 16;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    int g = 0;
+    for (int t = cluster_id; t < num_tiles; t += nclusters) {
+      const int m0 = (t % num_m_pairs) * 256 + static_cast<int>(cta) * Cfg::kRowsA;
+      const int n0 = (t / num_m_pairs) * Cfg::kPairN + colbase;
+      float acc[128];
+#pragma unroll
+      for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+      for (int c = 0; c < num_chunks; ++c, ++g) {
+        const uint32_t b = g & 1, tph = (g >> 1) & 1;
+        mbar_wait(&tfull_bar[b], tph);
+        tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          float v[32];
+          tmem_ld_32x32b_x32(tmem + lane_addr + b * Cfg::kPairN + colbase + c0, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[c0 + j] += v[j];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader0 + b * 8);
+      }
+      const int row = m0 + static_cast<int>(q * 32 + lane);
+#pragma unroll
+      for (int c0 = 0; c0 < 128; c0 += 32)
+        if (n0 + c0 < ep.N) epilogue_chunk<EPI>(ep, acc + c0, row, n0 + c0);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem, 512);
+  }
+}
+
+}  // namespace spb

@@ -34,6 +34,7 @@ enum Epi : int {
   kEpiStoreScaled = 1, // out_f32 = alpha * acc
   kEpiDgradTanh = 2,   // out = split(acc * (1 - h[m,n]^2)), h = h_hi + h_lo
   kEpiFwdLinear = 3,   // out = split(acc + bias[n])
+  kEpiWgradUpdate = 4, // W (= out_hi + out_lo) -= lr * sgd_dir(alpha * acc), in place (single-GPU step)
 };
 
 struct GemmEpilogue {
@@ -47,7 +48,21 @@ struct GemmEpilogue {
   long ld_h;
   float alpha;
   int M, N;  // valid output extent
+  // kEpiWgradUpdate: momentum buffer (nullable) and optimizer constants.
+  float* mom;
+  float lr, mu, wd;
 };
+
+// The optimizer step on one weight (PyTorch SGD semantics, see kernels.cu
+// sgd_update_kernel): g' = g + wd*w; buf = mu*buf + g'; w -= lr*buf.
+__device__ __forceinline__ float sgd_apply(float w, float g, float* buf, float lr, float mu, float wd) {
+  g = fmaf(wd, w, g);
+  if (buf) {
+    *buf = fmaf(mu, *buf, g);
+    g = *buf;
+  }
+  return w - lr * g;
+}
 
 constexpr int kBM = 128;
 constexpr int kBK = 32;  // 32 fp32 = one 128-byte swizzle row
@@ -109,6 +124,34 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
 #pragma unroll
       for (int j = 0; j < 32; ++j)
         if (col0 + j < ep.N) o[j] = ep.alpha * v[j];
+    }
+  } else if constexpr (EPI == kEpiWgradUpdate) {
+    float* oh = ep.out_hi + row * ep.ld_out + col0;
+    float* ol = ep.out_lo + row * ep.ld_out + col0;
+    float* mb = ep.mom ? ep.mom + row * ep.ld_out + col0 : nullptr;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        const float4 h = *reinterpret_cast<const float4*>(oh + j);
+        const float4 l = *reinterpret_cast<const float4*>(ol + j);
+        float4 b = mb ? *reinterpret_cast<const float4*>(mb + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 w;
+        w.x = sgd_apply(h.x + l.x, ep.alpha * v[j], mb ? &b.x : nullptr, ep.lr, ep.mu, ep.wd);
+        w.y = sgd_apply(h.y + l.y, ep.alpha * v[j + 1], mb ? &b.y : nullptr, ep.lr, ep.mu, ep.wd);
+        w.z = sgd_apply(h.z + l.z, ep.alpha * v[j + 2], mb ? &b.z : nullptr, ep.lr, ep.mu, ep.wd);
+        w.w = sgd_apply(h.w + l.w, ep.alpha * v[j + 3], mb ? &b.w : nullptr, ep.lr, ep.mu, ep.wd);
+        store_split4(oh + j, ol + j, w);
+        if (mb) *reinterpret_cast<float4*>(mb + j) = b;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (col0 + j >= ep.N) continue;
+        const float w = sgd_apply(oh[j] + ol[j], ep.alpha * v[j], mb ? mb + j : nullptr, ep.lr, ep.mu, ep.wd);
+        const float wh = tf32_rna(w);
+        oh[j] = wh;
+        ol[j] = w - wh;
+      }
     }
   } else if constexpr (EPI == kEpiFwdTanh || EPI == kEpiFwdLinear) {
     float* oh = ep.out_hi + row * ep.ld_out + col0;

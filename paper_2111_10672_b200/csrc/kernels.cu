@@ -159,15 +159,35 @@ __global__ void colreduce_partial_kernel(const float* __restrict__ hi, const flo
   for (int o = 0; o < nvec; ++o) partial[(static_cast<long>(split) * nvec + o) * ncols + c] = acc[o];
 }
 
-// Pass 2: out = alpha * sum over splits, in split order.
+// Pass 2: g = alpha * sum over splits, in split order; either stored to
+// out, or (upd != nullptr) applied as the optimizer step to the split pair
+// out/out_lo in place (single-GPU fused update of biases and the head).
+struct UpdArgs {
+  float* lo;
+  float* mom;
+  float lr, mu, wd;
+};
 __global__ void colreduce_final_kernel(const float* __restrict__ partial, int nsplit, int nvec, int ncols, float alpha,
-                                       float* __restrict__ out, long ld_out) {
+                                       float* __restrict__ out, long ld_out, UpdArgs upd, int update) {
   const long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= static_cast<long>(nvec) * ncols) return;
   const int o = static_cast<int>(t / ncols), c = static_cast<int>(t % ncols);
   float s = 0.f;
   for (int sp = 0; sp < nsplit; ++sp) s += partial[(static_cast<long>(sp) * nvec + o) * ncols + c];
-  out[o * ld_out + c] = alpha * s;
+  const long at = o * ld_out + c;
+  if (!update) {
+    out[at] = alpha * s;
+    return;
+  }
+  float g = fmaf(upd.wd, out[at] + upd.lo[at], alpha * s);
+  if (upd.mom) {
+    upd.mom[at] = fmaf(upd.mu, upd.mom[at], g);
+    g = upd.mom[at];
+  }
+  const float w = (out[at] + upd.lo[at]) - upd.lr * g;
+  const float wh = tf32_rna(w);
+  out[at] = wh;
+  upd.lo[at] = w - wh;
 }
 
 // Fused optimizer over the flat parameter pair, float4-vectorised, grid-stride:
@@ -175,9 +195,11 @@ __global__ void colreduce_final_kernel(const float* __restrict__ partial, int ns
 //   hi = rna_tf32(w); lo = w - hi  (the split the next forward's GEMMs read)
 // With mu = wd = 0 this is the reference's x -= gamma*g (spb.cpp:196). The
 // first momentum step sees buf = 0, so buf = g' exactly as in PyTorch SGD.
-__global__ void sgd_update_kernel(float4* __restrict__ p_hi, float4* __restrict__ p_lo,
+// <= 32 registers (launch bounds) so one block can sit beside a 1-CTA GEMM
+// CTA on the same SM and stream the update while the GEMMs run.
+__global__ void __launch_bounds__(256, 8) sgd_update_kernel(float4* __restrict__ p_hi, float4* __restrict__ p_lo,
                                   const float4* __restrict__ grad, float4* __restrict__ mom, long n4, float lr,
-                                  float mu, float wd, int* step_dev) {
+                                  float mu, float wd) {
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
   for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
     const float4 h = p_hi[i], l = p_lo[i], g = __ldg(&grad[i]);
@@ -207,7 +229,6 @@ __global__ void sgd_update_kernel(float4* __restrict__ p_hi, float4* __restrict_
     p_hi[i] = make_float4(nh[0], nh[1], nh[2], nh[3]);
     p_lo[i] = make_float4(nl[0], nl[1], nl[2], nl[3]);
   }
-  if (step_dev && blockIdx.x == 0 && threadIdx.x == 0) *step_dev += 1;  // next step's Rng stream
 }
 
 __global__ void aggregate_kernel(const float* const* __restrict__ srcs, int m, long n, float* __restrict__ out) {
@@ -235,7 +256,9 @@ __global__ void join_kernel(const float* __restrict__ hi, const float* __restric
 }
 
 // Deterministic single-CTA sum of the per-row losses (warp-shuffle tree).
-__global__ void sum_loss_kernel(const float* __restrict__ row_loss, int rows, float scale, float* __restrict__ out) {
+__global__ void sum_loss_kernel(const float* __restrict__ row_loss, int rows, float scale, float* __restrict__ out,
+                                int* step_dev) {
+  if (step_dev && threadIdx.x == 0) *step_dev += 1;  // the gather already read this step's Rng stream
   __shared__ float part[32];
   float s = 0.f;
   for (int r = threadIdx.x; r < rows; r += blockDim.x) s += row_loss[r];
@@ -294,7 +317,8 @@ long colreduce_scratch(int rows, int ncols, int nvec) {
 }
 
 void launch_colreduce(const float* hi, const float* lo, long ld, int r0, int r1, int ncols, const float* rowvec,
-                      int nvec, long ldv, float alpha, float* out, long ld_out, float* scratch, cudaStream_t s) {
+                      int nvec, long ldv, float alpha, float* out, long ld_out, float* scratch, cudaStream_t s,
+                      const ColUpdate* upd) {
   if (nvec > kMaxOut) throw std::invalid_argument("colreduce: nvec > 16");
   const int rows = r1 - r0;
   if (rows <= 0 || ncols <= 0) return;
@@ -303,18 +327,20 @@ void launch_colreduce(const float* hi, const float* lo, long ld, int r0, int r1,
   colreduce_partial_kernel<<<g1, kColThreads, 0, s>>>(hi, lo, ld, r0, r1, ncols, rowvec, nvec, ldv, scratch);
   SPB_CUDA(cudaGetLastError());
   const long tot = static_cast<long>(nvec) * ncols;
+  UpdArgs u{nullptr, nullptr, 0.f, 0.f, 0.f};
+  if (upd) u = UpdArgs{upd->lo, upd->mom, upd->lr, upd->mu, upd->wd};
   colreduce_final_kernel<<<static_cast<int>((tot + 255) / 256), 256, 0, s>>>(scratch, nsplit, nvec, ncols, alpha, out,
-                                                                             ld_out);
+                                                                             ld_out, u, upd ? 1 : 0);
   SPB_CUDA(cudaGetLastError());
 }
 
 void launch_sgd_update(float* p_hi, float* p_lo, const float* grad, float* mom, long n, float lr, float momentum,
-                       float wd, int* step_dev, cudaStream_t s) {
+                       float wd, cudaStream_t s) {
   if (n % 4) throw std::invalid_argument("update: n must be a multiple of 4");
   const long n4 = n / 4;
   sgd_update_kernel<<<grid_for(n4, 256), 256, 0, s>>>(
       reinterpret_cast<float4*>(p_hi), reinterpret_cast<float4*>(p_lo), reinterpret_cast<const float4*>(grad),
-      reinterpret_cast<float4*>(mom), n4, lr, momentum, wd, step_dev);
+      reinterpret_cast<float4*>(mom), n4, lr, momentum, wd);
   SPB_CUDA(cudaGetLastError());
 }
 
@@ -336,8 +362,8 @@ void launch_join(const float* hi, const float* lo, long n, float* out, cudaStrea
   SPB_CUDA(cudaGetLastError());
 }
 
-void launch_sum_loss(const float* row_loss, int rows, float scale, float* out, cudaStream_t s) {
-  sum_loss_kernel<<<1, 1024, 0, s>>>(row_loss, rows, scale, out);
+void launch_sum_loss(const float* row_loss, int rows, float scale, float* out, int* step_dev, cudaStream_t s) {
+  sum_loss_kernel<<<1, 1024, 0, s>>>(row_loss, rows, scale, out, step_dev);
   SPB_CUDA(cudaGetLastError());
 }
 

@@ -37,7 +37,10 @@ struct Operand {
 struct GemmEpilogue;  // gemm_tf32x3.cuh
 
 // D = epi(A * B^T) over M = A.mn, N = B.mn, K = A.k. Returns kernels launched.
+// Picks the 1-CTA 128x128 or the CTA-pair 256x256 kernel by wave-quantised cost.
 int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue& ep, cudaStream_t s);
+// Test hook: -1 automatic choice, 0 force 1-CTA, 1 force CTA pair.
+void gemm_force_variant(int v);
 
 // ---- non-GEMM kernels (kernels.cu) ----
 // H0 / Ybatch rows from the dataset. Indices come from `idx` (host-provided,
@@ -61,15 +64,24 @@ void launch_head(const float* h_hi, const float* h_lo, long ldh, int rows, int n
 // (vec = 1 when rowvec == nullptr, nvec = 1), deterministic two-pass column
 // reduction. scratch must hold colreduce_scratch(...) floats.
 long colreduce_scratch(int rows, int ncols, int nvec);
+// When upd is given, the reduced gradient is applied in place as the
+// optimizer step to the split pair (out = hi, upd->lo) instead of stored.
+struct ColUpdate {
+  float* lo;
+  float* mom;
+  float lr, mu, wd;
+};
 void launch_colreduce(const float* hi, const float* lo, long ld, int r0, int r1, int ncols, const float* rowvec,
-                      int nvec, long ldv, float alpha, float* out, long ld_out, float* scratch, cudaStream_t s);
+                      int nvec, long ldv, float alpha, float* out, long ld_out, float* scratch, cudaStream_t s,
+                      const ColUpdate* upd = nullptr);
 // Optimizer over the flat parameter pair (see engine.cu).
 void launch_sgd_update(float* p_hi, float* p_lo, const float* grad, float* mom, long n, float lr, float momentum,
-                       float wd, int* step_dev, cudaStream_t s);
+                       float wd, cudaStream_t s);
 // out[c] = (sum_{w} src[w][c]) / m for w ascending (aggregate, spb.cpp:97-103).
 void launch_aggregate(const float* const* srcs_dev, int m, long n, float* out, cudaStream_t s);
 void launch_split(const float* in, long n, float* hi, float* lo, cudaStream_t s);
 void launch_join(const float* hi, const float* lo, long n, float* out, cudaStream_t s);
-void launch_sum_loss(const float* row_loss, int rows, float scale, float* out, cudaStream_t s);
+// Also advances *step_dev (nullable): the next step's Rng stream.
+void launch_sum_loss(const float* row_loss, int rows, float scale, float* out, int* step_dev, cudaStream_t s);
 
 }  // namespace spb

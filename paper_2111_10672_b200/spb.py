@@ -62,6 +62,15 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         from . import build as _build
 
         _build.build()
+    if "SPB_NCCL_LIB" not in os.environ:
+        # Share torch's NCCL when it is installed (the engine dlopens NCCL lazily).
+        import importlib.util
+
+        spec = importlib.util.find_spec("nvidia.nccl") if importlib.util.find_spec("nvidia") else None
+        if spec and spec.submodule_search_locations:
+            cand = os.path.join(list(spec.submodule_search_locations)[0], "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["SPB_NCCL_LIB"] = cand
     lib = C.CDLL(path)
     i, ip, vp, f, fp, u64 = C.c_int, C.POINTER(C.c_int), C.c_void_p, C.c_float, C.POINTER(C.c_float), C.c_uint64
     sig = {
@@ -94,6 +103,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "spb_profile_step": (i, [vp, u64, i, i, i, fp, C.POINTER(C.c_double), ip, fp]),
         "spb_time_train_steps": (i, [vp, u64, i, i, i, fp]),
         "spb_bucket_plan": (i, [i, i, i, i, ip, ip, ip]),
+        "spb_set_fused_update": (i, [vp, i]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -108,7 +118,7 @@ EXPORTED = [
     "spb_get_params", "spb_set_optimizer", "spb_partial_backprop", "spb_aggregate", "spb_train_steps",
     "spb_step_host", "spb_loss", "spb_synchronize", "spb_stream", "spb_comm_unique_id", "spb_comm_init",
     "spb_last_batch", "spb_launches_per_step", "spb_make_random_chain_mlp",
-    "spb_get_grads", "spb_profile_step", "spb_time_train_steps", "spb_bucket_plan",
+    "spb_get_grads", "spb_profile_step", "spb_time_train_steps", "spb_bucket_plan", "spb_set_fused_update",
 ]
 
 PROFILE_CLASSES = ["gemm_fwd", "gemm_wgrad", "gemm_dgrad", "head", "colreduce", "update", "gather", "comm"]
@@ -324,6 +334,10 @@ class ChainMlp:
         p, _keep = _ptrs(out)
         _check(load_library().spb_get_grads(self._ctx, p), self._ctx)
         return out
+
+    def set_fused_update(self, fused: bool):
+        """Single-GPU: optimizer inside the wgrad epilogue, or a separate pass (default)."""
+        _check(load_library().spb_set_fused_update(self._ctx, int(fused)), self._ctx)
 
     def set_optimizer(self, lr: float, momentum: float = 0.0, weight_decay: float = 0.0):
         _check(load_library().spb_set_optimizer(self._ctx, lr, momentum, weight_decay), self._ctx)

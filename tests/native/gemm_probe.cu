@@ -70,8 +70,10 @@ int main() {
         for (int q = 0; q < c.K; ++q) s += static_cast<double>(A[static_cast<long>(i) * c.K + q]) * B[static_cast<long>(j) * c.K + q];
         R[static_cast<long>(i) * c.N + j] = s;
       }
+    for (int variant = 0; variant < 2; ++variant)
     for (int am = 0; am < 2; ++am)
       for (int bm = 0; bm < 2; ++bm) {
+        gemm_force_variant(variant);
         long lda, ldb;
         Dev a = upload(A, c.M, c.K, am, lda), b = upload(B, c.N, c.K, bm, ldb);
         float* out;
@@ -98,7 +100,8 @@ int main() {
             mx = std::max(mx, std::fabs(d));
           }
         const double rel = std::sqrt(num / (den > 0 ? den : 1));
-        std::printf("case am=%d bm=%d M=%d N=%d K=%d rel_err=%.3e max_abs=%.3e %s\n", am, bm, c.M, c.N, c.K, rel, mx,
+        std::printf("case %s am=%d bm=%d M=%d N=%d K=%d rel_err=%.3e max_abs=%.3e %s\n", variant ? "2sm" : "1sm", am, bm,
+                    c.M, c.N, c.K, rel, mx,
                     e == cudaSuccess ? "" : cudaGetErrorString(e));
         if (!(rel <= 2e-6) || e != cudaSuccess) ++bad;
         cudaFree(a.hi), cudaFree(a.lo), cudaFree(b.hi), cudaFree(b.lo), cudaFree(out);

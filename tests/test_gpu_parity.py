@@ -145,15 +145,18 @@ def test_aggregate_hand_example():
     assert agg[0][0] == -2.5
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("widths,N,k,bw", [([3, 5, 4, 1], 32, 3, 2), ([37, 33, 20, 1], 100, 4, 5),
                                           ([128, 96, 80, 64, 48, 1], 256, 8, 16), ([784, 512, 512, 1], 4096, 4, 128)])
-def test_spb_step_batches_grads_and_weights(orc, widths, N, k, bw):
+def test_spb_step_batches_grads_and_weights(orc, widths, N, k, bw, fused):
     """One device SPB step: batch indices bit-exact, the aggregated gradient
-    within 1e-5 of the oracle's aggregate, weights within 1e-4; then 5 steps."""
+    (unfused path) within 1e-5 of the oracle's aggregate, weights within 1e-4
+    (fused and unfused optimizer); then 5 steps."""
     m, X, Y, W = make(widths, N, 13, k=k, bw=bw)
     L = len(widths) - 1
     lr, seed = 0.05, 11
     m.set_optimizer(lr)
+    m.set_fused_update(fused)
     m.train_steps(seed, 1, 1)
     got = m.last_batch(k * bw)
     grads, covs = [], []
@@ -164,8 +167,9 @@ def test_spb_step_batches_grads_and_weights(orc, widths, N, k, bw):
         grads.append(g)
         covs.append(c)
     agg = orc.aggregate(grads, covs, k)
-    for l, (a, b) in enumerate(zip(m.get_grads(), agg)):
-        assert rel_err(a, b) <= GRAD_TOL, (l, rel_err(a, b))
+    if not fused:
+        for l, (a, b) in enumerate(zip(m.get_grads(), agg)):
+            assert rel_err(a, b) <= GRAD_TOL, (l, rel_err(a, b))
     P = [b.copy() for b in W]
     orc.spb_step(widths, X, Y, P, k, k * bw, lr, seed, 1)
     for a, b in zip(m.get_params(), P):
@@ -200,6 +204,7 @@ def test_golden_g3_ragged_aggregate(orc):
     k, bw = int(g["k"]), int(g["bw"])
     m, X, Y, W = make(widths, int(g["samples"]), int(g["seed"]), k=k, bw=bw)
     m.set_optimizer(0.0)
+    m.set_fused_update(False)
     m.train_steps(int(g["step_seed"]), 1, 1)
     for gr, p in zip(m.get_grads(), unpack_blocks(g, "agg", len(widths) - 1)):
         idx, val, norm, size = p
@@ -216,7 +221,9 @@ def test_golden_g4_cfg1():
     m, *_ = make(widths, int(g["samples"]), int(g["seed"]), k=k, bw=bw)
     m.set_optimizer(float(g["lr"]))
     L = len(widths) - 1
+    m.set_fused_update(False)  # step 1 unfused (aggregate readable), steps 2..10 fused
     m.train_steps(int(g["step_seed"]), 1, 1)
+    m.set_fused_update(True)
     for gr, p in zip(m.get_grads(), unpack_blocks(g, "agg", L)):
         idx, val, norm, size = p
         assert rel_err(gr[idx], val) <= GRAD_TOL
@@ -254,13 +261,16 @@ def test_k1_spb_equals_full_backprop_bitwise():
         assert np.array_equal(x, y)
 
 
-def test_momentum_weight_decay_restatement(orc):
+@pytest.mark.parametrize("fused", [False, True])
+def test_momentum_weight_decay_restatement(orc, fused):
     """Momentum SGD + wd (parity unpinned by the reference):
-    device update vs the oracle's PyTorch-semantics restatement over 3 steps."""
+    device update (separate kernel, or fused into the wgrad epilogue) vs the
+    oracle's PyTorch-semantics restatement over 3 steps."""
     widths, N, k, bw = [37, 33, 20, 1], 100, 4, 5
     lr, mu, wd, seed = 0.05, 0.9, 1e-2, 11
     m, X, Y, W = make(widths, N, 17, k=k, bw=bw)
     m.set_optimizer(lr, mu, wd)
+    m.set_fused_update(fused)
     L = len(widths) - 1
     P = [b.copy() for b in W]
     bufs = [np.zeros_like(b) for b in W]
@@ -310,6 +320,7 @@ def test_deep_wide_step_properties():
     del X, Y, W
     L = len(widths) - 1
     m.set_optimizer(0.0)
+    m.set_fused_update(False)
     m.train_steps(11, 1, 1)
     agg = m.get_grads()
     batches = m.last_batch(k * bw)
@@ -319,6 +330,7 @@ def test_deep_wide_step_properties():
     for a, b in zip(agg, ref):
         assert rel_err(a, b) <= 1e-5
     m.set_optimizer(0.01)
+    m.set_fused_update(True)
     l0 = m.train_steps(11, 2, 1, losses=True)[0]
     ls = m.train_steps(11, 3, 20, losses=True)
     assert np.isfinite(ls).all()
