@@ -120,7 +120,8 @@ struct Engine {
   // row workspace
   int cap_rows = 0;
   std::vector<float*> Hh, Hl;
-  float *Dh[2] = {nullptr, nullptr}, *Dl[2] = {nullptr, nullptr};
+  static constexpr int kDbuf = 3;  // Delta_l lives in buffer l % 3
+  float *Dh[kDbuf] = {nullptr, nullptr, nullptr}, *Dl[kDbuf] = {nullptr, nullptr, nullptr};
   float *delta = nullptr, *row_loss = nullptr, *ybatch = nullptr, *scratch = nullptr, *scratch2 = nullptr,
         *xin = nullptr;
   long scratch_n = 0;
@@ -129,6 +130,8 @@ struct Engine {
   float* loss_dev = nullptr;
   float* tmp = nullptr;
   long tmp_n = 0;
+  float* splitk_ws = nullptr;  // split-K partials (forward / dgrad GEMMs, stream s only)
+  static constexpr long kSplitkWsFloats = 16L << 20;
   Ctl* ctl = nullptr;
   int* workers_dev = nullptr;
   std::vector<int> workers;  // hosted workers, ascending
@@ -198,11 +201,12 @@ struct Engine {
     auto f = [](void* p) {
       if (p) cudaFree(p);
     };
+    f(splitk_ws);
     f(p_hi), f(p_lo), f(grad), f(mom), f(X), f(Y), f(delta), f(row_loss), f(ybatch), f(scratch), f(scratch2), f(xin), f(idx),
         f(idx_in), f(loss_dev), f(tmp), f(ctl), f(workers_dev);
     for (auto p : Hh) f(p);
     for (auto p : Hl) f(p);
-    for (int i = 0; i < 2; ++i) f(Dh[i]), f(Dl[i]);
+    for (int i = 0; i < kDbuf; ++i) f(Dh[i]), f(Dl[i]);
     if (st) cudaStreamDestroy(st);
     st = nullptr;
   }
@@ -251,6 +255,7 @@ struct Engine {
     grad = alloc<float>(nflat);
     tmp_n = maxblk;
     tmp = alloc<float>(tmp_n);
+    splitk_ws = alloc<float>(kSplitkWsFloats);
     ctl = alloc<Ctl>(1);
     loss_dev = alloc<float>(1);
     workers_dev = alloc<int>(k);
@@ -283,7 +288,7 @@ struct Engine {
     for (auto p : Hl) cudaFree(p);
     Hh.assign(L, nullptr);
     Hl.assign(L, nullptr);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kDbuf; ++i) {
       if (Dh[i]) cudaFree(Dh[i]), cudaFree(Dl[i]);
     }
     for (void* p : {(void*)delta, (void*)row_loss, (void*)ybatch, (void*)scratch, (void*)scratch2, (void*)xin, (void*)idx,
@@ -294,7 +299,7 @@ struct Engine {
       Hh[l] = alloc<float>(rows * ld[l]);
       Hl[l] = alloc<float>(rows * ld[l]);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kDbuf; ++i) {
       Dh[i] = alloc<float>(rows * ldd);
       Dl[i] = alloc<float>(rows * ldd);
     }
@@ -337,6 +342,8 @@ struct Engine {
       ep.bias_lo = p_lo + b_off[l];
       ep.M = rows;
       ep.N = w[l];
+      ep.splitk_ws = splitk_ws;
+      ep.splitk_ws_floats = kSplitkWsFloats;
       pbeg(s);
       n += gemm_tf32x3(A, B, kEpiFwdTanh, ep, s);
       pend(kClsFwd, 2.0 * rows * w[l] * w[l - 1], s);
@@ -345,8 +352,8 @@ struct Engine {
     const bool has_next = L > 1 && row0[L - 1] < rows;
     pbeg(s);
     launch_head(Hh[L - 1], Hl[L - 1], ld[L - 1], rows, w[L - 1], nout, p_hi + w_off[L], p_lo + w_off[L], ld[L - 1],
-                p_hi + b_off[L], p_lo + b_off[L], ybatch, delta, row_loss, has_next ? Dh[(L - 1) % 2] : nullptr,
-                has_next ? Dl[(L - 1) % 2] : nullptr, ldd, has_next ? row0[L - 1] : rows, false, s);
+                p_hi + b_off[L], p_lo + b_off[L], ybatch, delta, row_loss, has_next ? Dh[(L - 1) % kDbuf] : nullptr,
+                has_next ? Dl[(L - 1) % kDbuf] : nullptr, ldd, has_next ? row0[L - 1] : rows, false, s);
     launch_sum_loss(row_loss, rows, 1.0f / static_cast<float>(rows), loss_dev, step_dev, s);
     pend(kClsHead, 0, s);
     n += 2;
@@ -368,43 +375,52 @@ struct Engine {
     if (on_layer) on_layer(L, s);  // W_L: read by the head only
     // Truncated backward (model.cpp:161-185): layer l runs over its
     // contributor rows only; dgrad stops at the lowest covered layer.
-    // Unfused: wgrad_l (+ bias) runs on the side stream s2 beside dgrad_l
-    // (both only read Delta_l); dgrad_l waits for wgrad_{l+1}, which was the
-    // last reader of the Delta buffer it overwrites. Collectives and the final
-    // update wait on s2.
-    const bool two = !fused && concurrent;
+    // Two streams: dgrad_l on s (the Delta chain), wgrad_l (+ bias) on s2.
+    // Delta is triple-buffered (Delta_l in buffer l % 3), so dgrad_l only has
+    // to wait for wgrad_{l+2}, the last reader of the buffer it overwrites.
+    // Fused: wgrad_l updates W_l in place, so it also waits for dgrad_l (the
+    // last reader of W_l). Collectives and per-layer updates hang off the
+    // events recorded here.
+    const bool two = concurrent;
     if (two) {
       SPB_CUDA(cudaEventRecord(ev(kEvFork), s));
       SPB_CUDA(cudaStreamWaitEvent(s2, ev(kEvFork), 0));
     }
     cudaStream_t sw = two ? s2 : s;
+    auto ev_delta = [&](int l) { return ev(kEvLayer + 2 * l); };     // Delta_l ready (on s)
+    auto ev_wgrad = [&](int l) { return ev(kEvLayer + 2 * l + 1); }; // wgrad_l done (on s2)
+    if (two) SPB_CUDA(cudaEventRecord(ev_delta(L - 1), s));          // from the head kernel
     int l = L - 1;
     for (; l >= 1; --l) {
       if (row0[l] >= rows) break;
       const int r0 = row0[l], cnt = rows - r0;
-      const int b = l % 2;
-      auto dgrad = [&] {  // Delta_{l-1} = (Delta_l W_l) * (1 - H_{l-1}^2)
-        if (!(l > 1 && row0[l - 1] < rows)) return;
+      const int b = l % kDbuf, bn = (l - 1) % kDbuf;
+      const bool has_dgrad = l > 1 && row0[l - 1] < rows;
+      // dgrad: Delta_{l-1} = (Delta_l W_l) * (1 - H_{l-1}^2), on s.
+      if (has_dgrad) {
+        if (two && l + 2 <= L - 1) SPB_CUDA(cudaStreamWaitEvent(s, ev_wgrad(l + 2), 0));
         const int q0 = row0[l - 1], qn = rows - q0;
         Operand A{Dh[b] + q0 * ldd, Dl[b] + q0 * ldd, ldd, qn, w[l], false};
         Operand B{p_hi + w_off[l], p_lo + w_off[l], ld[l - 1], w[l - 1], w[l], true};
         GemmEpilogue ep{};
-        ep.out_hi = Dh[1 - b] + q0 * ldd;
-        ep.out_lo = Dl[1 - b] + q0 * ldd;
+        ep.out_hi = Dh[bn] + q0 * ldd;
+        ep.out_lo = Dl[bn] + q0 * ldd;
         ep.ld_out = ldd;
         ep.h_hi = Hh[l - 1] + q0 * ld[l - 1];
         ep.h_lo = Hl[l - 1] + q0 * ld[l - 1];
         ep.ld_h = ld[l - 1];
         ep.M = qn;
         ep.N = w[l - 1];
+        ep.splitk_ws = splitk_ws;
+        ep.splitk_ws_floats = kSplitkWsFloats;
         pbeg(s);
         n += gemm_tf32x3(A, B, kEpiDgradTanh, ep, s);
         pend(kClsDgrad, 2.0 * qn * w[l] * w[l - 1], s);
-      };
-      if (fused) dgrad();
-      if (two) {  // Delta_l is ready on s (head or dgrad_{l+1})
-        SPB_CUDA(cudaEventRecord(ev(kEvLayer + 2 * l), s));
-        SPB_CUDA(cudaStreamWaitEvent(s2, ev(kEvLayer + 2 * l), 0));
+      }
+      if (two) {
+        // Delta_{l-1} ready / dgrad_l (last reader of W_l) done.
+        SPB_CUDA(cudaEventRecord(ev_delta(l - 1), s));
+        SPB_CUDA(cudaStreamWaitEvent(s2, fused ? ev_delta(l - 1) : ev_delta(l), 0));
       }
       {  // wgrad: dW_l = alpha_l * Delta_l[r0:]^T H_{l-1}[r0:] (or the fused update of W_l)
         Operand A{Dh[b] + r0 * ldd, Dl[b] + r0 * ldd, ldd, w[l], cnt, true};
@@ -434,14 +450,9 @@ struct Engine {
                        fused ? p_hi + b_off[l] : grad + b_off[l], 0, scratch2, sw, fused ? &ub : nullptr);
       pend(kClsColred, 0, sw);
       n += 2;
-      if (two) {
-        SPB_CUDA(cudaEventRecord(ev(kEvLayer + 2 * l + 1), s2));  // wgrad_l done
-        // dgrad_l overwrites the Delta buffer that wgrad_{l+1} read: wait for it.
-        if (l + 1 <= L - 1) SPB_CUDA(cudaStreamWaitEvent(s, ev(kEvLayer + 2 * (l + 1) + 1), 0));
-      }
-      if (!fused) dgrad();
-      if (on_grad) n += on_grad(l, two ? s2 : s);
-      if (on_layer) on_layer(l, two ? s2 : s);  // grad of layer l final there; dgrad_l (last W_l reader) on s
+      if (two) SPB_CUDA(cudaEventRecord(ev_wgrad(l), s2));
+      if (on_grad) n += on_grad(l, sw);
+      if (on_layer) on_layer(l, sw);  // grad of layer l final on sw; dgrad_l (last W_l reader) done on s
     }
     if (two) {  // join the side stream
       SPB_CUDA(cudaEventRecord(ev(kEvJoin), s2));

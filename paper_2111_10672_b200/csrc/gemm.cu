@@ -5,6 +5,7 @@
 
 #include <mutex>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "gemm_2sm.cuh"
@@ -59,7 +60,7 @@ CUtensorMap operand_map(const Operand& X, const float* base, int tile_rows) {
 }
 
 template <int BN, bool AM, bool BM_, int EPI>
-void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
+void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, int splits = 1) {
   auto kern = gemm_tf32x3_kernel<BN, AM, BM_, EPI>;
   constexpr int smem = GemmCfg<BN>::kSmem;
   static bool configured = false;
@@ -72,8 +73,10 @@ void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cud
   const int num_kb = (A.k + kBK - 1) / kBK;
   const int num_m = (A.mn + kBM - 1) / kBM, num_n = (B.mn + BN - 1) / BN;
   const int tiles = num_m * num_n;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, 256, smem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, ep);
+  const int kbs = (num_kb + splits - 1) / splits;
+  const int units = tiles * ((num_kb + kbs - 1) / kbs);
+  const int grid = units < num_sms() ? units : num_sms();
+  kern<<<grid, 256, smem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, ep);
   SPB_CUDA(cudaGetLastError());
 }
 
@@ -105,22 +108,71 @@ void dispatch_2sm(const Operand& A, const Operand& B, const GemmEpilogue& ep, cu
   else launch_2sm<true, true, EPI>(A, B, ep, s);
 }
 
+// Split-K fixup: sum the per-split fp32 partials (in split order, so the
+// result is deterministic) and apply the real epilogue.
+template <int EPI>
+__global__ void splitk_fixup_kernel(const float* __restrict__ ws, int splits, long stride, long ldw, GemmEpilogue ep) {
+  const long n = static_cast<long>(ep.M) * ep.N;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / ep.N), c = static_cast<int>(i % ep.N);
+    float v = 0.f;
+    for (int sp = 0; sp < splits; ++sp) v += ws[sp * stride + r * ldw + c];
+    epilogue_one<EPI>(ep, v, r, c);
+  }
+}
+
+template <int EPI>
+void launch_splitk(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, int splits) {
+  const long ldw = round_up(B.mn, 4), stride = static_cast<long>(A.mn) * ldw;
+  GemmEpilogue part{};
+  part.out_hi = ep.splitk_ws;
+  part.ld_out = ldw;
+  part.alpha = 1.0f;
+  part.M = A.mn;
+  part.N = B.mn;
+  part.split_stride = stride;
+  if (!A.mn_major && !B.mn_major) launch_inst<128, false, false, kEpiStoreScaled>(A, B, part, s, splits);
+  else if (!A.mn_major && B.mn_major) launch_inst<128, false, true, kEpiStoreScaled>(A, B, part, s, splits);
+  else if (A.mn_major && !B.mn_major) launch_inst<128, true, false, kEpiStoreScaled>(A, B, part, s, splits);
+  else launch_inst<128, true, true, kEpiStoreScaled>(A, B, part, s, splits);
+  const long n = static_cast<long>(A.mn) * B.mn;
+  const int grid = static_cast<int>(std::min<long>((n + 255) / 256, 148L * 16));
+  splitk_fixup_kernel<EPI><<<grid, 256, 0, s>>>(ep.splitk_ws, splits, stride, ldw, ep);
+  SPB_CUDA(cudaGetLastError());
+}
+
 int g_force_variant = -1;  // -1 auto, 0 = 1-CTA 128x128, 1 = CTA pair 256x256
 
-// Wave-quantised cost of each variant, in units of one 1-CTA 128x128 tile.
-// A pair tile is 4 such tiles on 2 SMs at kPairSpeedup x the per-SM rate.
-bool use_2sm(int M, int N) {
-  if (g_force_variant >= 0) return g_force_variant == 1;
-  static const double ratio = [] {
-    const char* e = std::getenv("SPB_2SM_COST");
-    return e ? std::atof(e) : 0.7;
-  }();
+// Launch plan: the 1-CTA kernel with `splits` K-splits, or the CTA-pair
+// kernel. Wave-quantised cost model (microseconds) calibrated on B200 with
+// tests/native/gemm_bench.cu: a 1-CTA 128x128 work unit costs
+// 0.62 us per k-block + 2.8 us; a 256x256 pair tile 1.0 us per k-block +
+// 5.6 us on 2 SMs; a split-K fixup streams (splits + 2) M x N floats.
+struct Plan {
+  bool two_sm;
+  int splits;
+};
+
+Plan plan_gemm(int M, int N, int K, long ws_floats, bool can_split) {
   const int sms = num_sms();
+  const int kb = (K + kBK - 1) / kBK;
   const long t1 = static_cast<long>((M + 127) / 128) * ((N + 127) / 128);
   const long t2 = static_cast<long>((M + 255) / 256) * ((N + 255) / 256);
-  const double c1 = static_cast<double>((t1 + sms - 1) / sms);
-  const double c2 = static_cast<double>((t2 + sms / 2 - 1) / (sms / 2)) * 2.0 * ratio;
-  return c2 < c1;
+  if (g_force_variant >= 0) return {g_force_variant == 1, 1};
+  Plan best{false, 1};
+  double best_t = 1e30;
+  for (int sp = 1; sp <= 8; ++sp) {
+    if (sp > 1 && (!can_split || static_cast<long>(sp) * M * round_up(N, 4) > ws_floats || kb < 8 * sp)) break;
+    const int kbs = (kb + sp - 1) / sp;
+    const long units = t1 * ((kb + kbs - 1) / kbs);
+    double t = static_cast<double>((units + sms - 1) / sms) * (0.62 * kbs + 2.8);
+    if (sp > 1) t += 3.0 + (sp + 2.0) * M * static_cast<double>(N) * 4.0 / 4.0e6;
+    if (t < best_t) best_t = t, best = {false, sp};
+  }
+  const double t_two = static_cast<double>((t2 + sms / 2 - 1) / (sms / 2)) * (1.0 * kb + 5.6);
+  if (t_two < best_t) best = {true, 1};
+  return best;
 }
 
 template <int BN, int EPI>
@@ -141,7 +193,22 @@ int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue&
   if (A.mn <= 0 || B.mn <= 0 || A.k <= 0) return 0;
   if ((A.ld % 4) || (B.ld % 4)) throw std::invalid_argument("gemm: ld must be a multiple of 4");
   constexpr int BN = 128;
-  if (use_2sm(A.mn, B.mn)) {
+  static const bool no_split = std::getenv("SPB_NO_SPLITK") != nullptr;  // tuning experiments
+  const Plan plan = plan_gemm(A.mn, B.mn, A.k, ep.splitk_ws && !no_split ? ep.splitk_ws_floats : 0,
+                              ep.splitk_ws != nullptr && (epi == kEpiFwdTanh || epi == kEpiDgradTanh ||
+                                                          epi == kEpiFwdLinear));
+  if (plan.splits > 1) {
+    switch (epi) {
+      case kEpiFwdTanh: launch_splitk<kEpiFwdTanh>(A, B, ep, s, plan.splits); break;
+      case kEpiDgradTanh: launch_splitk<kEpiDgradTanh>(A, B, ep, s, plan.splits); break;
+      case kEpiFwdLinear: launch_splitk<kEpiFwdLinear>(A, B, ep, s, plan.splits); break;
+      default: throw std::invalid_argument("gemm: split-K not supported for this epilogue");
+    }
+    return 2;
+  }
+  // The in-place optimizer epilogue is HBM-latency bound: it always takes the
+  // pair kernel (16 epilogue warps per CTA) for its memory-level parallelism.
+  if (plan.two_sm || (epi == kEpiWgradUpdate && g_force_variant != 0)) {
     switch (epi) {
       case kEpiFwdTanh: dispatch_2sm<kEpiFwdTanh>(A, B, ep, s); break;
       case kEpiStoreScaled: dispatch_2sm<kEpiStoreScaled>(A, B, ep, s); break;

@@ -6,10 +6,14 @@
 // L2 bytes per FLOP of the 1-CTA 128 x 128 tile, which is what bounds the
 // 1-CTA kernel (tensor pipe ~60% active, profiles/r01_*).
 //
-// Roles (384 threads = 3 warpgroups, 1 CTA/SM): warp 0 TMA producer (both
+// Roles (640 threads = 5 warpgroups, 1 CTA/SM): warp 0 TMA producer (both
 // CTAs), warp 1 MMA issuer (leader only), warp 2 TMEM allocator, warp 3
-// idle; warps 4..11 epilogue: warp w drains TMEM lanes 32*(w%4)..+31 and
-// columns 128*((w-4)/4)..+127 of its CTA's 128 x 256 accumulator.
+// idle; warps 4..19 epilogue: warp w drains TMEM lanes 32*(w%4)..+31 and
+// columns 64*((w-4)/4)..+63 of its CTA's 128 x 256 accumulator (16 warps:
+// enough memory-level parallelism for the HBM-heavy fused epilogues).
+// The whole kernel fits 96 registers/thread (640 x 96 = 61440 of 64 K), so
+// no setmaxnreg rebalancing (a .dec below what ptxas allocated for the
+// producer / MMA code corrupts it).
 // Accumulation is chunked exactly as in gemm_tf32x3.cuh (kChunkKb k-blocks
 // per TMEM buffer, drained into fp32 registers), so numerics match.
 #pragma once
@@ -26,8 +30,9 @@ struct Gemm2smCfg {
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;  // 64 KB
   static constexpr int kStages = 3;
   static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
-  static constexpr int kThreads = 384;
-  static constexpr int kEpiWarps = 8;
+  static constexpr int kThreads = 640;
+  static constexpr int kEpiWarps = 16;
+  static constexpr int kEpiCols = 64;  // accumulator columns per epilogue thread
 };
 
 template <bool MN_MAJOR, int ROWS>
@@ -42,7 +47,7 @@ __device__ __forceinline__ void load_operand_2sm(uint8_t* dst, const CUtensorMap
 }
 
 template <bool A_MN, bool B_MN, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
     gemm_tf32x3_2sm_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                            const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                            int num_kb, int num_m_pairs, int num_tiles, GemmEpilogue ep) {
@@ -86,7 +91,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < 4) {
-    regs_dealloc<56>();
     if (warp == 0) {
       if (elect_one()) {
         int it = 0;
@@ -142,24 +146,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     }
     __syncwarp();
   } else {
-    regs_alloc<200>();
     const uint32_t q = warp & 3u;
-    const int colbase = static_cast<int>((warp - 4) >> 2) * 128;
+    const int colbase = static_cast<int>((warp - 4) >> 2) * Cfg::kEpiCols;
     const uint32_t lane_addr = (q * 32u) << 16;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     int g = 0;
     for (int t = cluster_id; t < num_tiles; t += nclusters) {
       const int m0 = (t % num_m_pairs) * 256 + static_cast<int>(cta) * Cfg::kRowsA;
       const int n0 = (t / num_m_pairs) * Cfg::kPairN + colbase;
-      float acc[128];
+      float acc[Cfg::kEpiCols];
 #pragma unroll
-      for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+      for (int j = 0; j < Cfg::kEpiCols; ++j) acc[j] = 0.f;
       for (int c = 0; c < num_chunks; ++c, ++g) {
         const uint32_t b = g & 1, tph = (g >> 1) & 1;
         mbar_wait(&tfull_bar[b], tph);
         tc_fence_after();
 #pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 32) {
+        for (int c0 = 0; c0 < Cfg::kEpiCols; c0 += 32) {
           float v[32];
           tmem_ld_32x32b_x32(tmem + lane_addr + b * Cfg::kPairN + colbase + c0, v);
 #pragma unroll
@@ -171,7 +174,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       }
       const int row = m0 + static_cast<int>(q * 32 + lane);
 #pragma unroll
-      for (int c0 = 0; c0 < 128; c0 += 32)
+      for (int c0 = 0; c0 < Cfg::kEpiCols; c0 += 32)
         if (n0 + c0 < ep.N) epilogue_chunk<EPI>(ep, acc + c0, row, n0 + c0);
     }
   }

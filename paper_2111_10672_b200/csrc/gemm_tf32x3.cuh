@@ -51,6 +51,12 @@ struct GemmEpilogue {
   // kEpiWgradUpdate: momentum buffer (nullable) and optimizer constants.
   float* mom;
   float lr, mu, wd;
+  // Split-K: work unit u covers K-split u / num_tiles and writes its partial
+  // sums at out_hi + split * split_stride (kEpiStoreScaled only).
+  long split_stride;
+  // Workspace the host launcher may use for split-K partials (nullable).
+  float* splitk_ws;
+  long splitk_ws_floats;
 };
 
 // The optimizer step on one weight (PyTorch SGD semantics, see kernels.cu
@@ -109,6 +115,33 @@ __device__ __forceinline__ void store_split4(float* hi, float* lo, float4 v) {
   *reinterpret_cast<float4*>(lo) = l;
 }
 
+// The epilogue of one output element (split-K fixup path).
+template <int EPI>
+__device__ __forceinline__ void epilogue_one(const GemmEpilogue& ep, float v, int row, int col) {
+  const long at = row * ep.ld_out + col;
+  if constexpr (EPI == kEpiStoreScaled) {
+    ep.out_hi[at] = ep.alpha * v;
+  } else if constexpr (EPI == kEpiFwdTanh || EPI == kEpiFwdLinear) {
+    float z = v + (ep.bias_hi[col] + ep.bias_lo[col]);
+    if (EPI == kEpiFwdTanh) z = tanhf(z);
+    const float h = tf32_rna(z);
+    ep.out_hi[at] = h;
+    ep.out_lo[at] = z - h;
+  } else if constexpr (EPI == kEpiDgradTanh) {
+    const float h = ep.h_hi[row * ep.ld_h + col] + ep.h_lo[row * ep.ld_h + col];
+    const float d = v * (1.0f - h * h);
+    const float dh = tf32_rna(d);
+    ep.out_hi[at] = dh;
+    ep.out_lo[at] = d - dh;
+  } else {
+    const float w = sgd_apply(ep.out_hi[at] + ep.out_lo[at], ep.alpha * v, ep.mom ? ep.mom + at : nullptr, ep.lr,
+                              ep.mu, ep.wd);
+    const float wh = tf32_rna(w);
+    ep.out_hi[at] = wh;
+    ep.out_lo[at] = w - wh;
+  }
+}
+
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const float* v, int row, int col0) {
   if (row >= ep.M) return;
@@ -130,18 +163,39 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
     float* ol = ep.out_lo + row * ep.ld_out + col0;
     float* mb = ep.mom ? ep.mom + row * ep.ld_out + col0 : nullptr;
     if (full) {
+      // 8-column slices, software-pipelined: the loads of slice j+1 are issued
+      // before the math and stores of slice j, so each thread keeps up to 12
+      // x 16 B in flight (x 512 epilogue threads per SM in the pair kernel).
+      float4 h0 = *reinterpret_cast<const float4*>(oh), h1 = *reinterpret_cast<const float4*>(oh + 4);
+      float4 l0 = *reinterpret_cast<const float4*>(ol), l1 = *reinterpret_cast<const float4*>(ol + 4);
+      float4 b0 = make_float4(0.f, 0.f, 0.f, 0.f), b1 = b0;
+      if (mb) b0 = *reinterpret_cast<const float4*>(mb), b1 = *reinterpret_cast<const float4*>(mb + 4);
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        const float4 h = *reinterpret_cast<const float4*>(oh + j);
-        const float4 l = *reinterpret_cast<const float4*>(ol + j);
-        float4 b = mb ? *reinterpret_cast<const float4*>(mb + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 w;
-        w.x = sgd_apply(h.x + l.x, ep.alpha * v[j], mb ? &b.x : nullptr, ep.lr, ep.mu, ep.wd);
-        w.y = sgd_apply(h.y + l.y, ep.alpha * v[j + 1], mb ? &b.y : nullptr, ep.lr, ep.mu, ep.wd);
-        w.z = sgd_apply(h.z + l.z, ep.alpha * v[j + 2], mb ? &b.z : nullptr, ep.lr, ep.mu, ep.wd);
-        w.w = sgd_apply(h.w + l.w, ep.alpha * v[j + 3], mb ? &b.w : nullptr, ep.lr, ep.mu, ep.wd);
-        store_split4(oh + j, ol + j, w);
-        if (mb) *reinterpret_cast<float4*>(mb + j) = b;
+      for (int j = 0; j < 32; j += 8) {
+        float4 nh0, nh1, nl0, nl1, nb0 = make_float4(0.f, 0.f, 0.f, 0.f), nb1 = nb0;
+        if (j + 8 < 32) {
+          nh0 = *reinterpret_cast<const float4*>(oh + j + 8);
+          nh1 = *reinterpret_cast<const float4*>(oh + j + 12);
+          nl0 = *reinterpret_cast<const float4*>(ol + j + 8);
+          nl1 = *reinterpret_cast<const float4*>(ol + j + 12);
+          if (mb) nb0 = *reinterpret_cast<const float4*>(mb + j + 8), nb1 = *reinterpret_cast<const float4*>(mb + j + 12);
+        }
+        float4 w0, w1;
+        w0.x = sgd_apply(h0.x + l0.x, ep.alpha * v[j + 0], mb ? &b0.x : nullptr, ep.lr, ep.mu, ep.wd);
+        w0.y = sgd_apply(h0.y + l0.y, ep.alpha * v[j + 1], mb ? &b0.y : nullptr, ep.lr, ep.mu, ep.wd);
+        w0.z = sgd_apply(h0.z + l0.z, ep.alpha * v[j + 2], mb ? &b0.z : nullptr, ep.lr, ep.mu, ep.wd);
+        w0.w = sgd_apply(h0.w + l0.w, ep.alpha * v[j + 3], mb ? &b0.w : nullptr, ep.lr, ep.mu, ep.wd);
+        w1.x = sgd_apply(h1.x + l1.x, ep.alpha * v[j + 4], mb ? &b1.x : nullptr, ep.lr, ep.mu, ep.wd);
+        w1.y = sgd_apply(h1.y + l1.y, ep.alpha * v[j + 5], mb ? &b1.y : nullptr, ep.lr, ep.mu, ep.wd);
+        w1.z = sgd_apply(h1.z + l1.z, ep.alpha * v[j + 6], mb ? &b1.z : nullptr, ep.lr, ep.mu, ep.wd);
+        w1.w = sgd_apply(h1.w + l1.w, ep.alpha * v[j + 7], mb ? &b1.w : nullptr, ep.lr, ep.mu, ep.wd);
+        store_split4(oh + j, ol + j, w0);
+        store_split4(oh + j + 4, ol + j + 4, w1);
+        if (mb) {
+          *reinterpret_cast<float4*>(mb + j) = b0;
+          *reinterpret_cast<float4*>(mb + j + 4) = b1;
+        }
+        if (j + 8 < 32) h0 = nh0, h1 = nh1, l0 = nl0, l1 = nl1, b0 = nb0, b1 = nb1;
       }
     } else {
 #pragma unroll
@@ -222,7 +276,8 @@ template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(256, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                        const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
-                       int num_kb, int num_m_tiles, int num_tiles, GemmEpilogue ep) {
+                       int num_kb, int num_m_tiles, int num_tiles, int kb_per_split, int num_units,
+                       GemmEpilogue ep) {
   using Cfg = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -234,7 +289,15 @@ __global__ void __launch_bounds__(256, 1)
 
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31u;
-  const int num_chunks = (num_kb + kChunkKb - 1) / kChunkKb;
+  // Work unit u -> output tile u % num_tiles, K-split u / num_tiles.
+  auto unit = [&](int u, int& m0, int& n0, int& kb0, int& kb1, int& split) {
+    const int t = u % num_tiles;
+    split = u / num_tiles;
+    m0 = (t % num_m_tiles) * kBM;
+    n0 = (t / num_m_tiles) * BN;
+    kb0 = split * kb_per_split;
+    kb1 = min(num_kb, kb0 + kb_per_split);
+  };
 
   if (warp == 0 && elect_one()) {
     tma_prefetch(&ta_hi);
@@ -262,9 +325,10 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0) {
     if (elect_one()) {
       int it = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m0 = (t % num_m_tiles) * kBM, n0 = (t / num_m_tiles) * BN;
-        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        int m0, n0, kb0, kb1, split;
+        unit(u, m0, n0, kb0, kb1, split);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % Cfg::kStages;
           const uint32_t ph = (it / Cfg::kStages) & 1u;
           mbar_wait(&empty_bar[s], ph ^ 1u);
@@ -281,14 +345,17 @@ __global__ void __launch_bounds__(256, 1)
     if (elect_one()) {
       constexpr uint32_t idesc = idesc_tf32(kBM, BN, A_MN, B_MN);
       int it = 0, g = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        int m0, n0, kb0, kb1, split;
+        unit(u, m0, n0, kb0, kb1, split);
+        const int num_chunks = (kb1 - kb0 + kChunkKb - 1) / kChunkKb;
         for (int c = 0; c < num_chunks; ++c, ++g) {
           const uint32_t b = g & 1, tph = (g >> 1) & 1;
           mbar_wait(&tempty_bar[b], tph ^ 1u);  // epilogue drained this buffer
           tc_fence_after();
           const uint32_t acc_addr = tmem + b * BN;
-          const int kb_end = min(num_kb, (c + 1) * kChunkKb);
-          for (int kb = c * kChunkKb; kb < kb_end; ++kb, ++it) {
+          const int kb_beg = kb0 + c * kChunkKb, kb_end = min(kb1, kb_beg + kChunkKb);
+          for (int kb = kb_beg; kb < kb_end; ++kb, ++it) {
             const int s = it % Cfg::kStages;
             const uint32_t ph = (it / Cfg::kStages) & 1u;
             mbar_wait(&full_bar[s], ph);
@@ -298,7 +365,7 @@ __global__ void __launch_bounds__(256, 1)
             const uint32_t b_hi = base + 2 * Cfg::kABytes, b_lo = b_hi + Cfg::kBBytes;
 #pragma unroll
             for (int kk = 0; kk < kBK / 8; ++kk) {
-              const uint32_t acc = (kb != c * kChunkKb) || kk != 0;
+              const uint32_t acc = (kb != kb_beg) || kk != 0;
               umma_tf32(acc_addr, operand_desc<A_MN>(a_lo, kk), operand_desc<B_MN>(b_hi, kk), idesc, acc);
               umma_tf32(acc_addr, operand_desc<A_MN>(a_hi, kk), operand_desc<B_MN>(b_lo, kk), idesc, 1u);
               umma_tf32(acc_addr, operand_desc<A_MN>(a_hi, kk), operand_desc<B_MN>(b_hi, kk), idesc, 1u);
@@ -313,8 +380,12 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t q = warp & 3u;
     const uint32_t lane_addr = (q * 32u) << 16;
     int g = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const int m0 = (t % num_m_tiles) * kBM, n0 = (t / num_m_tiles) * BN;
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      int m0, n0, kb0, kb1, split;
+      unit(u, m0, n0, kb0, kb1, split);
+      const int num_chunks = (kb1 - kb0 + kChunkKb - 1) / kChunkKb;
+      GemmEpilogue epu = ep;
+      if (EPI == kEpiStoreScaled) epu.out_hi = ep.out_hi + split * ep.split_stride;
       float acc[BN];
 #pragma unroll
       for (int j = 0; j < BN; ++j) acc[j] = 0.f;
@@ -336,7 +407,7 @@ __global__ void __launch_bounds__(256, 1)
       const int row = m0 + static_cast<int>(q * 32 + lane);
 #pragma unroll
       for (int c0 = 0; c0 < BN; c0 += 32)
-        if (n0 + c0 < ep.N) epilogue_chunk<EPI>(ep, acc + c0, row, n0 + c0);
+        if (n0 + c0 < ep.N) epilogue_chunk<EPI>(epu, acc + c0, row, n0 + c0);
     }
   }
   tc_fence_before();

@@ -57,6 +57,13 @@ int main() {
   };
   const Case cases[] = {{200, 300, 100}, {128, 128, 32}, {5, 7, 3}, {1024, 1024, 1024}, {333, 129, 517}, {256, 384, 4096}, {130, 260, 8192}};
   int bad = 0;
+  float *ws, *zb, *outh, *outl;
+  const long ws_floats = 16L << 20;
+  cudaMalloc(&ws, ws_floats * 4);
+  cudaMalloc(&zb, 16384 * 4);
+  cudaMemset(zb, 0, 16384 * 4);
+  cudaMalloc(&outh, 8L << 20);
+  cudaMalloc(&outl, 8L << 20);
   std::mt19937_64 rng(1234);
   std::uniform_real_distribution<float> U(-1.f, 1.f);
   for (const Case& c : cases) {
@@ -70,7 +77,7 @@ int main() {
         for (int q = 0; q < c.K; ++q) s += static_cast<double>(A[static_cast<long>(i) * c.K + q]) * B[static_cast<long>(j) * c.K + q];
         R[static_cast<long>(i) * c.N + j] = s;
       }
-    for (int variant = 0; variant < 2; ++variant)
+    for (int variant = -1; variant < 2; ++variant)
     for (int am = 0; am < 2; ++am)
       for (int bm = 0; bm < 2; ++bm) {
         gemm_force_variant(variant);
@@ -81,13 +88,27 @@ int main() {
         cudaMalloc(&out, static_cast<long>(c.M) * ldo * 4);
         cudaMemset(out, 0, static_cast<long>(c.M) * ldo * 4);
         Operand OA{a.hi, a.lo, lda, c.M, c.K, am != 0}, OB{b.hi, b.lo, ldb, c.N, c.K, bm != 0};
+        // variant -1: the automatic plan through the split-K path (linear
+        // epilogue with zero bias == the plain product).
         GemmEpilogue ep{};
-        ep.out_hi = out;
+        ep.out_hi = variant < 0 ? outh : out;
+        ep.out_lo = outl;
         ep.ld_out = ldo;
         ep.alpha = 1.0f;
         ep.M = c.M;
         ep.N = c.N;
-        gemm_tf32x3(OA, OB, kEpiStoreScaled, ep, 0);
+        ep.bias_hi = zb;
+        ep.bias_lo = zb;
+        ep.splitk_ws = ws;
+        ep.splitk_ws_floats = ws_floats;
+        gemm_tf32x3(OA, OB, variant < 0 ? kEpiFwdLinear : kEpiStoreScaled, ep, 0);
+        if (variant < 0) {  // out = hi + lo
+          std::vector<float> h(static_cast<long>(c.M) * ldo), l2(h.size());
+          cudaMemcpy(h.data(), outh, h.size() * 4, cudaMemcpyDeviceToHost);
+          cudaMemcpy(l2.data(), outl, l2.size() * 4, cudaMemcpyDeviceToHost);
+          for (size_t i = 0; i < h.size(); ++i) h[i] += l2[i];
+          cudaMemcpy(out, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
+        }
         cudaError_t e = cudaDeviceSynchronize();
         std::vector<float> got(static_cast<long>(c.M) * ldo);
         cudaMemcpy(got.data(), out, got.size() * 4, cudaMemcpyDeviceToHost);
@@ -100,7 +121,7 @@ int main() {
             mx = std::max(mx, std::fabs(d));
           }
         const double rel = std::sqrt(num / (den > 0 ? den : 1));
-        std::printf("case %s am=%d bm=%d M=%d N=%d K=%d rel_err=%.3e max_abs=%.3e %s\n", variant ? "2sm" : "1sm", am, bm,
+        std::printf("case %s am=%d bm=%d M=%d N=%d K=%d rel_err=%.3e max_abs=%.3e %s\n", variant < 0 ? "auto" : variant ? "2sm" : "1sm", am, bm,
                     c.M, c.N, c.K, rel, mx,
                     e == cudaSuccess ? "" : cudaGetErrorString(e));
         if (!(rel <= 2e-6) || e != cudaSuccess) ++bad;
