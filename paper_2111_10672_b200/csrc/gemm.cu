@@ -59,10 +59,10 @@ CUtensorMap operand_map(const Operand& X, const float* base, int tile_rows) {
   return tmap2d(base, X.mn, X.k, X.ld, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
-template <int BN, bool AM, bool BM_, int EPI>
+template <int BN, bool AM, bool BM_, int EPI, bool TMA_UPD = false>
 void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, int splits = 1) {
-  auto kern = gemm_tf32x3_kernel<BN, AM, BM_, EPI>;
-  constexpr int smem = GemmCfg<BN>::kSmem;
+  auto kern = gemm_tf32x3_kernel<BN, AM, BM_, EPI, TMA_UPD>;
+  constexpr int smem = GemmCfg<BN, TMA_UPD>::kSmem;
   static bool configured = false;
   if (!configured) {
     SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -76,7 +76,13 @@ void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cud
   const int kbs = (num_kb + splits - 1) / splits;
   const int units = tiles * ((num_kb + kbs - 1) / kbs);
   const int grid = units < num_sms() ? units : num_sms();
-  kern<<<grid, 256, smem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, ep);
+  CUtensorMap wh{}, wl{}, wm{};
+  if (TMA_UPD) {  // the W tile the optimizer epilogue updates in place: [M rows x N cols]
+    wh = tmap2d(ep.out_hi, B.mn, A.mn, ep.ld_out, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    wl = tmap2d(ep.out_lo, B.mn, A.mn, ep.ld_out, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    wm = ep.mom ? tmap2d(ep.mom, B.mn, A.mn, ep.ld_out, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B) : wh;
+  }
+  kern<<<grid, 256, smem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, ep, wh, wl, wm);
   SPB_CUDA(cudaGetLastError());
 }
 
@@ -206,9 +212,13 @@ int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue&
     }
     return 2;
   }
-  // The in-place optimizer epilogue is HBM-latency bound: it always takes the
-  // pair kernel (16 epilogue warps per CTA) for its memory-level parallelism.
-  if (plan.two_sm || (epi == kEpiWgradUpdate && g_force_variant != 0)) {
+  // The in-place optimizer epilogue is HBM bound: it always takes the 1-CTA
+  // kernel with TMA-staged W / momentum tiles (unless a test forces the pair kernel).
+  if (epi == kEpiWgradUpdate && g_force_variant != 1) {
+    launch_inst<BN, true, true, kEpiWgradUpdate, true>(A, B, ep, s);
+    return 1;
+  }
+  if (plan.two_sm) {
     switch (epi) {
       case kEpiFwdTanh: dispatch_2sm<kEpiFwdTanh>(A, B, ep, s); break;
       case kEpiStoreScaled: dispatch_2sm<kEpiStoreScaled>(A, B, ep, s); break;

@@ -50,7 +50,7 @@ template <bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
     gemm_tf32x3_2sm_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                            const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
-                           int num_kb, int num_m_pairs, int num_tiles, GemmEpilogue ep) {
+                           int num_kb, int num_m_pairs, int num_tiles, const __grid_constant__ GemmEpilogue ep) {
   using Cfg = Gemm2smCfg;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -162,11 +162,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
         mbar_wait(&tfull_bar[b], tph);
         tc_fence_after();
 #pragma unroll
-        for (int c0 = 0; c0 < Cfg::kEpiCols; c0 += 32) {
-          float v[32];
-          tmem_ld_32x32b_x32(tmem + lane_addr + b * Cfg::kPairN + colbase + c0, v);
+        for (int c0 = 0; c0 < Cfg::kEpiCols; c0 += 16) {
+          float v[16];
+          tmem_ld_32x32b_x16(tmem + lane_addr + b * Cfg::kPairN + colbase + c0, v);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) acc[c0 + j] += v[j];
+          for (int j = 0; j < 16; ++j) acc[c0 + j] += v[j];
         }
         tc_fence_before();
         __syncwarp();

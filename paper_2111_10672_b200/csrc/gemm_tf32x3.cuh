@@ -73,14 +73,25 @@ __device__ __forceinline__ float sgd_apply(float w, float g, float* buf, float l
 constexpr int kBM = 128;
 constexpr int kBK = 32;  // 32 fp32 = one 128-byte swizzle row
 
-template <int BN>
+template <int BN, bool TMA_UPD = false>
 struct GemmCfg {
   static constexpr int kABytes = kBM * kBK * 4;
   static constexpr int kBBytes = BN * kBK * 4;
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
-  static constexpr int kStages = (BN >= 256) ? 2 : 3;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kStages = TMA_UPD ? 2 : ((BN >= 256) ? 2 : 3);
+  // TMA-staged optimizer epilogue: per epilogue warp, 2 buffers x {W_hi,
+  // W_lo, mom} x one 32 x 32 fp32 tile (4 KB, 128B-swizzled).
+  static constexpr int kEpiTile = 32 * 32 * 4;
+  static constexpr int kEpiBytes = TMA_UPD ? 4 * 2 * 3 * kEpiTile : 0;
+  // stages | barrier page (1 KB) | epilogue tiles | + 1 KB alignment slack
+  static constexpr int kSmem = kStages * kStageBytes + (TMA_UPD ? 1024 + kEpiBytes : 256) + 1024;
+  static_assert(kSmem <= 232448, "exceeds 227 KB of dynamic shared memory");
 };
+
+// Element (r, c) of a 32 x 32 fp32 tile stored with the 128B swizzle.
+__device__ __forceinline__ uint32_t sw128_off(int r, int chunk16) {
+  return static_cast<uint32_t>(r * 128 + ((chunk16 ^ (r & 7)) << 4));
+}
 
 // TMA for one operand tile of ROWS (MN) x kBK (K) elements.
 template <bool MN_MAJOR, int ROWS>
@@ -142,12 +153,14 @@ __device__ __forceinline__ void epilogue_one(const GemmEpilogue& ep, float v, in
   }
 }
 
+// out_shift: split-K slice offset applied to out_hi (kEpiStoreScaled only).
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const float* v, int row, int col0) {
+__device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const float* v, int row, int col0,
+                                               long out_shift = 0) {
   if (row >= ep.M) return;
   const bool full = (col0 + 32 <= ep.N);
   if constexpr (EPI == kEpiStoreScaled) {
-    float* o = ep.out_hi + row * ep.ld_out + col0;
+    float* o = ep.out_hi + out_shift + row * ep.ld_out + col0;
     if (full) {
 #pragma unroll
       for (int j = 0; j < 32; j += 4)
@@ -272,20 +285,23 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
 // is then bounded independently of K.
 constexpr int kChunkKb = 4;  // 128 of K per TMEM chunk
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, bool A_MN, bool B_MN, int EPI, bool TMA_UPD = false>
 __global__ void __launch_bounds__(256, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                        const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                        int num_kb, int num_m_tiles, int num_tiles, int kb_per_split, int num_units,
-                       GemmEpilogue ep) {
-  using Cfg = GemmCfg<BN>;
+                       const __grid_constant__ GemmEpilogue ep, const __grid_constant__ CUtensorMap tw_hi,
+                       const __grid_constant__ CUtensorMap tw_lo, const __grid_constant__ CUtensorMap tw_mom) {
+  using Cfg = GemmCfg<BN, TMA_UPD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
   uint64_t* empty_bar = full_bar + Cfg::kStages;
   uint64_t* tfull_bar = empty_bar + Cfg::kStages;  // [2]
   uint64_t* tempty_bar = tfull_bar + 2;            // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* eload_bar = tempty_bar + 2;            // [4 warps][2 buffers] (TMA_UPD)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(eload_bar + 8);
+  uint8_t* epi_smem = smem + Cfg::kStages * Cfg::kStageBytes + 1024;  // after the barriers page
 
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31u;
@@ -314,6 +330,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&tfull_bar[b], 1);
       mbar_init(&tempty_bar[b], 4);  // one arrive per epilogue warp
     }
+    for (int i = 0; i < 8; ++i) mbar_init(&eload_bar[i], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 2 * BN);
@@ -380,12 +397,12 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t q = warp & 3u;
     const uint32_t lane_addr = (q * 32u) << 16;
     int g = 0;
+    int eload_phase[2] = {0, 0};
     for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
       int m0, n0, kb0, kb1, split;
       unit(u, m0, n0, kb0, kb1, split);
       const int num_chunks = (kb1 - kb0 + kChunkKb - 1) / kChunkKb;
-      GemmEpilogue epu = ep;
-      if (EPI == kEpiStoreScaled) epu.out_hi = ep.out_hi + split * ep.split_stride;
+      const long out_shift = EPI == kEpiStoreScaled ? split * ep.split_stride : 0;
       float acc[BN];
 #pragma unroll
       for (int j = 0; j < BN; ++j) acc[j] = 0.f;
@@ -405,9 +422,78 @@ __global__ void __launch_bounds__(256, 1)
         if (lane == 0) mbar_arrive(&tempty_bar[b]);
       }
       const int row = m0 + static_cast<int>(q * 32 + lane);
+      if constexpr (TMA_UPD) {
+        // In-place optimizer on the W tile rows [m0 + 32q, +32), columns
+        // [n0, n0 + BN): {W_hi, W_lo, mom} 32 x 32 tiles are TMA-loaded into
+        // this warp's smem (double-buffered: chunk c+1 loads while chunk c
+        // computes), updated row-per-lane from the fp32 accumulators, and
+        // TMA-stored back. TMA clips rows / columns outside W.
+        uint8_t* wbuf = epi_smem + q * (2 * 3 * Cfg::kEpiTile);
+        const int gr = m0 + static_cast<int>(q * 32);
+        const bool has_mom = ep.mom != nullptr;
+        const uint32_t tx = (has_mom ? 3 : 2) * Cfg::kEpiTile;
+        auto issue = [&](int c) {
+          uint8_t* bb = wbuf + (c & 1) * 3 * Cfg::kEpiTile;
+          uint64_t* bar = &eload_bar[q * 2 + (c & 1)];
+          mbar_arrive_expect_tx(bar, tx);
+          tma_load_2d(bb, &tw_hi, bar, n0 + c * 32, gr);
+          tma_load_2d(bb + Cfg::kEpiTile, &tw_lo, bar, n0 + c * 32, gr);
+          if (has_mom) tma_load_2d(bb + 2 * Cfg::kEpiTile, &tw_mom, bar, n0 + c * 32, gr);
+        };
+        if (lane == 0) {
+          bulk_wait_read_all();  // previous tile's stores have left these buffers
+          issue(0);
+          if (BN / 32 > 1) issue(1);
+        }
+        __syncwarp();
 #pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 32)
-        if (n0 + c0 < ep.N) epilogue_chunk<EPI>(epu, acc + c0, row, n0 + c0);
+        for (int c = 0; c < BN / 32; ++c) {
+          const int bsel = c & 1;
+          uint8_t* bb = wbuf + bsel * 3 * Cfg::kEpiTile;
+          mbar_wait(&eload_bar[q * 2 + bsel], static_cast<uint32_t>(eload_phase[bsel]));
+          eload_phase[bsel] ^= 1;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t off = sw128_off(static_cast<int>(lane), k);
+            float4* ph = reinterpret_cast<float4*>(bb + off);
+            float4* pl = reinterpret_cast<float4*>(bb + Cfg::kEpiTile + off);
+            float4* pm = reinterpret_cast<float4*>(bb + 2 * Cfg::kEpiTile + off);
+            const float4 h = *ph, l = *pl;
+            float4 b = has_mom ? *pm : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float* a = acc + c * 32 + 4 * k;
+            float4 w;
+            w.x = sgd_apply(h.x + l.x, ep.alpha * a[0], has_mom ? &b.x : nullptr, ep.lr, ep.mu, ep.wd);
+            w.y = sgd_apply(h.y + l.y, ep.alpha * a[1], has_mom ? &b.y : nullptr, ep.lr, ep.mu, ep.wd);
+            w.z = sgd_apply(h.z + l.z, ep.alpha * a[2], has_mom ? &b.z : nullptr, ep.lr, ep.mu, ep.wd);
+            w.w = sgd_apply(h.w + l.w, ep.alpha * a[3], has_mom ? &b.w : nullptr, ep.lr, ep.mu, ep.wd);
+            const float4 wh = make_float4(tf32_rna(w.x), tf32_rna(w.y), tf32_rna(w.z), tf32_rna(w.w));
+            *ph = wh;
+            *pl = make_float4(w.x - wh.x, w.y - wh.y, w.z - wh.z, w.w - wh.w);
+            if (has_mom) *pm = b;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tw_hi, bb, n0 + c * 32, gr);
+            tma_store_2d(&tw_lo, bb + Cfg::kEpiTile, n0 + c * 32, gr);
+            if (has_mom) tma_store_2d(&tw_mom, bb + 2 * Cfg::kEpiTile, n0 + c * 32, gr);
+            bulk_commit();
+            if (c + 2 < BN / 32) {
+              bulk_wait_read_all();  // this buffer's store has read smem
+              issue(c + 2);
+            }
+          }
+          __syncwarp();
+        }
+      } else {
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 32)
+          if (n0 + c0 < ep.N) epilogue_chunk<EPI>(ep, acc + c0, row, n0 + c0, out_shift);
+      }
+    }
+    if constexpr (TMA_UPD) {
+      if (lane == 0) bulk_wait_all();
+      __syncwarp();
     }
   }
   tc_fence_before();
