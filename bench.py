@@ -295,6 +295,7 @@ def run_b200(args, world, rank, local, dist):
         t0 = time.perf_counter()
         for i in range(K):
             loss = m.step_host(xs[i % nb], ys[i % nb])
+        m.synchronize()
         t_e2e = time.perf_counter() - t0
         barrier(dist)
         t_e2e = max_over_ranks(dist, t_e2e)

@@ -335,10 +335,10 @@ void launch_colreduce(const float* hi, const float* lo, long ld, int r0, int r1,
 }
 
 void launch_sgd_update(float* p_hi, float* p_lo, const float* grad, float* mom, long n, float lr, float momentum,
-                       float wd, cudaStream_t s) {
+                       float wd, cudaStream_t s, int ctas) {
   if (n % 4) throw std::invalid_argument("update: n must be a multiple of 4");
   const long n4 = n / 4;
-  sgd_update_kernel<<<grid_for(n4, 256), 256, 0, s>>>(
+  sgd_update_kernel<<<ctas > 0 ? ctas : grid_for(n4, 256), 256, 0, s>>>(
       reinterpret_cast<float4*>(p_hi), reinterpret_cast<float4*>(p_lo), reinterpret_cast<const float4*>(grad),
       reinterpret_cast<float4*>(mom), n4, lr, momentum, wd);
   SPB_CUDA(cudaGetLastError());

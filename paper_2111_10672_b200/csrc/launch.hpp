@@ -75,8 +75,9 @@ void launch_colreduce(const float* hi, const float* lo, long ld, int r0, int r1,
                       int nvec, long ldv, float alpha, float* out, long ld_out, float* scratch, cudaStream_t s,
                       const ColUpdate* upd = nullptr);
 // Optimizer over the flat parameter pair (see engine.cu).
+// ctas > 0 fixes the grid (measurement tools); 0 sizes it to the SM count.
 void launch_sgd_update(float* p_hi, float* p_lo, const float* grad, float* mom, long n, float lr, float momentum,
-                       float wd, cudaStream_t s);
+                       float wd, cudaStream_t s, int ctas = 0);
 // out[c] = (sum_{w} src[w][c]) / m for w ascending (aggregate, spb.cpp:97-103).
 void launch_aggregate(const float* const* srcs_dev, int m, long n, float* out, cudaStream_t s);
 void launch_split(const float* in, long n, float* hi, float* lo, cudaStream_t s);
