@@ -75,7 +75,9 @@ __global__ void split_rows_kernel(const float* __restrict__ x, long ldx, int col
 constexpr int kMaxOut = 16;
 
 // One warp per row (model.cpp:121-126 for layer L, :156 for the output
-// delta, :172-183 for the delta entering layer L-1).
+// delta, :172-183 for the delta entering layer L-1). Rows are read as float4
+// over the padded width ld (padding columns of H and W are zero), 4 chunks per
+// lane in flight.
 __global__ void head_kernel(const float* __restrict__ h_hi, const float* __restrict__ h_lo, long ldh, int rows,
                             int n_in, int n_out, const float* __restrict__ w_hi, const float* __restrict__ w_lo,
                             long ldw, const float* __restrict__ b_hi, const float* __restrict__ b_lo,
@@ -86,16 +88,26 @@ __global__ void head_kernel(const float* __restrict__ h_hi, const float* __restr
   const int r = blockIdx.x * warps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
-  const float* hh = h_hi + r * ldh;
-  const float* hl = h_lo + r * ldh;
+  const int n4 = static_cast<int>((n_in + 3) / 4);
+  const float4* hh = reinterpret_cast<const float4*>(h_hi + r * ldh);
+  const float4* hl = reinterpret_cast<const float4*>(h_lo + r * ldh);
   float acc[kMaxOut];
 #pragma unroll
   for (int o = 0; o < kMaxOut; ++o) acc[o] = 0.f;
-  for (int i = lane; i < n_in; i += 32) {
-    const float h = hh[i] + hl[i];
+#pragma unroll 4
+  for (int c = lane; c < n4; c += 32) {
+    const float4 a = hh[c], b = hl[c];
+    const float4 h = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 #pragma unroll
-    for (int o = 0; o < kMaxOut; ++o)
-      if (o < n_out) acc[o] = fmaf(w_hi[o * ldw + i] + w_lo[o * ldw + i], h, acc[o]);
+    for (int o = 0; o < kMaxOut; ++o) {
+      if (o >= n_out) break;
+      const float4 wa = __ldg(reinterpret_cast<const float4*>(w_hi + o * ldw) + c);
+      const float4 wb = __ldg(reinterpret_cast<const float4*>(w_lo + o * ldw) + c);
+      acc[o] = fmaf(wa.x + wb.x, h.x, acc[o]);
+      acc[o] = fmaf(wa.y + wb.y, h.y, acc[o]);
+      acc[o] = fmaf(wa.z + wb.z, h.z, acc[o]);
+      acc[o] = fmaf(wa.w + wb.w, h.w, acc[o]);
+    }
   }
   float d[kMaxOut];
   float loss = 0.f;
@@ -114,18 +126,27 @@ __global__ void head_kernel(const float* __restrict__ h_hi, const float* __restr
     row_loss[r] = loss;
   }
   if (dn_hi && r >= cont_row0) {
-    float* oh = dn_hi + r * ldd;
-    float* ol = dn_lo + r * ldd;
-    for (int i = lane; i < n_in; i += 32) {
-      float s = 0.f;
+    float4* oh = reinterpret_cast<float4*>(dn_hi + r * ldd);
+    float4* ol = reinterpret_cast<float4*>(dn_lo + r * ldd);
+#pragma unroll 4
+    for (int c = lane; c < n4; c += 32) {
+      float4 sv = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int o = 0; o < kMaxOut; ++o)
-        if (o < n_out) s = fmaf(d[o], w_hi[o * ldw + i] + w_lo[o * ldw + i], s);
-      const float h = hh[i] + hl[i];
-      const float v = s * (1.0f - h * h);
-      const float vh = tf32_rna(v);
-      oh[i] = vh;
-      ol[i] = v - vh;
+      for (int o = 0; o < kMaxOut; ++o) {
+        if (o >= n_out) break;
+        const float4 wa = __ldg(reinterpret_cast<const float4*>(w_hi + o * ldw) + c);
+        const float4 wb = __ldg(reinterpret_cast<const float4*>(w_lo + o * ldw) + c);
+        sv.x = fmaf(d[o], wa.x + wb.x, sv.x);
+        sv.y = fmaf(d[o], wa.y + wb.y, sv.y);
+        sv.z = fmaf(d[o], wa.z + wb.z, sv.z);
+        sv.w = fmaf(d[o], wa.w + wb.w, sv.w);
+      }
+      const float4 a = hh[c], b = hl[c];
+      float v[4] = {sv.x * (1.0f - (a.x + b.x) * (a.x + b.x)), sv.y * (1.0f - (a.y + b.y) * (a.y + b.y)),
+                    sv.z * (1.0f - (a.z + b.z) * (a.z + b.z)), sv.w * (1.0f - (a.w + b.w) * (a.w + b.w))};
+      const float4 vh = make_float4(tf32_rna(v[0]), tf32_rna(v[1]), tf32_rna(v[2]), tf32_rna(v[3]));
+      oh[c] = vh;
+      ol[c] = make_float4(v[0] - vh.x, v[1] - vh.y, v[2] - vh.z, v[3] - vh.w);
     }
   }
 }
@@ -145,6 +166,7 @@ __global__ void colreduce_partial_kernel(const float* __restrict__ hi, const flo
   float acc[kMaxOut];
 #pragma unroll
   for (int o = 0; o < kMaxOut; ++o) acc[o] = 0.f;
+#pragma unroll 8
   for (int r = ra; r < rb; ++r) {
     float v = hi[r * ld + c];
     if (lo) v += lo[r * ld + c];
