@@ -86,10 +86,10 @@ void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cud
   SPB_CUDA(cudaGetLastError());
 }
 
-template <bool AM, bool BM_, int EPI>
-void launch_2sm(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
-  using Cfg = Gemm2smCfg;
-  auto kern = gemm_tf32x3_2sm_kernel<AM, BM_, EPI>;
+template <bool AM, bool BM_, int EPI, int PN>
+void launch_2sm_pn(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
+  using Cfg = Gemm2smCfg<PN>;
+  auto kern = gemm_tf32x3_2sm_kernel<AM, BM_, EPI, PN>;
   static bool configured = false;
   if (!configured) {
     SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
@@ -104,6 +104,22 @@ void launch_2sm(const Operand& A, const Operand& B, const GemmEpilogue& ep, cuda
   const int clusters = tiles < pairs ? tiles : pairs;
   kern<<<2 * clusters, Cfg::kThreads, Cfg::kSmem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, ep);
   SPB_CUDA(cudaGetLastError());
+}
+
+// Pair-tile N: 240 when it turns a partial last wave into a full one.
+int pair_n_for(int M, int N) {
+  const int pairs = num_sms() / 2;
+  auto waves = [&](int pn) {
+    const long t = static_cast<long>((M + 255) / 256) * ((N + pn - 1) / pn);
+    return static_cast<double>((t + pairs - 1) / pairs) * pn;  // ~ time: waves x per-tile width
+  };
+  return waves(240) < waves(256) ? 240 : 256;
+}
+
+template <bool AM, bool BM_, int EPI>
+void launch_2sm(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
+  if (pair_n_for(A.mn, B.mn) == 240) launch_2sm_pn<AM, BM_, EPI, 240>(A, B, ep, s);
+  else launch_2sm_pn<AM, BM_, EPI, 256>(A, B, ep, s);
 }
 
 template <int EPI>
@@ -160,6 +176,8 @@ struct Plan {
   int splits;
 };
 
+int pair_n_for(int M, int N);
+
 Plan plan_gemm(int M, int N, int K, long ws_floats, bool can_split) {
   const int sms = num_sms();
   const int kb = (K + kBK - 1) / kBK;
@@ -176,7 +194,10 @@ Plan plan_gemm(int M, int N, int K, long ws_floats, bool can_split) {
     if (sp > 1) t += 3.0 + (sp + 2.0) * M * static_cast<double>(N) * 4.0 / 4.0e6;
     if (t < best_t) best_t = t, best = {false, sp};
   }
-  const double t_two = static_cast<double>((t2 + sms / 2 - 1) / (sms / 2)) * (1.0 * kb + 5.6);
+  const int pn = pair_n_for(M, N);
+  const long t2n = static_cast<long>((M + 255) / 256) * ((N + pn - 1) / pn);
+  (void)t2;
+  const double t_two = static_cast<double>((t2n + sms / 2 - 1) / (sms / 2)) * (1.0 * kb + 5.6) * pn / 256.0;
   if (t_two < best_t) best = {true, 1};
   return best;
 }

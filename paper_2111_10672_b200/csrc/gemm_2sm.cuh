@@ -21,12 +21,15 @@
 
 namespace spb {
 
+// PN: the pair tile's N (256, or 240 so that e.g. 4096 columns make 18 tiles
+// and a 1024-row forward fills 72 of the 74 SM pairs in one wave).
+template <int PN = 256>
 struct Gemm2smCfg {
-  static constexpr int kRowsA = 128;  // per CTA
-  static constexpr int kRowsB = 128;  // per CTA (pair N = 256)
-  static constexpr int kPairN = 256;
+  static constexpr int kRowsA = 128;      // per CTA
+  static constexpr int kPairN = PN;
+  static constexpr int kRowsB = PN / 2;   // per CTA
   static constexpr int kABytes = kRowsA * kBK * 4;
-  static constexpr int kBBytes = kRowsB * kBK * 4;
+  static constexpr int kBBytes = 128 * kBK * 4;  // smem slot (MN-major loads whole 32-row boxes)
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;  // 64 KB
   static constexpr int kStages = 3;
   static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
@@ -42,16 +45,19 @@ __device__ __forceinline__ void load_operand_2sm(uint8_t* dst, const CUtensorMap
     tma_load_2d_2sm(dst, tm, bar, k0, mn0);
   } else {
 #pragma unroll
-    for (int c = 0; c < ROWS / 32; ++c) tma_load_2d_2sm(dst + c * 4096, tm, bar, mn0 + c * 32, k0);
+    for (int c = 0; c < (ROWS + 31) / 32; ++c) tma_load_2d_2sm(dst + c * 4096, tm, bar, mn0 + c * 32, k0);
   }
 }
 
-template <bool A_MN, bool B_MN, int EPI>
+template <bool A_MN, bool B_MN, int EPI, int PN = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
     gemm_tf32x3_2sm_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                            const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                            int num_kb, int num_m_pairs, int num_tiles, const __grid_constant__ GemmEpilogue ep) {
-  using Cfg = Gemm2smCfg;
+  using Cfg = Gemm2smCfg<PN>;
+  // TMA bytes one CTA brings per k-block (A hi/lo + B hi/lo).
+  constexpr uint32_t kBLoaded = B_MN ? ((Cfg::kRowsB + 31) / 32) * 4096 : Cfg::kRowsB * 128;
+  constexpr uint32_t kCtaBytes = 2 * Cfg::kABytes + 2 * kBLoaded;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
@@ -101,7 +107,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
             const int s = it % Cfg::kStages;
             const uint32_t ph = (it / Cfg::kStages) & 1u;
             mbar_wait(&empty_bar[s], ph ^ 1u);
-            if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * Cfg::kStageBytes);
+            if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * kCtaBytes);
             uint8_t* base = smem + s * Cfg::kStageBytes;
             load_operand_2sm<A_MN, Cfg::kRowsA>(base, &ta_hi, &full_bar[s], m0, kb * kBK);
             load_operand_2sm<A_MN, Cfg::kRowsA>(base + Cfg::kABytes, &ta_lo, &full_bar[s], m0, kb * kBK);
@@ -148,12 +154,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
   } else {
     const uint32_t q = warp & 3u;
     const int colbase = static_cast<int>((warp - 4) >> 2) * Cfg::kEpiCols;
+    const int width = min(Cfg::kEpiCols, PN - colbase);  // this warp's accumulator columns
     const uint32_t lane_addr = (q * 32u) << 16;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     int g = 0;
     for (int t = cluster_id; t < num_tiles; t += nclusters) {
       const int m0 = (t % num_m_pairs) * 256 + static_cast<int>(cta) * Cfg::kRowsA;
-      const int n0 = (t / num_m_pairs) * Cfg::kPairN + colbase;
+      const int n_pair0 = (t / num_m_pairs) * Cfg::kPairN;
+      const int n0 = n_pair0 + colbase;
+      const int n_lim = min(ep.N, n_pair0 + PN);
       float acc[Cfg::kEpiCols];
 #pragma unroll
       for (int j = 0; j < Cfg::kEpiCols; ++j) acc[j] = 0.f;
@@ -163,6 +172,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
         tc_fence_after();
 #pragma unroll
         for (int c0 = 0; c0 < Cfg::kEpiCols; c0 += 16) {
+          if (c0 >= width) break;
           float v[16];
           tmem_ld_32x32b_x16(tmem + lane_addr + b * Cfg::kPairN + colbase + c0, v);
 #pragma unroll
@@ -175,7 +185,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       const int row = m0 + static_cast<int>(q * 32 + lane);
 #pragma unroll
       for (int c0 = 0; c0 < Cfg::kEpiCols; c0 += 32)
-        if (n0 + c0 < ep.N) epilogue_chunk<EPI>(ep, acc + c0, row, n0 + c0);
+        if (n0 + c0 < n_lim) epilogue_chunk<EPI>(ep, acc + c0, row, n0 + c0, 0, n_lim);
     }
   }
   tc_fence_before();

@@ -101,7 +101,7 @@ __device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* tm
     tma_load_2d(dst, tm, bar, k0, mn0);  // box {32 (K), ROWS (MN)}
   } else {
 #pragma unroll
-    for (int c = 0; c < ROWS / 32; ++c)  // boxes {32 (MN), 32 (K)}, 4 KB apart
+    for (int c = 0; c < (ROWS + 31) / 32; ++c)  // boxes {32 (MN), 32 (K)}, 4 KB apart
       tma_load_2d(dst + c * 4096, tm, bar, mn0 + c * 32, k0);
   }
 }
@@ -154,11 +154,14 @@ __device__ __forceinline__ void epilogue_one(const GemmEpilogue& ep, float v, in
 }
 
 // out_shift: split-K slice offset applied to out_hi (kEpiStoreScaled only).
+// n_lim: first column NOT to write (the output width, or the end of a tile
+// narrower than the 32-column chunk grid).
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const float* v, int row, int col0,
-                                               long out_shift = 0) {
+                                               long out_shift = 0, int n_lim = -1) {
+  if (n_lim < 0) n_lim = ep.N;
   if (row >= ep.M) return;
-  const bool full = (col0 + 32 <= ep.N);
+  const bool full = (col0 + 32 <= n_lim);
   if constexpr (EPI == kEpiStoreScaled) {
     float* o = ep.out_hi + out_shift + row * ep.ld_out + col0;
     if (full) {
@@ -169,7 +172,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
-        if (col0 + j < ep.N) o[j] = ep.alpha * v[j];
+        if (col0 + j < n_lim) o[j] = ep.alpha * v[j];
     }
   } else if constexpr (EPI == kEpiWgradUpdate) {
     float* oh = ep.out_hi + row * ep.ld_out + col0;
@@ -213,7 +216,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        if (col0 + j >= ep.N) continue;
+        if (col0 + j >= n_lim) continue;
         const float w = sgd_apply(oh[j] + ol[j], ep.alpha * v[j], mb ? mb + j : nullptr, ep.lr, ep.mu, ep.wd);
         const float wh = tf32_rna(w);
         oh[j] = wh;
@@ -236,7 +239,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        if (col0 + j >= ep.N) continue;
+        if (col0 + j >= n_lim) continue;
         float z = v[j] + (ep.bias_hi[col0 + j] + ep.bias_lo[col0 + j]);
         if (EPI == kEpiFwdTanh) z = tanhf(z);
         float h = tf32_rna(z);
@@ -262,7 +265,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        if (col0 + j >= ep.N) continue;
+        if (col0 + j >= n_lim) continue;
         float h = hh[j] + hl[j];
         float d = v[j] * (1.0f - h * h);
         float dh = tf32_rna(d);

@@ -36,17 +36,33 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Waits for the phase with `parity` to complete. A pipeline bug must not hang
+// the GPU: after ~20 s of waiting the kernel traps (the launch then fails with
+// an error the host reports) instead of spinning forever.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   const uint32_t a = smem_u32(bar);
-  do {
+  uint64_t t0 = 0;
+  for (uint32_t spin = 0;; ++spin) {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(a), "r"(parity)
         : "memory");
-  } while (!done);
+    if (done) return;
+    if ((spin & 0xFFFu) == 0xFFFu) {
+      const uint64_t t = globaltimer_ns();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 20000000000ull) __trap();
+    }
+  }
 }
 
 // ---- TMA ---------------------------------------------------------------------
