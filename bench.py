@@ -187,7 +187,7 @@ def run_reference_arm(args, world, rank):
         return
     value, kind, cores, sample = cpu_reference(cfg, max(1, args.steps), max(0, args.warmup), REF_BW)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator make_random_chain_mlp)",
             "config": {"workload": cfg["workload"], "k": cfg["k"], "per_worker_batch_sampled": REF_BW,
                        "global_batch": cfg["k"] * REF_BW},
@@ -222,7 +222,7 @@ def roofline_of(prof: dict, peaks, traffic=None):
 
 
 def traffic_from_profiles():
-    p = os.path.join(ROOT, "profiles", "gemm_ncu_summary.json")
+    p = os.path.join(ROOT, "profiles", "r01_gemm_fwd_ncu_full.json")
     if os.path.exists(p):
         try:
             return json.load(open(p)).get("dram_bytes_per_launch")

@@ -553,9 +553,7 @@ struct Engine {
     };
     if (comm) fork(cst, kEvStepFork);
     if (per_layer && concurrent) fork(s3, kEvUpdFork);
-    static const bool skip_update = std::getenv("SPB_DEBUG_SKIP_UPDATE") != nullptr;  // timing experiments only
     auto on_layer = [&](int l, cudaStream_t grad_stream) {
-      if (skip_update) return;
       cudaStream_t src = comm ? cst : grad_stream;
       SPB_CUDA(cudaEventRecord(ev(kEvUpd + 2 * l), s));  // dgrad_l issued before this point on s
       SPB_CUDA(cudaEventRecord(ev(kEvUpd + 2 * l + 1), src));
@@ -953,6 +951,9 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     e.rank = rank;
     e.nranks = nranks;
     SPB_CUDA(cudaStreamCreateWithFlags(&e.cst, cudaStreamNonBlocking));
+    // NCCL's kernels need SMs while the backward GEMMs run: keep some free.
+    const char* rs = std::getenv("SPB_COMM_SMS");
+    spb::gemm_reserve_sms(rs ? std::atoi(rs) : 16);
     e.buckets[0] = spb::bucket_plan(e.k, e.L, nranks, false);
     e.buckets[1] = spb::bucket_plan(e.k, e.L, nranks, true);
     e.set_workers(spb::rank_workers(e.k, e.L, rank, nranks));

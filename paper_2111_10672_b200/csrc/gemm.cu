@@ -44,6 +44,9 @@ CUtensorMap tmap2d(const float* base, long inner, long outer, long ld, int box_i
   return m;
 }
 
+int g_reserved_sms = 0;  // SMs left free for concurrent NCCL kernels (multi-GPU)
+
+// SMs a persistent GEMM grid may occupy.
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -51,7 +54,7 @@ int num_sms() {
     SPB_CUDA(cudaGetDevice(&dev));
     SPB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
   }
-  return n;
+  return std::max(2, (n - g_reserved_sms) & ~1);
 }
 
 CUtensorMap operand_map(const Operand& X, const float* base, int tile_rows) {
@@ -213,6 +216,8 @@ void dispatch_major(const Operand& A, const Operand& B, const GemmEpilogue& ep, 
 }  // namespace
 
 void gemm_force_variant(int v) { g_force_variant = v; }
+
+void gemm_reserve_sms(int n) { g_reserved_sms = n < 0 ? 0 : n; }
 
 int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue& ep, cudaStream_t s) {
   if (A.k != B.k) throw std::invalid_argument("gemm: K mismatch");

@@ -41,6 +41,8 @@ struct GemmEpilogue;  // gemm_tf32x3.cuh
 int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue& ep, cudaStream_t s);
 // Test hook: -1 automatic choice, 0 force 1-CTA, 1 force CTA pair.
 void gemm_force_variant(int v);
+// Persistent GEMM grids leave n SMs free (for NCCL kernels running beside them).
+void gemm_reserve_sms(int n);
 
 // ---- non-GEMM kernels (kernels.cu) ----
 // H0 / Ybatch rows from the dataset. Indices come from `idx` (host-provided,
