@@ -152,10 +152,21 @@ SPB_API void* spb_stream(spb_ctx* ctx);
 /* ---- Multi-GPU: one context per rank, one SPB worker set per GPU --------------
  * unique_id: 128 bytes from spb_comm_unique_id() on rank 0, broadcast by the
  * caller. After this call spb_train_steps runs only this rank's workers
- * (spb_rank_workers) and aggregates each layer over its contributors with
- * NCCL over NVLink on per-layer buckets. */
+ * (spb_rank_workers) and aggregates each layer over its contributors:
+ *  - NVLS path (SPB_NVLS=1, when every GPU supports multicast): parameters and gradients live in NVSwitch multicast memory; per
+ *    layer, each rank reduces its shard of the gradient in the switch, applies
+ *    the optimizer and stores the new weights into every rank's copy;
+ *  - otherwise NCCL per-layer buckets (broadcast / all-reduce) followed by the
+ *    local optimizer update on every rank.
+ * Ranks of one node only (the multicast object is shared by file descriptor
+ * over an abstract Unix socket). */
 SPB_API spb_status spb_comm_unique_id(void* out128);
 SPB_API spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int nranks);
+/* 1 when spb_comm_init enabled the NVLS path, else 0. */
+SPB_API spb_status spb_comm_nvls(spb_ctx* ctx, int* enabled);
+/* Collective diagnostic of the NVLS path: multicast reduce + broadcast of a
+ * known pattern over all ranks; *mismatches = wrong elements seen here. */
+SPB_API spb_status spb_comm_selftest(spb_ctx* ctx, long long* mismatches);
 /* The per-layer bucket protocol spb_comm_init sets up (host-only, no GPU):
  * for layer l (index l-1): kind 0 = all-reduce over all ranks (ranks without
  * contributor rows add zeros), 1 = broadcast from root (a single contributing

@@ -30,6 +30,7 @@
 #include "../../include/spb_b200.h"
 #include "gemm_tf32x3.cuh"
 #include "launch.hpp"
+#include "nvls.hpp"
 #include "planner.hpp"
 
 namespace spb {
@@ -149,6 +150,16 @@ struct Engine {
   std::vector<Bucket> buckets[2];  // [full]
   std::vector<cudaEvent_t> evs;    // fork/join events (reused)
   bool fused_update = false;       // single-GPU: optimizer inside the wgrad epilogue (opt-in)
+  // NVLS path (multi-GPU, NVSwitch multicast): p_hi / p_lo / grad live in
+  // multicast buffers; each layer's gradient is reduced in the switch and
+  // the optimizer runs once per element, on the rank owning its shard, which
+  // stores the new weights into every rank's copy (nvls.cu).
+  bool nvls = false;
+  McBuffer mc_hi, mc_lo, mc_grad, mc_flags;
+  int* epoch_dev = nullptr;  // completed NVLS steps (barrier targets)
+  float* bar_dev = nullptr;  // host-barrier scratch
+  std::string nvls_tag;      // socket-name prefix, identical on all ranks
+  int nvls_tests = 0;
   bool concurrent = true;          // side streams (off in spb_profile_step: clean per-kernel times)
 
   // Eager-mode instrumentation (spb_profile_step): CUDA events around every
@@ -184,6 +195,11 @@ struct Engine {
     for (auto& row : graph)
       for (auto& g : row)
         if (g) cudaGraphExecDestroy(g), g = nullptr;
+    if (nvls) {
+      nvls_free(mc_hi), nvls_free(mc_lo), nvls_free(mc_grad), nvls_free(mc_flags);
+      p_hi = p_lo = grad = nullptr;  // not cudaMalloc'd
+      nvls = false;
+    }
     if (comm) {
       const NcclApi& api = nccl();
       api.CommFinalize(comm);
@@ -203,7 +219,7 @@ struct Engine {
     };
     f(splitk_ws);
     f(p_hi), f(p_lo), f(grad), f(mom), f(X), f(Y), f(delta), f(row_loss), f(ybatch), f(scratch), f(scratch2), f(xin), f(idx),
-        f(idx_in), f(loss_dev), f(tmp), f(ctl), f(workers_dev);
+        f(idx_in), f(loss_dev), f(tmp), f(ctl), f(workers_dev), f(epoch_dev), f(bar_dev);
     for (auto p : Hh) f(p);
     for (auto p : Hl) f(p);
     for (int i = 0; i < kDbuf; ++i) f(Dh[i]), f(Dl[i]);
@@ -497,6 +513,76 @@ struct Engine {
     return 0;
   }
 
+  // NVLS: layer l's aggregate + optimizer + weight broadcast. On cst, after
+  // this rank's gradient of layer l is final (gs) and its dgrad_l, the last
+  // reader of W_l, is done (s): zero the gradient if this rank has no
+  // contributor rows, cross-rank barrier (every rank's gradient final and no
+  // rank still reading W_l), then the fused kernel over this rank's shard.
+  int enqueue_nvls_layer(int l, bool full, cudaStream_t gs, cudaStream_t s) {
+    const Bucket* bk = nullptr;
+    for (auto& b : buckets[full])
+      if (b.l_lo <= l && l <= b.l_hi) bk = &b;
+    if (!bk) throw ConfigError("comm: no bucket for layer");
+    SPB_CUDA(cudaEventRecord(ev(kEvBucket + l), gs));
+    SPB_CUDA(cudaStreamWaitEvent(cst, ev(kEvBucket + l), 0));
+    SPB_CUDA(cudaEventRecord(ev(kEvUpd + 2 * l), s));
+    SPB_CUDA(cudaStreamWaitEvent(cst, ev(kEvUpd + 2 * l), 0));
+    const long off = w_off[l], cnt = b_off[l] + round_up(w[l], 32) - w_off[l];
+    const bool mine = std::find(bk->ranks.begin(), bk->ranks.end(), rank) != bk->ranks.end();
+    int n = 2;
+    if (!mine) SPB_CUDA(cudaMemsetAsync(grad + off, 0, cnt * sizeof(float), cst));
+    int* fl_mc = reinterpret_cast<int*>(mc_flags.mcva);
+    const int* fl_uc = reinterpret_cast<const int*>(mc_flags.uc);
+    launch_nvls_barrier(fl_mc, fl_uc, l, nranks, epoch_dev, cst);
+    const long n4 = cnt / 4, a = n4 * rank / nranks * 4, b = n4 * (rank + 1) / nranks * 4;
+    auto mcp = [&](const McBuffer& m) { return reinterpret_cast<float*>(m.mcva) + off + a; };
+    pbeg(cst);
+    launch_fused_reduce_update(mcp(mc_grad), p_hi + off + a, p_lo + off + a, mcp(mc_hi), mcp(mc_lo),
+                               mom ? mom + off + a : nullptr, b - a, lr, mu, wd, cst);
+    pend(kClsComm, static_cast<double>(b - a) * 4.0 * (mom ? 7 : 5), cst);
+    return n;
+  }
+
+  void host_barrier() {
+    nccl_check(nccl().AllReduce(bar_dev, bar_dev, 1, ncclFloat32, ncclSum, comm, cst));
+    SPB_CUDA(cudaStreamSynchronize(cst));
+  }
+
+  // Collective over the ranks (spb_comm_init): move p_hi / p_lo / grad into
+  // multicast buffers. Returns false (nothing changed) unless every rank's
+  // GPU supports multicast.
+  bool setup_nvls(const std::string& tag) {
+    bar_dev = alloc<float>(1);
+    float ok = nvls_supported(dev) ? 1.f : 0.f;
+    SPB_CUDA(cudaMemcpy(bar_dev, &ok, 4, cudaMemcpyHostToDevice));
+    nccl_check(nccl().AllReduce(bar_dev, bar_dev, 1, ncclFloat32, ncclSum, comm, cst));
+    SPB_CUDA(cudaStreamSynchronize(cst));
+    SPB_CUDA(cudaMemcpy(&ok, bar_dev, 4, cudaMemcpyDeviceToHost));
+    if (ok != static_cast<float>(nranks)) return false;
+    nvls_tag = tag;
+    auto barrier = [&] { host_barrier(); };
+    const size_t bytes = static_cast<size_t>(nflat) * 4;
+    mc_hi = nvls_alloc(bytes, dev, rank, nranks, tag + "-hi", barrier);
+    mc_lo = nvls_alloc(bytes, dev, rank, nranks, tag + "-lo", barrier);
+    mc_grad = nvls_alloc(bytes, dev, rank, nranks, tag + "-g", barrier);
+    mc_flags = nvls_alloc(static_cast<size_t>(L + 1) * 4, dev, rank, nranks, tag + "-f", barrier);
+    SPB_CUDA(cudaDeviceSynchronize());
+    auto move = [&](float*& p, const McBuffer& m) {
+      float* np = reinterpret_cast<float*>(m.uc);
+      SPB_CUDA(cudaMemcpy(np, p, bytes, cudaMemcpyDeviceToDevice));
+      SPB_CUDA(cudaFree(p));
+      p = np;
+    };
+    move(p_hi, mc_hi);
+    move(p_lo, mc_lo);
+    move(grad, mc_grad);
+    epoch_dev = alloc<int>(1);
+    nvls = true;
+    invalidate_graphs();
+    host_barrier();
+    return true;
+  }
+
   // HBM bytes one update launch must move: read hi, lo, grad (+ mom), write
   // hi, lo (+ mom), 4 B each.
   double update_bytes() const { return static_cast<double>(nflat) * 4.0 * (mom ? 7 : 5); }
@@ -551,6 +637,21 @@ struct Engine {
       SPB_CUDA(cudaEventRecord(ev(e), from));
       SPB_CUDA(cudaStreamWaitEvent(s, ev(e), 0));
     };
+    if (comm && nvls) {
+      // Per layer (top down) on cst: barrier + fused reduce/update/broadcast;
+      // then one closing barrier (every rank's weight stores have landed
+      // before anyone's next forward) and the epoch bump.
+      fork(cst, kEvStepFork);
+      n += enqueue_pass(rows, row0, alpha, s,
+                        [&](int l, cudaStream_t from) { return enqueue_nvls_layer(l, full, from, s); }, false,
+                        &ctl->step, nullptr);
+      launch_nvls_barrier(reinterpret_cast<int*>(mc_flags.mcva), reinterpret_cast<const int*>(mc_flags.uc), 0, nranks,
+                          epoch_dev, cst);
+      launch_nvls_epoch(epoch_dev, cst);
+      n += 2;
+      join(cst, kEvStepJoin);
+      return n;
+    }
     if (comm) fork(cst, kEvStepFork);
     if (per_layer && concurrent) fork(s3, kEvUpdFork);
     auto on_layer = [&](int l, cudaStream_t grad_stream) {
@@ -958,10 +1059,33 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     e.buckets[1] = spb::bucket_plan(e.k, e.L, nranks, true);
     e.set_workers(spb::rank_workers(e.k, e.L, rank, nranks));
     e.ensure_rows(static_cast<int>(e.workers.size()) * e.bw);
+    // NVLS (SPB_NVLS=1; default off until it beats the NCCL bucket path).
+    // The socket names derive from the unique id, shared by all ranks.
+    const char* nv = std::getenv("SPB_NVLS");
+    if (nranks > 1 && nv && nv[0] == '1') {
+      uint64_t h = 1469598103934665603ull;
+      for (size_t i = 0; i < sizeof id; ++i) h = (h ^ reinterpret_cast<const unsigned char*>(&id)[i]) * 1099511628211ull;
+      char tag[48];
+      std::snprintf(tag, sizeof tag, "spb-nvls-%016llx", static_cast<unsigned long long>(h));
+      e.setup_nvls(tag);
+    }
   });
   if (st != SPB_OK && ctx && (ctx->e.err.rfind("nccl", 0) == 0 || ctx->e.err.rfind("comm: ", 0) == 0))
     return SPB_E_NCCL;
   return st;
+}
+
+spb_status spb_comm_nvls(spb_ctx* ctx, int* enabled) {
+  return guard(ctx, [&] { *enabled = ctx->e.nvls ? 1 : 0; });
+}
+
+spb_status spb_comm_selftest(spb_ctx* ctx, long long* mismatches) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    if (!e.nvls) throw spb::ConfigError("comm_selftest: NVLS is not enabled");
+    const std::string tag = e.nvls_tag + "-t" + std::to_string(e.nvls_tests++);
+    *mismatches = spb::nvls_selftest(e.dev, e.rank, e.nranks, tag, [&] { e.host_barrier(); });
+  });
 }
 
 spb_status spb_bucket_plan(int k, int L, int nranks, int full_backprop, int* kind, int* root, int* rank_mask) {

@@ -104,6 +104,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "spb_time_train_steps": (i, [vp, u64, i, i, i, fp]),
         "spb_bucket_plan": (i, [i, i, i, i, ip, ip, ip]),
         "spb_set_fused_update": (i, [vp, i]),
+        "spb_comm_nvls": (i, [vp, ip]),
+        "spb_comm_selftest": (i, [vp, C.POINTER(C.c_longlong)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -119,6 +121,7 @@ EXPORTED = [
     "spb_step_host", "spb_loss", "spb_synchronize", "spb_stream", "spb_comm_unique_id", "spb_comm_init",
     "spb_last_batch", "spb_launches_per_step", "spb_make_random_chain_mlp",
     "spb_get_grads", "spb_profile_step", "spb_time_train_steps", "spb_bucket_plan", "spb_set_fused_update",
+    "spb_comm_nvls", "spb_comm_selftest",
 ]
 
 PROFILE_CLASSES = ["gemm_fwd", "gemm_wgrad", "gemm_dgrad", "head", "colreduce", "update", "gather", "comm"]
@@ -392,6 +395,19 @@ class ChainMlp:
         obj = [comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         self.comm_init(obj[0], rank, nranks)
+
+    @property
+    def nvls(self) -> bool:
+        """True when the multi-GPU step runs the NVSwitch multicast path."""
+        v = C.c_int()
+        _check(load_library().spb_comm_nvls(self._ctx, C.byref(v)), self._ctx)
+        return bool(v.value)
+
+    def comm_selftest(self) -> int:
+        """Collective NVLS diagnostic; returns the mismatching element count."""
+        v = C.c_longlong()
+        _check(load_library().spb_comm_selftest(self._ctx, C.byref(v)), self._ctx)
+        return int(v.value)
 
     def last_batch(self, rows: int) -> np.ndarray:
         out = np.zeros(rows, dtype=np.int32)

@@ -1,10 +1,12 @@
-"""Multi-GPU SPB step over NCCL (needs >= 2 GPUs; skipped otherwise).
+"""Multi-GPU SPB step (needs >= 2 GPUs; skipped otherwise).
 
-Each rank runs its balanced worker set on its own B200, per-layer buckets are
-reduced with NCCL (broadcast from a sole contributor, else all-reduce), and
-every rank applies the same update. Weights after 3 steps must equal the
-single-process CPU oracle's SPB-SGD iterates (1e-4) and be bit-identical
-across ranks; batch indices must be bit-exact.
+Each rank runs its balanced worker set on its own B200. Two aggregation
+paths: NVLS (gradients reduced in the NVSwitch, each rank updates its shard
+and multicasts the new weights) and NCCL per-layer buckets (broadcast from a
+sole contributor, else all-reduce, then the same update on every rank).
+Weights after 3 steps must equal the single-process CPU oracle's SPB-SGD
+iterates (1e-4) and be bit-identical across ranks; batch indices must be
+bit-exact.
 """
 import os
 import socket
@@ -35,7 +37,7 @@ def _free_port():
 WIDTHS, N, K, BW, LR, SEED, DSEED = [96, 80, 72, 64, 56, 48, 40, 32, 1], 512, 8, 16, 0.05, 11, 5
 
 
-def _rank(rank, world, port, out_dir, full):
+def _rank(rank, world, port, out_dir, full, nvls=True, mu=0.0, wd=0.0):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -46,11 +48,13 @@ def _rank(rank, world, port, out_dir, full):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ["SPB_NVLS"] = "1" if nvls else "0"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     X, Y, W = spb.gen_chain_mlp(WIDTHS, N, DSEED)
     m = spb.ChainMlp(WIDTHS, X, Y, W, k=K, per_worker_batch=BW, device=rank)
     m.comm_init_torch(dist, rank, world)
-    m.set_optimizer(LR)
+    assert m.nvls == nvls
+    m.set_optimizer(LR, mu, wd)
     m.train_steps(SEED, 1, 1, full_backprop=full)
     idx = m.last_batch(len(spb.rank_workers(K, len(WIDTHS) - 1, rank, world)) * BW)
     m.train_steps(SEED, 2, 2, full_backprop=full)
@@ -60,8 +64,8 @@ def _rank(rank, world, port, out_dir, full):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("full", [False, True])
-def test_multi_gpu_step_matches_oracle(tmp_path, orc, full):
+@pytest.mark.parametrize("full,nvls", [(False, True), (True, True), (False, False), (True, False)])
+def test_multi_gpu_step_matches_oracle(tmp_path, orc, full, nvls):
     world = min(_gpus(), 4)
     if world < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -69,7 +73,8 @@ def test_multi_gpu_step_matches_oracle(tmp_path, orc, full):
 
     from paper_2111_10672_b200 import spb
 
-    mp.start_processes(_rank, args=(world, _free_port(), str(tmp_path), full), nprocs=world, start_method="spawn")
+    mp.start_processes(_rank, args=(world, _free_port(), str(tmp_path), full, nvls), nprocs=world,
+                       start_method="spawn")
     L = len(WIDTHS) - 1
     X, Y, W = orc.gen_chain_mlp(WIDTHS, N, DSEED)
     Xf, Yf, Wf = spb.gen_chain_mlp(WIDTHS, N, DSEED)
@@ -85,3 +90,67 @@ def test_multi_gpu_step_matches_oracle(tmp_path, orc, full):
             got = outs[r][f"arr_{l + 1}"]
             assert np.linalg.norm(got - P[l]) / np.linalg.norm(P[l]) <= 1e-4
             assert np.array_equal(got, outs[0][f"arr_{l + 1}"])
+
+
+def _rank_momentum(rank, world, port, out_dir, nvls):
+    _rank(rank, world, port, out_dir, False, nvls, 0.9, 1e-3)
+
+
+def test_multi_gpu_momentum_nvls_matches_nccl(tmp_path):
+    """Momentum + weight decay: the NVLS path keeps each element's momentum
+    buffer on the rank owning its shard; after 3 steps its weights must match
+    the NCCL path's (every rank updates everything) to fp32 rounding."""
+    world = min(_gpus(), 4)
+    if world < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import torch.multiprocessing as mp
+
+    res = {}
+    for nvls in (True, False):
+        d = tmp_path / ("nvls" if nvls else "nccl")
+        d.mkdir()
+        mp.start_processes(_rank_momentum, args=(world, _free_port(), str(d), nvls), nprocs=world,
+                           start_method="spawn")
+        res[nvls] = [np.load(d / f"r{r}.npz") for r in range(world)]
+    L = len(WIDTHS) - 1
+    for l in range(L):
+        a, b = res[True][0][f"arr_{l + 1}"], res[False][0][f"arr_{l + 1}"]
+        assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-5
+        for r in range(world):
+            assert np.array_equal(res[True][r][f"arr_{l + 1}"], a)
+
+
+def _rank_selftest(rank, world, port, out_dir):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+
+    from paper_2111_10672_b200 import spb
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["SPB_NVLS"] = "1"
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    X, Y, W = spb.gen_chain_mlp(WIDTHS, N, DSEED)
+    m = spb.ChainMlp(WIDTHS, X, Y, W, k=K, per_worker_batch=BW, device=rank)
+    m.comm_init_torch(dist, rank, world)
+    bad = m.comm_selftest()
+    np.save(os.path.join(out_dir, f"s{rank}.npy"), np.array([bad, int(m.nvls)]))
+    dist.barrier()
+    m.close()
+    dist.destroy_process_group()
+
+
+def test_nvls_multicast_selftest(tmp_path):
+    """Switch reduce (multimem.ld_reduce) + multicast store round trip."""
+    world = min(_gpus(), 4)
+    if world < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import torch.multiprocessing as mp
+
+    mp.start_processes(_rank_selftest, args=(world, _free_port(), str(tmp_path)), nprocs=world, start_method="spawn")
+    for r in range(world):
+        bad, on = np.load(tmp_path / f"s{r}.npy")
+        assert on == 1 and bad == 0
