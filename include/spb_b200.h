@@ -152,21 +152,29 @@ SPB_API void* spb_stream(spb_ctx* ctx);
 /* ---- Multi-GPU: one context per rank, one SPB worker set per GPU --------------
  * unique_id: 128 bytes from spb_comm_unique_id() on rank 0, broadcast by the
  * caller. After this call spb_train_steps runs only this rank's workers
- * (spb_rank_workers) and aggregates each layer over its contributors:
- *  - NVLS path (SPB_NVLS=1, when every GPU supports multicast): parameters and gradients live in NVSwitch multicast memory; per
- *    layer, each rank reduces its shard of the gradient in the switch, applies
- *    the optimizer and stores the new weights into every rank's copy;
- *  - otherwise NCCL per-layer buckets (broadcast / all-reduce) followed by the
- *    local optimizer update on every rank.
- * Ranks of one node only (the multicast object is shared by file descriptor
- * over an abstract Unix socket). */
+ * (spb_rank_workers) and aggregates each layer over its contributors. The
+ * aggregation mode comes from the environment variable SPB_COMM:
+ *  - "p2p" (default): each layer's parameters are sharded over the ranks;
+ *    the rank owning a shard pulls the contributors' gradients of it over
+ *    NVLink with the copy engines (CUDA IPC), applies the optimizer and the
+ *    other ranks pull the updated fp32 shard back, synchronised by
+ *    epoch-stamped device flags (no NCCL in the step);
+ *  - "nvls": parameters and gradients in NVSwitch multicast memory; each rank
+ *    reduces its shard in the switch, updates it and multicasts the weights;
+ *  - "nccl": per-layer NCCL buckets (broadcast / all-reduce), then the local
+ *    optimizer update on every rank.
+ * Ranks of one node only. */
 SPB_API spb_status spb_comm_unique_id(void* out128);
 SPB_API spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int nranks);
-/* 1 when spb_comm_init enabled the NVLS path, else 0. */
-SPB_API spb_status spb_comm_nvls(spb_ctx* ctx, int* enabled);
+/* Active aggregation mode: 0 nccl, 1 nvls, 2 p2p (-1 before spb_comm_init). */
+SPB_API spb_status spb_comm_mode(spb_ctx* ctx, int* mode);
 /* Collective diagnostic of the NVLS path: multicast reduce + broadcast of a
  * known pattern over all ranks; *mismatches = wrong elements seen here. */
 SPB_API spb_status spb_comm_selftest(spb_ctx* ctx, long long* mismatches);
+/* Collective tuning aid of the NVLS path: times the switch reduce, the
+ * multicast store and the fused reduce/update/store kernel over launch
+ * shapes on an n_floats layer; rank 0 prints one line per variant. */
+SPB_API spb_status spb_comm_bench(spb_ctx* ctx, long long n_floats, int reps);
 /* The per-layer bucket protocol spb_comm_init sets up (host-only, no GPU):
  * for layer l (index l-1): kind 0 = all-reduce over all ranks (ranks without
  * contributor rows add zeros), 1 = broadcast from root (a single contributing

@@ -31,6 +31,7 @@
 #include "gemm_tf32x3.cuh"
 #include "launch.hpp"
 #include "nvls.hpp"
+#include "p2p.hpp"
 #include "planner.hpp"
 
 namespace spb {
@@ -48,6 +49,7 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
   ncclResult_t (*CommFinalize)(ncclComm_t);
   ncclResult_t (*CommDestroy)(ncclComm_t);
   ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*);
@@ -75,6 +77,7 @@ const NcclApi& nccl() {
     api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
     api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
+    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
     api.CommFinalize = reinterpret_cast<decltype(api.CommFinalize)>(sym("ncclCommFinalize"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
     api.CommGetAsyncError = reinterpret_cast<decltype(api.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
@@ -97,7 +100,7 @@ struct Ctl {
 // Event slots (Engine::ev): fork/join of the step, per-layer backward and
 // per-layer bucket events.
 enum { kEvStepFork = 0, kEvStepJoin = 1, kEvFork = 2, kEvJoin = 3, kEvUpdFork = 4, kEvUpdJoin = 5, kEvBucket = 8,
-       kEvLayer = 8 + 1024, kEvUpd = 8 + 3072 };
+       kEvLayer = 8 + 1024, kEvUpd = 8 + 3072, kEvP2pFork = 8 + 5120, kEvP2pLayer = 8 + 5120 + 16 };
 
 // Kernel classes of spb_profile_step (index into its output arrays).
 enum { kClsFwd = 0, kClsWgrad, kClsDgrad, kClsHead, kClsColred, kClsUpdate, kClsGather, kClsComm, kNumCls };
@@ -150,6 +153,19 @@ struct Engine {
   std::vector<Bucket> buckets[2];  // [full]
   std::vector<cudaEvent_t> evs;    // fork/join events (reused)
   bool fused_update = false;       // single-GPU: optimizer inside the wgrad epilogue (opt-in)
+  // Multi-GPU aggregation mode: 0 = NCCL buckets, 1 = NVLS multicast,
+  // 2 = peer-to-peer copy-engine pulls (p2p.cu; the default).
+  int comm_mode = 0;
+  // p2p mode: fp32 weights (own shards published to the peers), epoch-stamped
+  // flags [2 * (L + 1)][nranks], gradient staging [2][nranks - 1][shard], and
+  // the peers' IPC-mapped grad / w32 / flags.
+  float* w32 = nullptr;
+  int* flags = nullptr;
+  float* stage = nullptr;
+  long stage_shard = 0;
+  PeerPtrs<int> peer_flags{};
+  std::vector<float*> peer_grad, peer_w32;
+  cudaStream_t cst2 = nullptr, s4 = nullptr;
   // NVLS path (multi-GPU, NVSwitch multicast): p_hi / p_lo / grad live in
   // multicast buffers; each layer's gradient is reduced in the switch and
   // the optimizer runs once per element, on the rank owning its shard, which
@@ -195,6 +211,24 @@ struct Engine {
     for (auto& row : graph)
       for (auto& g : row)
         if (g) cudaGraphExecDestroy(g), g = nullptr;
+    if (comm_mode == 2) {
+      // Peers may still read this rank's memory until they pass this point.
+      if (s3) cudaStreamSynchronize(s3);
+      if (s4) cudaStreamSynchronize(s4);
+      if (cst2) cudaStreamSynchronize(cst2);
+      try {
+        host_barrier();
+      } catch (...) {
+      }
+      for (int p = 0; p < nranks; ++p) {
+        if (p == rank) continue;
+        if (peer_grad[p]) cudaIpcCloseMemHandle(peer_grad[p]);
+        if (peer_w32[p]) cudaIpcCloseMemHandle(peer_w32[p]);
+        if (peer_flags.p[p]) cudaIpcCloseMemHandle(peer_flags.p[p]);
+      }
+      peer_grad.clear(), peer_w32.clear();
+      comm_mode = 0;
+    }
     if (nvls) {
       nvls_free(mc_hi), nvls_free(mc_lo), nvls_free(mc_grad), nvls_free(mc_flags);
       p_hi = p_lo = grad = nullptr;  // not cudaMalloc'd
@@ -210,6 +244,8 @@ struct Engine {
       comm = nullptr;
     }
     if (cst) cudaStreamDestroy(cst), cst = nullptr;
+    if (cst2) cudaStreamDestroy(cst2), cst2 = nullptr;
+    if (s4) cudaStreamDestroy(s4), s4 = nullptr;
     if (s2) cudaStreamDestroy(s2), s2 = nullptr;
     if (s3) cudaStreamDestroy(s3), s3 = nullptr;
     for (auto ev : evs) cudaEventDestroy(ev);
@@ -219,7 +255,8 @@ struct Engine {
     };
     f(splitk_ws);
     f(p_hi), f(p_lo), f(grad), f(mom), f(X), f(Y), f(delta), f(row_loss), f(ybatch), f(scratch), f(scratch2), f(xin), f(idx),
-        f(idx_in), f(loss_dev), f(tmp), f(ctl), f(workers_dev), f(epoch_dev), f(bar_dev);
+        f(idx_in), f(loss_dev), f(tmp), f(ctl), f(workers_dev), f(epoch_dev), f(bar_dev), f(w32), f(flags),
+        f(stage);
     for (auto p : Hh) f(p);
     for (auto p : Hl) f(p);
     for (int i = 0; i < kDbuf; ++i) f(Dh[i]), f(Dl[i]);
@@ -543,6 +580,131 @@ struct Engine {
     return n;
   }
 
+  // p2p mode, layer l (see p2p.cu for the protocol). gs: the stream that
+  // produced this rank's gradient of l; s: the main stream (dgrad_l, the last
+  // local reader of W_l, was issued on it before this call).
+  int enqueue_p2p_layer(int l, bool full, cudaStream_t gs, cudaStream_t s) {
+    const Bucket* bk = nullptr;
+    for (auto& b : buckets[full])
+      if (b.l_lo <= l && l <= b.l_hi) bk = &b;
+    if (!bk) throw ConfigError("comm: no bucket for layer");
+    unsigned contrib = 0;
+    for (int r : bk->ranks) contrib |= 1u << r;
+    const unsigned all = (nranks >= 32 ? ~0u : (1u << nranks) - 1u), others = all & ~(1u << rank);
+    const long off = w_off[l], cnt = b_off[l] + round_up(w[l], 32) - w_off[l], n4 = cnt / 4;
+    auto lo_of = [&](int r) { return n4 * r / nranks * 4; };
+    const long a = lo_of(rank), b = lo_of(rank + 1), sh = b - a;
+    auto evl = [&](int k) { return ev(kEvP2pLayer + 4 * l + k); };
+    int n = 0;
+    // 1. gradient of l final here -> G[l] to every rank.
+    launch_p2p_signal(peer_flags, 2 * l, nranks, rank, epoch_dev, gs);
+    SPB_CUDA(cudaEventRecord(evl(3), s));  // dgrad_l issued on s before this point
+    ++n;
+    // 2. copy engines: pull the contributors' gradients of this shard. Every
+    // rank's G[l] is awaited (not only the contributors'), which also orders
+    // this step's writes after every peer finished the previous step.
+    float* st_buf = stage + static_cast<long>(l % 2) * (nranks - 1) * stage_shard;
+    if (l + 2 <= L) SPB_CUDA(cudaStreamWaitEvent(cst, ev(kEvP2pLayer + 4 * (l + 2) + 1), 0));
+    launch_p2p_wait(flags, 2 * l, nranks, others, epoch_dev, cst);
+    ++n;
+    PeerPtrs<const float> src{};
+    int nsrc = 0, slot = 0;
+    pbeg(cst);
+    for (int r = 0; r < nranks; ++r) {
+      if (!(contrib >> r & 1u)) continue;
+      if (r == rank) {
+        src.p[nsrc++] = grad + off + a;
+        continue;
+      }
+      float* dst = st_buf + static_cast<long>(slot++) * stage_shard;
+      if (sh > 0) SPB_CUDA(cudaMemcpyAsync(dst, peer_grad[r] + off + a, sh * 4, cudaMemcpyDeviceToDevice, cst));
+      src.p[nsrc++] = dst;
+    }
+    pend(kClsComm, static_cast<double>(sh) * 4.0 * (nsrc - ((contrib >> rank) & 1u)), cst);
+    SPB_CUDA(cudaEventRecord(evl(0), cst));
+    // 3. shard update (SMs) -> U[l].
+    SPB_CUDA(cudaStreamWaitEvent(s3, evl(0), 0));
+    SPB_CUDA(cudaStreamWaitEvent(s3, evl(3), 0));
+    if (contrib >> rank & 1u) {
+      SPB_CUDA(cudaEventRecord(ev(kEvBucket + l), gs));
+      SPB_CUDA(cudaStreamWaitEvent(s3, ev(kEvBucket + l), 0));
+    }
+    pbeg(s3);
+    launch_p2p_update(src, nsrc, p_hi + off + a, p_lo + off + a, mom ? mom + off + a : nullptr, w32 + off + a, sh, lr, mu,
+                      wd, s3);
+    pend(kClsUpdate, static_cast<double>(sh) * 4.0 * (nsrc + (mom ? 7 : 5)), s3);
+    launch_p2p_signal(peer_flags, 2 * l + 1, nranks, rank, epoch_dev, s3);
+    SPB_CUDA(cudaEventRecord(evl(1), s3));
+    n += 2;
+    // 4. copy engines: pull every other rank's updated fp32 shard.
+    launch_p2p_wait(flags, 2 * l + 1, nranks, others, epoch_dev, cst2);
+    ++n;
+    pbeg(cst2);
+    for (int r = 0; r < nranks; ++r) {
+      if (r == rank) continue;
+      const long ra = lo_of(r), rb = lo_of(r + 1);
+      if (rb > ra)
+        SPB_CUDA(cudaMemcpyAsync(w32 + off + ra, peer_w32[r] + off + ra, (rb - ra) * 4, cudaMemcpyDeviceToDevice, cst2));
+    }
+    pend(kClsComm, static_cast<double>(cnt - sh) * 4.0, cst2);
+    SPB_CUDA(cudaEventRecord(evl(2), cst2));
+    // 5. split the pulled shards into (hi, lo) (after dgrad_l).
+    SPB_CUDA(cudaStreamWaitEvent(s4, evl(2), 0));
+    SPB_CUDA(cudaStreamWaitEvent(s4, evl(3), 0));
+    pbeg(s4);
+    launch_p2p_split(w32 + off, p_hi + off, p_lo + off, cnt, a, b, s4);
+    pend(kClsUpdate, static_cast<double>(cnt - sh) * 12.0, s4);
+    ++n;
+    return n;
+  }
+
+  // Collective over the ranks (spb_comm_init): allocate the p2p buffers and
+  // map every peer's grad / w32 / flags through CUDA IPC.
+  void setup_p2p() {
+    if (nranks > kMaxPeers) throw ConfigError("comm: p2p mode supports at most 8 ranks");
+    if (!bar_dev) bar_dev = alloc<float>(1);
+    w32 = alloc<float>(nflat);
+    flags = alloc<int>(2L * (L + 1) * nranks);
+    epoch_dev = alloc<int>(1);
+    long maxcnt = 0;
+    for (int l = 1; l <= L; ++l) maxcnt = std::max(maxcnt, b_off[l] + round_up(w[l], 32) - w_off[l]);
+    stage_shard = round_up((maxcnt / 4 + nranks - 1) / nranks * 4, 32);
+    stage = alloc<float>(2L * std::max(1, nranks - 1) * stage_shard);
+    cudaIpcMemHandle_t mine[3];
+    SPB_CUDA(cudaIpcGetMemHandle(&mine[0], grad));
+    SPB_CUDA(cudaIpcGetMemHandle(&mine[1], w32));
+    SPB_CUDA(cudaIpcGetMemHandle(&mine[2], flags));
+    const size_t hb = sizeof mine;
+    char* dbuf = nullptr;
+    SPB_CUDA(cudaMalloc(&dbuf, hb * (nranks + 1)));
+    SPB_CUDA(cudaMemcpy(dbuf, mine, hb, cudaMemcpyHostToDevice));
+    nccl_check(nccl().AllGather(dbuf, dbuf + hb, hb, ncclUint8, comm, cst));
+    SPB_CUDA(cudaStreamSynchronize(cst));
+    std::vector<cudaIpcMemHandle_t> all(3 * nranks);
+    SPB_CUDA(cudaMemcpy(all.data(), dbuf + hb, hb * nranks, cudaMemcpyDeviceToHost));
+    cudaFree(dbuf);
+    peer_grad.assign(nranks, nullptr);
+    peer_w32.assign(nranks, nullptr);
+    for (int p = 0; p < nranks; ++p) {
+      if (p == rank) {
+        peer_grad[p] = grad, peer_w32[p] = w32, peer_flags.p[p] = flags;
+        continue;
+      }
+      void* q = nullptr;
+      SPB_CUDA(cudaIpcOpenMemHandle(&q, all[3 * p + 0], cudaIpcMemLazyEnablePeerAccess));
+      peer_grad[p] = static_cast<float*>(q);
+      SPB_CUDA(cudaIpcOpenMemHandle(&q, all[3 * p + 1], cudaIpcMemLazyEnablePeerAccess));
+      peer_w32[p] = static_cast<float*>(q);
+      SPB_CUDA(cudaIpcOpenMemHandle(&q, all[3 * p + 2], cudaIpcMemLazyEnablePeerAccess));
+      peer_flags.p[p] = static_cast<int*>(q);
+    }
+    SPB_CUDA(cudaStreamCreateWithFlags(&cst2, cudaStreamNonBlocking));
+    SPB_CUDA(cudaStreamCreateWithFlags(&s4, cudaStreamNonBlocking));
+    comm_mode = 2;
+    invalidate_graphs();
+    host_barrier();
+  }
+
   void host_barrier() {
     nccl_check(nccl().AllReduce(bar_dev, bar_dev, 1, ncclFloat32, ncclSum, comm, cst));
     SPB_CUDA(cudaStreamSynchronize(cst));
@@ -637,6 +799,19 @@ struct Engine {
       SPB_CUDA(cudaEventRecord(ev(e), from));
       SPB_CUDA(cudaStreamWaitEvent(s, ev(e), 0));
     };
+    if (comm && comm_mode == 2) {
+      // Per layer (top down): G signal on the gradient stream, gradient pulls
+      // on cst, shard update on s3, weight pulls on cst2, split on s4; all
+      // joined back into s, then the epoch advances.
+      cudaStream_t side[4] = {cst, cst2, s3, s4};
+      for (int i = 0; i < 4; ++i) fork(side[i], kEvP2pFork + i);
+      n += enqueue_pass(rows, row0, alpha, s,
+                        [&](int l, cudaStream_t from) { return enqueue_p2p_layer(l, full, from, s); }, false,
+                        &ctl->step, nullptr);
+      for (int i = 0; i < 4; ++i) join(side[i], kEvP2pFork + 4 + i);
+      launch_p2p_epoch(epoch_dev, s);
+      return n + 1;
+    }
     if (comm && nvls) {
       // Per layer (top down) on cst: barrier + fused reduce/update/broadcast;
       // then one closing barrier (every rank's weight stores have landed
@@ -1059,15 +1234,19 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     e.buckets[1] = spb::bucket_plan(e.k, e.L, nranks, true);
     e.set_workers(spb::rank_workers(e.k, e.L, rank, nranks));
     e.ensure_rows(static_cast<int>(e.workers.size()) * e.bw);
-    // NVLS (SPB_NVLS=1; default off until it beats the NCCL bucket path).
-    // The socket names derive from the unique id, shared by all ranks.
-    const char* nv = std::getenv("SPB_NVLS");
-    if (nranks > 1 && nv && nv[0] == '1') {
+    // Aggregation mode: SPB_COMM = p2p (default) | nccl | nvls.
+    const char* cm = std::getenv("SPB_COMM");
+    const std::string mode = cm ? cm : "p2p";
+    if (mode != "p2p" && mode != "nccl" && mode != "nvls")
+      throw spb::ArgumentError("comm: SPB_COMM must be p2p, nccl or nvls");
+    if (nranks > 1 && mode == "p2p") e.setup_p2p();
+    if (nranks > 1 && mode == "nvls") {
+      // Socket names derive from the unique id, shared by all ranks.
       uint64_t h = 1469598103934665603ull;
       for (size_t i = 0; i < sizeof id; ++i) h = (h ^ reinterpret_cast<const unsigned char*>(&id)[i]) * 1099511628211ull;
       char tag[48];
       std::snprintf(tag, sizeof tag, "spb-nvls-%016llx", static_cast<unsigned long long>(h));
-      e.setup_nvls(tag);
+      if (e.setup_nvls(tag)) e.comm_mode = 1;
     }
   });
   if (st != SPB_OK && ctx && (ctx->e.err.rfind("nccl", 0) == 0 || ctx->e.err.rfind("comm: ", 0) == 0))
@@ -1075,8 +1254,8 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
   return st;
 }
 
-spb_status spb_comm_nvls(spb_ctx* ctx, int* enabled) {
-  return guard(ctx, [&] { *enabled = ctx->e.nvls ? 1 : 0; });
+spb_status spb_comm_mode(spb_ctx* ctx, int* mode) {
+  return guard(ctx, [&] { *mode = ctx->e.comm ? ctx->e.comm_mode : -1; });
 }
 
 spb_status spb_comm_selftest(spb_ctx* ctx, long long* mismatches) {
@@ -1085,6 +1264,15 @@ spb_status spb_comm_selftest(spb_ctx* ctx, long long* mismatches) {
     if (!e.nvls) throw spb::ConfigError("comm_selftest: NVLS is not enabled");
     const std::string tag = e.nvls_tag + "-t" + std::to_string(e.nvls_tests++);
     *mismatches = spb::nvls_selftest(e.dev, e.rank, e.nranks, tag, [&] { e.host_barrier(); });
+  });
+}
+
+spb_status spb_comm_bench(spb_ctx* ctx, long long n_floats, int reps) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    if (!e.nvls) throw spb::ConfigError("comm_bench: NVLS is not enabled");
+    const std::string tag = e.nvls_tag + "-t" + std::to_string(e.nvls_tests++);
+    spb::nvls_bench(e.dev, e.rank, e.nranks, tag, [&] { e.host_barrier(); }, n_floats, reps);
   });
 }
 

@@ -293,48 +293,99 @@ __global__ void nvls_epoch_kernel(int* epoch) { *epoch += 1; }
 //   w   = hi + lo (this rank's copy; all copies are identical)
 //   g' = g + wd*w; buf = mu*buf + g'; w -= lr*buf   (buf local to the owner)
 //   hi, lo = split(w) -> multimem.st to every rank's copy
-__global__ void fused_reduce_update_kernel(const float* __restrict__ grad_mc, const float* __restrict__ hi_uc,
-                                           const float* __restrict__ lo_uc, float* hi_mc, float* lo_mc,
-                                           float* __restrict__ mom, long n4, float lr, float mu, float wd) {
+// U independent 16-byte switch reductions in flight per thread: the
+// round trip through the switch is long, so bandwidth needs many of them.
+template <int U>
+__global__ void __launch_bounds__(256) fused_reduce_update_kernel(const float* __restrict__ grad_mc,
+                                                                  const float* __restrict__ hi_uc,
+                                                                  const float* __restrict__ lo_uc, float* hi_mc,
+                                                                  float* lo_mc, float* __restrict__ mom, long n4,
+                                                                  float lr, float mu, float wd) {
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
-  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
-    float g[4];
-    asm volatile("multimem.ld_reduce.weak.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(g[0]), "=f"(g[1]), "=f"(g[2]), "=f"(g[3])
-                 : "l"(grad_mc + 4 * i)
-                 : "memory");
-    const float4 h = reinterpret_cast<const float4*>(hi_uc)[i];
-    const float4 l = reinterpret_cast<const float4*>(lo_uc)[i];
-    float w[4] = {h.x + l.x, h.y + l.y, h.z + l.z, h.w + l.w};
-    float b[4] = {0.f, 0.f, 0.f, 0.f};
-    if (mom) {
-      const float4 m = reinterpret_cast<const float4*>(mom)[i];
-      b[0] = m.x, b[1] = m.y, b[2] = m.z, b[3] = m.w;
-    }
-    float nh[4], nl[4];
+  for (long i0 = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
+    float g[U][4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float gg = fmaf(wd, w[j], g[j]);
-      if (mom) {
-        b[j] = fmaf(mu, b[j], gg);
-        gg = b[j];
-      }
-      const float wn = w[j] - lr * gg;
-      uint32_t r;
-      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(wn));
-      nh[j] = __uint_as_float(r);
-      nl[j] = wn - nh[j];
+    for (int u = 0; u < U; ++u) {
+      const long i = i0 + u * stride;
+      if (i < n4)
+        asm volatile("multimem.ld_reduce.weak.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(g[u][0]), "=f"(g[u][1]), "=f"(g[u][2]), "=f"(g[u][3])
+                     : "l"(grad_mc + 4 * i)
+                     : "memory");
     }
-    asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(hi_mc + 4 * i), "f"(nh[0]),
-                 "f"(nh[1]), "f"(nh[2]), "f"(nh[3])
-                 : "memory");
-    asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(lo_mc + 4 * i), "f"(nl[0]),
-                 "f"(nl[1]), "f"(nl[2]), "f"(nl[3])
-                 : "memory");
-    if (mom) reinterpret_cast<float4*>(mom)[i] = make_float4(b[0], b[1], b[2], b[3]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long i = i0 + u * stride;
+      if (i >= n4) break;
+      const float4 h = reinterpret_cast<const float4*>(hi_uc)[i];
+      const float4 l = reinterpret_cast<const float4*>(lo_uc)[i];
+      float w[4] = {h.x + l.x, h.y + l.y, h.z + l.z, h.w + l.w};
+      float b[4] = {0.f, 0.f, 0.f, 0.f};
+      if (mom) {
+        const float4 m = reinterpret_cast<const float4*>(mom)[i];
+        b[0] = m.x, b[1] = m.y, b[2] = m.z, b[3] = m.w;
+      }
+      float nh[4], nl[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float gg = fmaf(wd, w[j], g[u][j]);
+        if (mom) {
+          b[j] = fmaf(mu, b[j], gg);
+          gg = b[j];
+        }
+        const float wn = w[j] - lr * gg;
+        uint32_t r;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(wn));
+        nh[j] = __uint_as_float(r);
+        nl[j] = wn - nh[j];
+      }
+      asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(hi_mc + 4 * i), "f"(nh[0]),
+                   "f"(nh[1]), "f"(nh[2]), "f"(nh[3])
+                   : "memory");
+      asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(lo_mc + 4 * i), "f"(nl[0]),
+                   "f"(nl[1]), "f"(nl[2]), "f"(nl[3])
+                   : "memory");
+      if (mom) reinterpret_cast<float4*>(mom)[i] = make_float4(b[0], b[1], b[2], b[3]);
+    }
   }
   __threadfence_system();
 }
+
+// Microbenchmark pieces: switch reduce only / multicast store only.
+template <int U>
+__global__ void __launch_bounds__(256) ldreduce_only_kernel(const float* grad_mc, float* out, long n4) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long i0 = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
+    float g[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long i = i0 + u * stride;
+      if (i < n4)
+        asm volatile("multimem.ld_reduce.weak.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(g[u][0]), "=f"(g[u][1]), "=f"(g[u][2]), "=f"(g[u][3])
+                     : "l"(grad_mc + 4 * i)
+                     : "memory");
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long i = i0 + u * stride;
+      if (i < n4) reinterpret_cast<float4*>(out)[i] = make_float4(g[u][0], g[u][1], g[u][2], g[u][3]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) mcstore_only_kernel(const float* in, float* out_mc, long n4) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 v = reinterpret_cast<const float4*>(in)[i];
+    asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(out_mc + 4 * i), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w)
+                 : "memory");
+  }
+  __threadfence_system();
+}
+
+int g_fused_unroll = 4, g_fused_blocks_per_sm = 4;
 
 // Self-test: out[i] = sum over ranks of (rank + 1) * (i + 1) via ld_reduce,
 // then multimem.st of the sum into every copy of `bcast`.
@@ -371,9 +422,88 @@ void launch_fused_reduce_update(const float* grad_mc, const float* hi_uc, const 
   if (n <= 0) return;
   if (n % 4) throw std::invalid_argument("nvls: shard must be a multiple of 4 floats");
   const long n4 = n / 4;
-  const int grid = static_cast<int>(std::min<long>((n4 + 255) / 256, 148L * 4));
-  fused_reduce_update_kernel<<<grid, 256, 0, s>>>(grad_mc, hi_uc, lo_uc, hi_mc, lo_mc, mom, n4, lr, mu, wd);
+  const int U = g_fused_unroll;
+  const int grid = static_cast<int>(std::max<long>(1, std::min<long>((n4 + 256L * U - 1) / (256L * U),
+                                                                     148L * g_fused_blocks_per_sm)));
+  switch (U) {
+    case 1: fused_reduce_update_kernel<1><<<grid, 256, 0, s>>>(grad_mc, hi_uc, lo_uc, hi_mc, lo_mc, mom, n4, lr, mu, wd); break;
+    case 2: fused_reduce_update_kernel<2><<<grid, 256, 0, s>>>(grad_mc, hi_uc, lo_uc, hi_mc, lo_mc, mom, n4, lr, mu, wd); break;
+    case 8: fused_reduce_update_kernel<8><<<grid, 256, 0, s>>>(grad_mc, hi_uc, lo_uc, hi_mc, lo_mc, mom, n4, lr, mu, wd); break;
+    default: fused_reduce_update_kernel<4><<<grid, 256, 0, s>>>(grad_mc, hi_uc, lo_uc, hi_mc, lo_mc, mom, n4, lr, mu, wd);
+  }
   SPB_CUDA(cudaGetLastError());
+}
+
+void nvls_set_launch(int unroll, int blocks_per_sm) {
+  if (unroll > 0) g_fused_unroll = unroll;
+  if (blocks_per_sm > 0) g_fused_blocks_per_sm = blocks_per_sm;
+}
+
+// Standalone timings (rank 0 prints): switch reduce only, multicast store
+// only, and the fused kernel over (unroll, blocks/SM) on this rank's shard of
+// an n-float layer, all ranks running concurrently.
+void nvls_bench(int device, int rank, int nranks, const std::string& name, const std::function<void()>& barrier, long n,
+                int reps) {
+  n = (n + 4L * nranks - 1) / (4L * nranks) * (4L * nranks);
+  McBuffer g = nvls_alloc(n * 4, device, rank, nranks, name + "-g", barrier);
+  McBuffer h = nvls_alloc(n * 4, device, rank, nranks, name + "-h", barrier);
+  McBuffer l = nvls_alloc(n * 4, device, rank, nranks, name + "-l", barrier);
+  float* mom = nullptr;
+  float* loc = nullptr;
+  SPB_CUDA(cudaMalloc(&mom, n * 4));
+  SPB_CUDA(cudaMalloc(&loc, n * 4));
+  SPB_CUDA(cudaMemset(mom, 0, n * 4));
+  SPB_CUDA(cudaMemset(loc, 0, n * 4));
+  cudaStream_t st;
+  SPB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaEvent_t e0, e1;
+  SPB_CUDA(cudaEventCreate(&e0));
+  SPB_CUDA(cudaEventCreate(&e1));
+  const long shard = n / nranks, a = shard * rank;
+  const long n4 = shard / 4;
+  auto mc = [&](const McBuffer& b) { return reinterpret_cast<float*>(b.mcva) + a; };
+  auto uc = [&](const McBuffer& b) { return reinterpret_cast<float*>(b.uc) + a; };
+  auto timeit = [&](const char* what, const std::function<void()>& body, double bytes) {
+    body();
+    SPB_CUDA(cudaStreamSynchronize(st));
+    barrier();
+    SPB_CUDA(cudaEventRecord(e0, st));
+    for (int r = 0; r < reps; ++r) body();
+    SPB_CUDA(cudaEventRecord(e1, st));
+    SPB_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    SPB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    barrier();
+    const double us = 1e3 * ms / reps;
+    if (rank == 0)
+      std::printf("nvls_bench N=%d n=%ld %-28s %9.1f us  %8.1f GB/s (shard bytes/us)\n", nranks, n, what, us,
+                  bytes / (us * 1e3));
+    std::fflush(stdout);
+  };
+  const double sb = static_cast<double>(shard) * 4.0;
+  for (int bps : {1, 2, 4, 8}) {
+    const int grid1 = static_cast<int>(std::min<long>((n4 + 1023) / 1024, 148L * bps));
+    char tag[64];
+    std::snprintf(tag, sizeof tag, "ldreduce U4 b%d", bps);
+    timeit(tag, [&] { ldreduce_only_kernel<4><<<grid1, 256, 0, st>>>(mc(g), loc, n4); }, sb);
+    std::snprintf(tag, sizeof tag, "mcstore b%d", bps);
+    const int grid2 = static_cast<int>(std::min<long>((n4 + 255) / 256, 148L * bps));
+    timeit(tag, [&] { mcstore_only_kernel<<<grid2, 256, 0, st>>>(loc, mc(h), n4); }, sb);
+  }
+  for (int U : {1, 2, 4, 8})
+    for (int bps : {1, 2, 4, 8}) {
+      nvls_set_launch(U, bps);
+      char tag[64];
+      std::snprintf(tag, sizeof tag, "fused U%d b%d", U, bps);
+      timeit(tag, [&] { launch_fused_reduce_update(mc(g), uc(h), uc(l), mc(h), mc(l), mom + a, shard, 1e-3f, 0.9f, 0.f, st); },
+             sb);
+    }
+  nvls_set_launch(4, 4);
+  SPB_CUDA(cudaStreamDestroy(st));
+  cudaEventDestroy(e0), cudaEventDestroy(e1);
+  cudaFree(mom), cudaFree(loc);
+  barrier();
+  nvls_free(g), nvls_free(h), nvls_free(l);
 }
 
 // Returns the number of mismatching elements (0 = multicast reduce + store work).

@@ -30,6 +30,9 @@ void launch_nvls_epoch(int* epoch, cudaStream_t s);
 // switch), apply the optimizer, broadcast hi / lo to every rank.
 void launch_fused_reduce_update(const float* grad_mc, const float* hi_uc, const float* lo_uc, float* hi_mc, float* lo_mc,
                                 float* mom, long n, float lr, float mu, float wd, cudaStream_t s);
+void nvls_set_launch(int unroll, int blocks_per_sm);
+void nvls_bench(int device, int rank, int nranks, const std::string& name, const std::function<void()>& barrier, long n,
+                int reps);
 long nvls_selftest(int device, int rank, int nranks, const std::string& name, const std::function<void()>& barrier);
 
 }  // namespace spb

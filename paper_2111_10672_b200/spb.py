@@ -104,8 +104,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "spb_time_train_steps": (i, [vp, u64, i, i, i, fp]),
         "spb_bucket_plan": (i, [i, i, i, i, ip, ip, ip]),
         "spb_set_fused_update": (i, [vp, i]),
-        "spb_comm_nvls": (i, [vp, ip]),
+        "spb_comm_mode": (i, [vp, ip]),
         "spb_comm_selftest": (i, [vp, C.POINTER(C.c_longlong)]),
+        "spb_comm_bench": (i, [vp, C.c_longlong, i]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -121,7 +122,7 @@ EXPORTED = [
     "spb_step_host", "spb_loss", "spb_synchronize", "spb_stream", "spb_comm_unique_id", "spb_comm_init",
     "spb_last_batch", "spb_launches_per_step", "spb_make_random_chain_mlp",
     "spb_get_grads", "spb_profile_step", "spb_time_train_steps", "spb_bucket_plan", "spb_set_fused_update",
-    "spb_comm_nvls", "spb_comm_selftest",
+    "spb_comm_mode", "spb_comm_selftest", "spb_comm_bench",
 ]
 
 PROFILE_CLASSES = ["gemm_fwd", "gemm_wgrad", "gemm_dgrad", "head", "colreduce", "update", "gather", "comm"]
@@ -397,17 +398,21 @@ class ChainMlp:
         self.comm_init(obj[0], rank, nranks)
 
     @property
-    def nvls(self) -> bool:
-        """True when the multi-GPU step runs the NVSwitch multicast path."""
+    def comm_mode(self):
+        """Multi-GPU aggregation mode: "p2p", "nvls", "nccl" (None before comm_init)."""
         v = C.c_int()
-        _check(load_library().spb_comm_nvls(self._ctx, C.byref(v)), self._ctx)
-        return bool(v.value)
+        _check(load_library().spb_comm_mode(self._ctx, C.byref(v)), self._ctx)
+        return {0: "nccl", 1: "nvls", 2: "p2p"}.get(v.value)
 
     def comm_selftest(self) -> int:
         """Collective NVLS diagnostic; returns the mismatching element count."""
         v = C.c_longlong()
         _check(load_library().spb_comm_selftest(self._ctx, C.byref(v)), self._ctx)
         return int(v.value)
+
+    def comm_bench(self, n_floats: int, reps: int = 20):
+        """Collective NVLS tuning aid (rank 0 prints the timings)."""
+        _check(load_library().spb_comm_bench(self._ctx, n_floats, reps), self._ctx)
 
     def last_batch(self, rows: int) -> np.ndarray:
         out = np.zeros(rows, dtype=np.int32)

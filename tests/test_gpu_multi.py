@@ -1,9 +1,11 @@
 """Multi-GPU SPB step (needs >= 2 GPUs; skipped otherwise).
 
-Each rank runs its balanced worker set on its own B200. Two aggregation
-paths: NVLS (gradients reduced in the NVSwitch, each rank updates its shard
-and multicasts the new weights) and NCCL per-layer buckets (broadcast from a
-sole contributor, else all-reduce, then the same update on every rank).
+Each rank runs its balanced worker set on its own B200. Three aggregation
+paths: p2p (copy-engine pulls of gradient shards, sharded update, pulls of
+the updated weights), NVLS (gradients reduced in the NVSwitch, each rank
+updates its shard and multicasts the new weights) and NCCL per-layer buckets
+(broadcast from a sole contributor, else all-reduce, then the same update on
+every rank).
 Weights after 3 steps must equal the single-process CPU oracle's SPB-SGD
 iterates (1e-4) and be bit-identical across ranks; batch indices must be
 bit-exact.
@@ -37,7 +39,7 @@ def _free_port():
 WIDTHS, N, K, BW, LR, SEED, DSEED = [96, 80, 72, 64, 56, 48, 40, 32, 1], 512, 8, 16, 0.05, 11, 5
 
 
-def _rank(rank, world, port, out_dir, full, nvls=True, mu=0.0, wd=0.0):
+def _rank(rank, world, port, out_dir, full, mode="p2p", mu=0.0, wd=0.0):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -48,12 +50,12 @@ def _rank(rank, world, port, out_dir, full, nvls=True, mu=0.0, wd=0.0):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    os.environ["SPB_NVLS"] = "1" if nvls else "0"
+    os.environ["SPB_COMM"] = mode
     dist.init_process_group("gloo", rank=rank, world_size=world)
     X, Y, W = spb.gen_chain_mlp(WIDTHS, N, DSEED)
     m = spb.ChainMlp(WIDTHS, X, Y, W, k=K, per_worker_batch=BW, device=rank)
     m.comm_init_torch(dist, rank, world)
-    assert m.nvls == nvls
+    assert m.comm_mode == mode
     m.set_optimizer(LR, mu, wd)
     m.train_steps(SEED, 1, 1, full_backprop=full)
     idx = m.last_batch(len(spb.rank_workers(K, len(WIDTHS) - 1, rank, world)) * BW)
@@ -64,8 +66,9 @@ def _rank(rank, world, port, out_dir, full, nvls=True, mu=0.0, wd=0.0):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("full,nvls", [(False, True), (True, True), (False, False), (True, False)])
-def test_multi_gpu_step_matches_oracle(tmp_path, orc, full, nvls):
+@pytest.mark.parametrize("mode", ["p2p", "nvls", "nccl"])
+@pytest.mark.parametrize("full", [False, True])
+def test_multi_gpu_step_matches_oracle(tmp_path, orc, full, mode):
     world = min(_gpus(), 4)
     if world < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -73,7 +76,7 @@ def test_multi_gpu_step_matches_oracle(tmp_path, orc, full, nvls):
 
     from paper_2111_10672_b200 import spb
 
-    mp.start_processes(_rank, args=(world, _free_port(), str(tmp_path), full, nvls), nprocs=world,
+    mp.start_processes(_rank, args=(world, _free_port(), str(tmp_path), full, mode), nprocs=world,
                        start_method="spawn")
     L = len(WIDTHS) - 1
     X, Y, W = orc.gen_chain_mlp(WIDTHS, N, DSEED)
@@ -92,32 +95,34 @@ def test_multi_gpu_step_matches_oracle(tmp_path, orc, full, nvls):
             assert np.array_equal(got, outs[0][f"arr_{l + 1}"])
 
 
-def _rank_momentum(rank, world, port, out_dir, nvls):
-    _rank(rank, world, port, out_dir, False, nvls, 0.9, 1e-3)
+def _rank_momentum(rank, world, port, out_dir, mode):
+    _rank(rank, world, port, out_dir, False, mode, 0.9, 1e-3)
 
 
-def test_multi_gpu_momentum_nvls_matches_nccl(tmp_path):
-    """Momentum + weight decay: the NVLS path keeps each element's momentum
-    buffer on the rank owning its shard; after 3 steps its weights must match
-    the NCCL path's (every rank updates everything) to fp32 rounding."""
+def test_multi_gpu_momentum_sharded_matches_nccl(tmp_path):
+    """Momentum + weight decay: the p2p and NVLS paths keep each element's
+    momentum buffer on the rank owning its shard; after 3 steps their weights
+    must match the NCCL path's (every rank updates everything) to fp32
+    rounding, and be bit-identical across ranks."""
     world = min(_gpus(), 4)
     if world < 2:
         pytest.skip("needs >= 2 GPUs")
     import torch.multiprocessing as mp
 
     res = {}
-    for nvls in (True, False):
-        d = tmp_path / ("nvls" if nvls else "nccl")
+    for mode in ("p2p", "nvls", "nccl"):
+        d = tmp_path / mode
         d.mkdir()
-        mp.start_processes(_rank_momentum, args=(world, _free_port(), str(d), nvls), nprocs=world,
+        mp.start_processes(_rank_momentum, args=(world, _free_port(), str(d), mode), nprocs=world,
                            start_method="spawn")
-        res[nvls] = [np.load(d / f"r{r}.npz") for r in range(world)]
+        res[mode] = [np.load(d / f"r{r}.npz") for r in range(world)]
     L = len(WIDTHS) - 1
-    for l in range(L):
-        a, b = res[True][0][f"arr_{l + 1}"], res[False][0][f"arr_{l + 1}"]
-        assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-5
-        for r in range(world):
-            assert np.array_equal(res[True][r][f"arr_{l + 1}"], a)
+    for mode in ("p2p", "nvls"):
+        for l in range(L):
+            a, b = res[mode][0][f"arr_{l + 1}"], res["nccl"][0][f"arr_{l + 1}"]
+            assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-5
+            for r in range(world):
+                assert np.array_equal(res[mode][r][f"arr_{l + 1}"], a)
 
 
 def _rank_selftest(rank, world, port, out_dir):
@@ -131,13 +136,13 @@ def _rank_selftest(rank, world, port, out_dir):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    os.environ["SPB_NVLS"] = "1"
+    os.environ["SPB_COMM"] = "nvls"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     X, Y, W = spb.gen_chain_mlp(WIDTHS, N, DSEED)
     m = spb.ChainMlp(WIDTHS, X, Y, W, k=K, per_worker_batch=BW, device=rank)
     m.comm_init_torch(dist, rank, world)
     bad = m.comm_selftest()
-    np.save(os.path.join(out_dir, f"s{rank}.npy"), np.array([bad, int(m.nvls)]))
+    np.save(os.path.join(out_dir, f"s{rank}.npy"), np.array([bad, int(m.comm_mode == "nvls")]))
     dist.barrier()
     m.close()
     dist.destroy_process_group()
