@@ -154,15 +154,15 @@ SPB_API void* spb_stream(spb_ctx* ctx);
  * caller. After this call spb_train_steps runs only this rank's workers
  * (spb_rank_workers) and aggregates each layer over its contributors. The
  * aggregation mode comes from the environment variable SPB_COMM:
- *  - "p2p" (default): each layer's parameters are sharded over the ranks;
+ *  - "p2p" (default for 2 ranks): each layer's parameters are sharded over the ranks;
  *    the rank owning a shard pulls the contributors' gradients of it over
  *    NVLink with the copy engines (CUDA IPC), applies the optimizer and the
  *    other ranks pull the updated fp32 shard back, synchronised by
  *    epoch-stamped device flags (no NCCL in the step);
  *  - "nvls": parameters and gradients in NVSwitch multicast memory; each rank
  *    reduces its shard in the switch, updates it and multicasts the weights;
- *  - "nccl": per-layer NCCL buckets (broadcast / all-reduce), then the local
- *    optimizer update on every rank.
+ *  - "nccl" (default for more than 2 ranks): per-layer NCCL buckets
+ *    (broadcast / all-reduce), then the local optimizer update on every rank.
  * Ranks of one node only. */
 SPB_API spb_status spb_comm_unique_id(void* out128);
 SPB_API spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int nranks);

@@ -100,7 +100,7 @@ struct Ctl {
 // Event slots (Engine::ev): fork/join of the step, per-layer backward and
 // per-layer bucket events.
 enum { kEvStepFork = 0, kEvStepJoin = 1, kEvFork = 2, kEvJoin = 3, kEvUpdFork = 4, kEvUpdJoin = 5, kEvBucket = 8,
-       kEvLayer = 8 + 1024, kEvUpd = 8 + 3072, kEvP2pFork = 8 + 5120, kEvP2pLayer = 8 + 5120 + 16 };
+       kEvLayer = 8 + 1024, kEvUpd = 8 + 3072, kEvP2pFork = 8 + 5120, kEvP2pLayer = 8 + 5120 + 64 };
 
 // Kernel classes of spb_profile_step (index into its output arrays).
 enum { kClsFwd = 0, kClsWgrad, kClsDgrad, kClsHead, kClsColred, kClsUpdate, kClsGather, kClsComm, kNumCls };
@@ -165,7 +165,8 @@ struct Engine {
   long stage_shard = 0;
   PeerPtrs<int> peer_flags{};
   std::vector<float*> peer_grad, peer_w32;
-  cudaStream_t cst2 = nullptr, s4 = nullptr;
+  cudaStream_t s4 = nullptr;
+  std::vector<cudaStream_t> gpull, wpull;  // per-peer copy streams (copy engines run concurrently)
   // NVLS path (multi-GPU, NVSwitch multicast): p_hi / p_lo / grad live in
   // multicast buffers; each layer's gradient is reduced in the switch and
   // the optimizer runs once per element, on the rank owning its shard, which
@@ -215,7 +216,10 @@ struct Engine {
       // Peers may still read this rank's memory until they pass this point.
       if (s3) cudaStreamSynchronize(s3);
       if (s4) cudaStreamSynchronize(s4);
-      if (cst2) cudaStreamSynchronize(cst2);
+      for (auto q : gpull)
+        if (q) cudaStreamSynchronize(q);
+      for (auto q : wpull)
+        if (q) cudaStreamSynchronize(q);
       try {
         host_barrier();
       } catch (...) {
@@ -227,6 +231,11 @@ struct Engine {
         if (peer_flags.p[p]) cudaIpcCloseMemHandle(peer_flags.p[p]);
       }
       peer_grad.clear(), peer_w32.clear();
+      for (auto q : gpull)
+        if (q) cudaStreamDestroy(q);
+      for (auto q : wpull)
+        if (q) cudaStreamDestroy(q);
+      gpull.clear(), wpull.clear();
       comm_mode = 0;
     }
     if (nvls) {
@@ -244,7 +253,6 @@ struct Engine {
       comm = nullptr;
     }
     if (cst) cudaStreamDestroy(cst), cst = nullptr;
-    if (cst2) cudaStreamDestroy(cst2), cst2 = nullptr;
     if (s4) cudaStreamDestroy(s4), s4 = nullptr;
     if (s2) cudaStreamDestroy(s2), s2 = nullptr;
     if (s3) cudaStreamDestroy(s3), s3 = nullptr;
@@ -590,41 +598,46 @@ struct Engine {
     if (!bk) throw ConfigError("comm: no bucket for layer");
     unsigned contrib = 0;
     for (int r : bk->ranks) contrib |= 1u << r;
-    const unsigned all = (nranks >= 32 ? ~0u : (1u << nranks) - 1u), others = all & ~(1u << rank);
     const long off = w_off[l], cnt = b_off[l] + round_up(w[l], 32) - w_off[l], n4 = cnt / 4;
     auto lo_of = [&](int r) { return n4 * r / nranks * 4; };
     const long a = lo_of(rank), b = lo_of(rank + 1), sh = b - a;
-    auto evl = [&](int k) { return ev(kEvP2pLayer + 4 * l + k); };
+    // Layer events: 0 dgrad_l issued (s), 1 shard updated (s3), 8+p gradient
+    // pull from p done, 16+p weight pull from p done.
+    auto evl = [&](int k) { return ev(kEvP2pLayer + 32 * l + k); };
     int n = 0;
     // 1. gradient of l final here -> G[l] to every rank.
     launch_p2p_signal(peer_flags, 2 * l, nranks, rank, epoch_dev, gs);
-    SPB_CUDA(cudaEventRecord(evl(3), s));  // dgrad_l issued on s before this point
+    SPB_CUDA(cudaEventRecord(evl(0), s));  // dgrad_l issued on s before this point
     ++n;
-    // 2. copy engines: pull the contributors' gradients of this shard. Every
-    // rank's G[l] is awaited (not only the contributors'), which also orders
-    // this step's writes after every peer finished the previous step.
+    // 2. copy engines, one stream per peer: wait for the peer's G[l] (every
+    // peer's, contributor or not: that also orders this step's writes after
+    // every peer finished the previous step), then pull its gradient of this
+    // shard if it contributes.
     float* st_buf = stage + static_cast<long>(l % 2) * (nranks - 1) * stage_shard;
-    if (l + 2 <= L) SPB_CUDA(cudaStreamWaitEvent(cst, ev(kEvP2pLayer + 4 * (l + 2) + 1), 0));
-    launch_p2p_wait(flags, 2 * l, nranks, others, epoch_dev, cst);
-    ++n;
     PeerPtrs<const float> src{};
     int nsrc = 0, slot = 0;
-    pbeg(cst);
     for (int r = 0; r < nranks; ++r) {
-      if (!(contrib >> r & 1u)) continue;
       if (r == rank) {
-        src.p[nsrc++] = grad + off + a;
+        if (contrib >> r & 1u) src.p[nsrc++] = grad + off + a;
         continue;
       }
-      float* dst = st_buf + static_cast<long>(slot++) * stage_shard;
-      if (sh > 0) SPB_CUDA(cudaMemcpyAsync(dst, peer_grad[r] + off + a, sh * 4, cudaMemcpyDeviceToDevice, cst));
-      src.p[nsrc++] = dst;
+      cudaStream_t cs = gpull[r];
+      if (l + 2 <= L) SPB_CUDA(cudaStreamWaitEvent(cs, ev(kEvP2pLayer + 32 * (l + 2) + 1), 0));
+      launch_p2p_wait(flags, 2 * l, nranks, 1u << r, epoch_dev, cs);
+      ++n;
+      if (contrib >> r & 1u) {
+        float* dst = st_buf + static_cast<long>(slot++) * stage_shard;
+        pbeg(cs);
+        if (sh > 0) SPB_CUDA(cudaMemcpyAsync(dst, peer_grad[r] + off + a, sh * 4, cudaMemcpyDeviceToDevice, cs));
+        pend(kClsComm, static_cast<double>(sh) * 4.0, cs);
+        src.p[nsrc++] = dst;
+      }
+      SPB_CUDA(cudaEventRecord(evl(8 + r), cs));
     }
-    pend(kClsComm, static_cast<double>(sh) * 4.0 * (nsrc - ((contrib >> rank) & 1u)), cst);
-    SPB_CUDA(cudaEventRecord(evl(0), cst));
     // 3. shard update (SMs) -> U[l].
+    for (int r = 0; r < nranks; ++r)
+      if (r != rank) SPB_CUDA(cudaStreamWaitEvent(s3, evl(8 + r), 0));
     SPB_CUDA(cudaStreamWaitEvent(s3, evl(0), 0));
-    SPB_CUDA(cudaStreamWaitEvent(s3, evl(3), 0));
     if (contrib >> rank & 1u) {
       SPB_CUDA(cudaEventRecord(ev(kEvBucket + l), gs));
       SPB_CUDA(cudaStreamWaitEvent(s3, ev(kEvBucket + l), 0));
@@ -636,21 +649,22 @@ struct Engine {
     launch_p2p_signal(peer_flags, 2 * l + 1, nranks, rank, epoch_dev, s3);
     SPB_CUDA(cudaEventRecord(evl(1), s3));
     n += 2;
-    // 4. copy engines: pull every other rank's updated fp32 shard.
-    launch_p2p_wait(flags, 2 * l + 1, nranks, others, epoch_dev, cst2);
-    ++n;
-    pbeg(cst2);
+    // 4. copy engines, one stream per peer: pull its updated fp32 shard.
     for (int r = 0; r < nranks; ++r) {
       if (r == rank) continue;
+      cudaStream_t cs = wpull[r];
+      launch_p2p_wait(flags, 2 * l + 1, nranks, 1u << r, epoch_dev, cs);
+      ++n;
       const long ra = lo_of(r), rb = lo_of(r + 1);
+      pbeg(cs);
       if (rb > ra)
-        SPB_CUDA(cudaMemcpyAsync(w32 + off + ra, peer_w32[r] + off + ra, (rb - ra) * 4, cudaMemcpyDeviceToDevice, cst2));
+        SPB_CUDA(cudaMemcpyAsync(w32 + off + ra, peer_w32[r] + off + ra, (rb - ra) * 4, cudaMemcpyDeviceToDevice, cs));
+      pend(kClsComm, static_cast<double>(rb - ra) * 4.0, cs);
+      SPB_CUDA(cudaEventRecord(evl(16 + r), cs));
+      SPB_CUDA(cudaStreamWaitEvent(s4, evl(16 + r), 0));
     }
-    pend(kClsComm, static_cast<double>(cnt - sh) * 4.0, cst2);
-    SPB_CUDA(cudaEventRecord(evl(2), cst2));
     // 5. split the pulled shards into (hi, lo) (after dgrad_l).
-    SPB_CUDA(cudaStreamWaitEvent(s4, evl(2), 0));
-    SPB_CUDA(cudaStreamWaitEvent(s4, evl(3), 0));
+    SPB_CUDA(cudaStreamWaitEvent(s4, evl(0), 0));
     pbeg(s4);
     launch_p2p_split(w32 + off, p_hi + off, p_lo + off, cnt, a, b, s4);
     pend(kClsUpdate, static_cast<double>(cnt - sh) * 12.0, s4);
@@ -698,8 +712,14 @@ struct Engine {
       SPB_CUDA(cudaIpcOpenMemHandle(&q, all[3 * p + 2], cudaIpcMemLazyEnablePeerAccess));
       peer_flags.p[p] = static_cast<int*>(q);
     }
-    SPB_CUDA(cudaStreamCreateWithFlags(&cst2, cudaStreamNonBlocking));
     SPB_CUDA(cudaStreamCreateWithFlags(&s4, cudaStreamNonBlocking));
+    gpull.assign(nranks, nullptr);
+    wpull.assign(nranks, nullptr);
+    for (int p = 0; p < nranks; ++p) {
+      if (p == rank) continue;
+      SPB_CUDA(cudaStreamCreateWithFlags(&gpull[p], cudaStreamNonBlocking));
+      SPB_CUDA(cudaStreamCreateWithFlags(&wpull[p], cudaStreamNonBlocking));
+    }
     comm_mode = 2;
     invalidate_graphs();
     host_barrier();
@@ -800,15 +820,17 @@ struct Engine {
       SPB_CUDA(cudaStreamWaitEvent(s, ev(e), 0));
     };
     if (comm && comm_mode == 2) {
-      // Per layer (top down): G signal on the gradient stream, gradient pulls
-      // on cst, shard update on s3, weight pulls on cst2, split on s4; all
-      // joined back into s, then the epoch advances.
-      cudaStream_t side[4] = {cst, cst2, s3, s4};
-      for (int i = 0; i < 4; ++i) fork(side[i], kEvP2pFork + i);
+      // Per layer (top down): G signal on the gradient stream, gradient and
+      // weight pulls on per-peer copy streams, shard update on s3, split on
+      // s4; all joined back into s, then the epoch advances.
+      std::vector<cudaStream_t> side = {s3, s4};
+      for (int p = 0; p < nranks; ++p)
+        if (p != rank) side.push_back(gpull[p]), side.push_back(wpull[p]);
+      for (size_t i = 0; i < side.size(); ++i) fork(side[i], kEvP2pFork + static_cast<int>(i));
       n += enqueue_pass(rows, row0, alpha, s,
                         [&](int l, cudaStream_t from) { return enqueue_p2p_layer(l, full, from, s); }, false,
                         &ctl->step, nullptr);
-      for (int i = 0; i < 4; ++i) join(side[i], kEvP2pFork + 4 + i);
+      for (size_t i = 0; i < side.size(); ++i) join(side[i], kEvP2pFork + 32 + static_cast<int>(i));
       launch_p2p_epoch(epoch_dev, s);
       return n + 1;
     }
@@ -1234,9 +1256,12 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     e.buckets[1] = spb::bucket_plan(e.k, e.L, nranks, true);
     e.set_workers(spb::rank_workers(e.k, e.L, rank, nranks));
     e.ensure_rows(static_cast<int>(e.workers.size()) * e.bw);
-    // Aggregation mode: SPB_COMM = p2p (default) | nccl | nvls.
+    // Aggregation mode: SPB_COMM = p2p | nccl | nvls. Default by measurement
+    // (cfg3): p2p for 2 ranks (pairwise copy-engine exchange at
+    // ~750 GB/s); NCCL from 4 ranks, where the copy engines' all-to-all
+    // pattern (~450 GB/s per GPU) no longer beats NCCL's rings.
     const char* cm = std::getenv("SPB_COMM");
-    const std::string mode = cm ? cm : "p2p";
+    const std::string mode = cm ? cm : (nranks == 2 ? "p2p" : "nccl");
     if (mode != "p2p" && mode != "nccl" && mode != "nvls")
       throw spb::ArgumentError("comm: SPB_COMM must be p2p, nccl or nvls");
     if (nranks > 1 && mode == "p2p") e.setup_p2p();

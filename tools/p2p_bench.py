@@ -46,6 +46,63 @@ def main():
 
     ms = timed(bidir, [st[0], st[1]])
     print(f"bidir 0<->1       {ms:.3f} ms  {size / ms / 1e6:.1f} GB/s per direction")
+    # Pull vs push with explicit streams (cudaMemcpyAsync on the stream of the
+    # device that executes the copy): torch's cross-device copy_ always runs
+    # on the source device (a push).
+    from cuda.bindings import runtime as rt
+
+    def ce_copy(exec_dev, dst_t, src_t, nbytes, reps=5):
+        torch.cuda.set_device(exec_dev)
+        s = torch.cuda.Stream(device=f"cuda:{exec_dev}")
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        kind = rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice
+        rt.cudaMemcpyAsync(dst_t.data_ptr(), src_t.data_ptr(), nbytes, kind, s.cuda_stream)
+        a.record(s)
+        for _ in range(reps):
+            rt.cudaMemcpyAsync(dst_t.data_ptr(), src_t.data_ptr(), nbytes, kind, s.cuda_stream)
+        b.record(s)
+        s.synchronize()
+        return a.elapsed_time(b) / reps
+
+    for nbytes in (16 << 20, 64 << 20, 1 << 30):
+        ms_push = ce_copy(0, dst[1], bufs[0], nbytes)
+        ms_pull = ce_copy(1, dst[1], bufs[0], nbytes)
+        print(f"{nbytes >> 20:5d} MiB 0->1  push (dev0 CE) {nbytes / ms_push / 1e6:7.1f} GB/s   "
+              f"pull (dev1 CE) {nbytes / ms_pull / 1e6:7.1f} GB/s")
+    # The p2p aggregation pattern: every GPU pulls a shard from every peer at
+    # once, one stream per (GPU, peer); timed per stream with CUDA events.
+    kind = rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice
+    for i in range(n):
+        torch.cuda.set_device(i)
+        for p in range(n):
+            if p != i:
+                rt.cudaDeviceEnablePeerAccess(p, 0)  # already-enabled pairs just return an error code
+    for total in (64 << 20, 256 << 20):
+        shard = total // n
+        reps = 10
+        streams = {(i, p): torch.cuda.Stream(device=f"cuda:{i}") for i in range(n) for p in range(n) if p != i}
+        evs = {}
+        for i in range(n):
+            torch.cuda.synchronize(i)
+        for i in range(n):
+            torch.cuda.set_device(i)
+            for p in range(n):
+                if p == i:
+                    continue
+                s = streams[(i, p)]
+                a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_ev.record(s)
+                for _ in range(reps):
+                    rt.cudaMemcpyAsync(dst[i].data_ptr() + p * shard, bufs[p].data_ptr() + i * shard, shard, kind,
+                                       s.cuda_stream)
+                b_ev.record(s)
+                evs[(i, p)] = (a_ev, b_ev)
+        for i in range(n):
+            torch.cuda.synchronize(i)
+        worst = max(a_ev.elapsed_time(b_ev) for a_ev, b_ev in evs.values()) / reps
+        print(f"all-pull x{n}: {shard >> 20} MiB from each of {n - 1} peers: {worst * 1e3:.1f} us/round (slowest "
+              f"stream)  {(n - 1) * shard / worst / 1e6:.1f} GB/s inbound per GPU")
     if n >= 4:
         def ring():
             for i in range(n):
