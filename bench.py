@@ -231,6 +231,38 @@ def traffic_from_profiles():
     return None
 
 
+def spb_savings(widths, k, bw, world):
+    """Backward FLOPs and gradient-exchange bytes of one SPB step vs full
+    backprop (north_star: SPB saves both). Backward per layer l over its
+    contributor rows: wgrad 2*rows*n_l*n_{l-1}, dgrad 2*rows*n_l*n_{l-1} for
+    l >= 2 over the contributor rows of layer l-1 (the rows Delta_{l-1} is
+    needed for). Exchange: per layer, the gradient bytes of
+    every rank hosting a contributor (a rank without contributors sends
+    nothing); at 1 GPU, the bytes of the local aggregate."""
+    from paper_2111_10672_b200 import spb
+
+    L = len(widths) - 1
+    chunks = spb.layer_chunks(k, L)
+    out = {}
+    for full in (False, True):
+        fl = 0.0
+        by = 0.0
+        plan = spb.bucket_plan(k, L, max(world, 1), full) if world > 1 else None
+        for l in range(1, L + 1):
+            m = k if full else chunks[l - 1]
+            rows = m * bw
+            fl += 2.0 * rows * widths[l] * widths[l - 1]
+            if l >= 2:
+                fl += 2.0 * (k if full else chunks[l - 2]) * bw * widths[l] * widths[l - 1]
+            nranks_l = len(plan[l - 1][2]) if plan else 1
+            by += 4.0 * (widths[l] * widths[l - 1] + widths[l]) * nranks_l
+        out["full" if full else "spb"] = (fl, by)
+    return {"backward_flops_spb": out["spb"][0], "backward_flops_full": out["full"][0],
+            "exchange_bytes_spb": out["spb"][1], "exchange_bytes_full": out["full"][1],
+            "saved_backward_flops_frac": round(1 - out["spb"][0] / out["full"][0], 4),
+            "saved_exchange_bytes_frac": round(1 - out["spb"][1] / out["full"][1], 4)}
+
+
 def run_b200(args, world, rank, local, dist):
     from paper_2111_10672_b200 import spb
 
@@ -240,8 +272,10 @@ def run_b200(args, world, rank, local, dist):
     X, Y, W = spb.gen_chain_mlp(widths, cfg["N"], cfg["data_seed"])
     m = spb.ChainMlp(widths, X, Y, W, k=k, per_worker_batch=bw, device=local)
     del W
+    comm_mode = None
     if world > 1:
         m.comm_init_torch(dist, rank, world)
+        comm_mode = m.comm_mode
     workers = spb.rank_workers(k, L, rank, world) if world > 1 else list(range(1, k + 1))
     rows = len(workers) * bw
     m.set_optimizer(cfg["lr"], cfg["momentum"], cfg["weight_decay"])
@@ -314,7 +348,9 @@ def run_b200(args, world, rank, local, dist):
         "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05)", "data": "synthetic (reference generator make_random_chain_mlp, seed 7)",
         "config": {"workload": cfg["workload"], "widths": "4096x16+1", "k": k, "per_worker_batch": bw,
                    "global_batch": k * bw, "dataset": cfg["N"], "optimizer": "momentum 0.9, wd 1e-4, lr 0.01",
-                   "parallelism": f"spb-dp{world} (workers/rank {len(workers)})", "l2": "inputs exceed L2 (2 GB weights)"},
+                   "parallelism": f"spb-dp{world} (workers/rank {len(workers)})", "l2": "inputs exceed L2 (2 GB weights)",
+                   "aggregation": comm_mode or "local (1 GPU)"},
+        "spb_savings": spb_savings(widths, k, bw, world),
         "full_backprop": {"value": round(full_value, 2), "unit": UNIT, "ms_per_step": round(ms_full / K, 4),
                           "spb_speedup": round(value / full_value, 4)},
         "gpu_launches": launches * K,

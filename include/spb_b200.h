@@ -182,6 +182,17 @@ SPB_API spb_status spb_comm_bench(spb_ctx* ctx, long long n_floats, int reps);
 SPB_API spb_status spb_bucket_plan(int k, int L, int nranks, int full_backprop, int* kind, int* root,
                                    int* rank_mask);
 
+/* ---- Task profiles for the Jigsaw simulator (profile.hpp:20-40) -----------------
+ * One worker task on this GPU: forward + head over `rows` samples, then the
+ * truncated backward of the top `suffix` layers (partial_backprop,
+ * spb.cpp:51-68), each captured as a graph and replayed `reps` times.
+ * forward_ms: forward + head; backward_ms: the additional time of the
+ * backward; peak_mem_gb: the task's device working set (parameters as hi/lo,
+ * covered gradient blocks, activations, Delta buffers), in 1e9 bytes. These
+ * fill one ProfileEntry knot at fraction suffix / L (profile.cpp:118-171). */
+SPB_API spb_status spb_profile_task(spb_ctx* ctx, int rows, int suffix, int reps, float* forward_ms, float* backward_ms,
+                                    double* peak_mem_gb);
+
 /* ---- Introspection for tests and the bench ----------------------------------- */
 /* Batch indices the last device-drawn step used (rows in hosted-worker order). */
 SPB_API spb_status spb_last_batch(spb_ctx* ctx, int* out, int rows);

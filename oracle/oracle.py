@@ -226,6 +226,7 @@ class Ref(_Common):
         L.ref_time_steps.restype = C.c_double
         L.ref_time_steps.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_int,
                                      C.c_int, C.c_int]
+        L.ref_profile_query.argtypes = [C.c_char_p, C.c_char_p, C.c_double, C.POINTER(C.c_double)]
 
     def _check(self, st: int, what: str = ""):
         if st != ST_OK:
@@ -233,6 +234,13 @@ class Ref(_Common):
 
     def mix(self, a: int, b: int) -> int:
         return int(self.lib.ref_rng_mix(a, b))
+
+    def profile_query(self, csv_text: str, model: str, fraction: float) -> dict:
+        """ProfileTable::from_csv + the interpolators (profile.cpp:67-171)."""
+        out = np.zeros(7, dtype=np.float64)
+        self._check(self.lib.ref_profile_query(csv_text.encode(), model.encode(), fraction, _dp(out)), "profile")
+        keys = ("forward_ms", "backward_ms", "peak_mem_gb", "grad_size_mb", "batch", "duration_ms", "comm_mb")
+        return dict(zip(keys, (float(v) for v in out)))
 
 
 class RefModel:

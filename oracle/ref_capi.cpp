@@ -7,6 +7,10 @@
 //   spb_sgd_run       spb.hpp:82-83  (spb.cpp:164-210)
 //   suffix/chunk bookkeeping spb.hpp:39-49 (spb.cpp:16-49)
 //   make_random_chain_mlp    model.hpp:240-241 (model.cpp:208-231)
+//   ProfileTable::from_csv + forward_time / backward_time / peak_memory /
+//   task_demand  profile.hpp:43-80 (profile.cpp:67-171): parses and queries
+//                the task profiles the B200 emitter writes
+//                (paper_2111_10672_b200/jigsaw_profiles.py)
 // Only tests/, __graft_entry__.smoke() and bench.py's CPU legs load it. It is
 // built only where /root/reference exists (this container); the .so itself
 // travels to the GPU box with the snapshot.
@@ -19,6 +23,7 @@
 #include <thread>
 #include <vector>
 
+#include "jigsaw/cost/profile.hpp"
 #include "jigsaw/errors.hpp"
 #include "jigsaw/rng.hpp"
 #include "jigsaw/spb/model.hpp"
@@ -283,6 +288,25 @@ double ref_time_steps(void* p, int k, int B, double lr, uint64_t seed, int s0, i
   for (int s = s0; s < s0 + steps; ++s)
     if (ref_step(p, k, B, lr, seed, s, full, threads) != kOk) return -1.0;
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// Parses `csv` with the reference's ProfileTable::from_csv (which validates
+// every entry) and queries model `model` at `fraction`:
+// out = {forward_time, backward_time, peak_memory, grad_size_mb, batch,
+//        task_demand(fraction).duration_ms, task_demand.comm_mb}.
+int ref_profile_query(const char* csv, const char* model, double fraction, double* out) {
+  return guard([&] {
+    auto table = jigsaw::cost::ProfileTable::from_csv(csv, "<b200>");
+    const auto& e = table.get(model);
+    out[0] = jigsaw::cost::forward_time(e, fraction);
+    out[1] = jigsaw::cost::backward_time(e, fraction);
+    out[2] = jigsaw::cost::peak_memory(e, fraction);
+    out[3] = e.grad_size_mb;
+    out[4] = e.batch_size;
+    auto d = jigsaw::cost::task_demand(e, fraction);
+    out[5] = d.duration_ms;
+    out[6] = d.comm_mb;
+  });
 }
 
 }  // extern "C"

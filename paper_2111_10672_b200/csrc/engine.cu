@@ -1379,6 +1379,71 @@ spb_status spb_time_train_steps(spb_ctx* ctx, uint64_t seed, int step0, int step
   });
 }
 
+spb_status spb_profile_task(spb_ctx* ctx, int rows, int suffix, int reps, float* forward_ms, float* backward_ms,
+                            double* peak_mem_gb) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    const int L = e.L;
+    if (!e.X) throw spb::ConfigError("profile_task: no dataset");
+    if (rows < 1) throw spb::ArgumentError("profile_task: rows must be >= 1");
+    if (suffix < 0 || suffix > L) throw spb::ArgumentError("profile_task: suffix out of range");
+    if (reps < 1) throw spb::ArgumentError("profile_task: reps must be >= 1");
+    e.ensure_rows(rows);
+    std::vector<int> iota(rows);
+    for (int i = 0; i < rows; ++i) iota[i] = i % e.N;
+    SPB_CUDA(cudaMemcpyAsync(e.idx_in, iota.data(), rows * sizeof(int), cudaMemcpyHostToDevice, e.st));
+    spb::launch_gather(e.X, e.ld[0], e.Y, e.w[0], e.nout, e.N, rows, rows, e.workers_dev, nullptr, 0, nullptr, 0, e.idx_in,
+                       e.idx, e.Hh[0], e.Hl[0], e.ld[0], e.ybatch, e.st);
+    // One worker task (partial_backprop, spb.cpp:51-68, on one batch): the
+    // forward + head, then dgrad / wgrad of the top `suffix` layers. Each
+    // variant is captured into a graph and replayed `reps` times.
+    auto time_pass = [&](int suf) {
+      std::vector<int> row0(L + 1, rows);
+      std::vector<float> alpha(L + 1, 1.0f / static_cast<float>(rows));
+      for (int l = L - suf + 1; l <= L; ++l) row0[l] = 0;
+      cudaGraph_t gr;
+      cudaGraphExec_t ge;
+      SPB_CUDA(cudaStreamBeginCapture(e.st, cudaStreamCaptureModeThreadLocal));
+      try {
+        e.enqueue_pass(rows, row0, alpha, e.st);
+      } catch (...) {
+        cudaStreamEndCapture(e.st, &gr);
+        throw;
+      }
+      SPB_CUDA(cudaStreamEndCapture(e.st, &gr));
+      SPB_CUDA(cudaGraphInstantiate(&ge, gr, 0));
+      cudaGraphDestroy(gr);
+      cudaEvent_t a, b;
+      SPB_CUDA(cudaEventCreate(&a));
+      SPB_CUDA(cudaEventCreate(&b));
+      SPB_CUDA(cudaGraphLaunch(ge, e.st));  // warm-up
+      SPB_CUDA(cudaEventRecord(a, e.st));
+      for (int i = 0; i < reps; ++i) SPB_CUDA(cudaGraphLaunch(ge, e.st));
+      SPB_CUDA(cudaEventRecord(b, e.st));
+      SPB_CUDA(cudaEventSynchronize(b));
+      float ms = 0.f;
+      SPB_CUDA(cudaEventElapsedTime(&ms, a, b));
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      cudaGraphExecDestroy(ge);
+      return ms / static_cast<float>(reps);
+    };
+    const float f = time_pass(0);
+    const float fb = suffix > 0 ? time_pass(suffix) : f;
+    *forward_ms = f;
+    *backward_ms = std::max(0.f, fb - f);
+    // Device working set of the task: parameters (hi + lo), the gradient
+    // blocks of the covered layers, the activations (split pairs) and, when
+    // backpropagating, the three Delta buffers.
+    double bytes = 8.0 * static_cast<double>(e.nflat);
+    for (int l = L - suffix + 1; l <= L; ++l) bytes += 4.0 * static_cast<double>(e.w[l]) * (e.w[l - 1] + 1);
+    for (int l = 0; l < L; ++l) bytes += 8.0 * rows * static_cast<double>(e.ld[l]);
+    bytes += 4.0 * rows * (e.w[0] + 2.0 * e.nout + 2.0);
+    if (suffix > 0) bytes += 3.0 * 8.0 * rows * static_cast<double>(e.ldd);
+    *peak_mem_gb = bytes / 1e9;
+  });
+}
+
 spb_status spb_last_batch(spb_ctx* ctx, int* out, int rows) {
   return guard(ctx, [&] {
     auto& e = ctx->e;

@@ -107,6 +107,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "spb_comm_mode": (i, [vp, ip]),
         "spb_comm_selftest": (i, [vp, C.POINTER(C.c_longlong)]),
         "spb_comm_bench": (i, [vp, C.c_longlong, i]),
+        "spb_profile_task": (i, [vp, i, i, i, fp, fp, C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -122,7 +123,7 @@ EXPORTED = [
     "spb_step_host", "spb_loss", "spb_synchronize", "spb_stream", "spb_comm_unique_id", "spb_comm_init",
     "spb_last_batch", "spb_launches_per_step", "spb_make_random_chain_mlp",
     "spb_get_grads", "spb_profile_step", "spb_time_train_steps", "spb_bucket_plan", "spb_set_fused_update",
-    "spb_comm_mode", "spb_comm_selftest", "spb_comm_bench",
+    "spb_comm_mode", "spb_comm_selftest", "spb_comm_bench", "spb_profile_task",
 ]
 
 PROFILE_CLASSES = ["gemm_fwd", "gemm_wgrad", "gemm_dgrad", "head", "colreduce", "update", "gather", "comm"]
@@ -409,6 +410,15 @@ class ChainMlp:
         v = C.c_longlong()
         _check(load_library().spb_comm_selftest(self._ctx, C.byref(v)), self._ctx)
         return int(v.value)
+
+    def profile_task(self, rows: int, suffix: int, reps: int = 10):
+        """(forward_ms, backward_ms, peak_mem_gb) of one worker task that
+        backpropagates the top `suffix` layers of a `rows`-sample batch."""
+        f = np.zeros(1, dtype=np.float32)
+        b = np.zeros(1, dtype=np.float32)
+        mem = C.c_double()
+        _check(load_library().spb_profile_task(self._ctx, rows, suffix, reps, _fp(f), _fp(b), C.byref(mem)), self._ctx)
+        return float(f[0]), float(b[0]), float(mem.value)
 
     def comm_bench(self, n_floats: int, reps: int = 20):
         """Collective NVLS tuning aid (rank 0 prints the timings)."""
