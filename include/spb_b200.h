@@ -182,6 +182,13 @@ SPB_API spb_status spb_comm_bench(spb_ctx* ctx, long long n_floats, int reps);
 SPB_API spb_status spb_bucket_plan(int k, int L, int nranks, int full_backprop, int* kind, int* root,
                                    int* rank_mask);
 
+/* ---- Gradient-noise estimator (spb.hpp:84-101) -----------------------------------
+ * empirical_variance (spb.cpp:212-265) at the context's current parameters,
+ * on the GPU, with the reference's sampling protocol sample for sample:
+ * out = {spb, spb_se, baseline, baseline_se, p_hat[0..k), p_se[0..k)}.
+ * cfg.k / cfg.B must match the context (k, k * per_worker_batch); one GPU. */
+SPB_API spb_status spb_empirical_variance(spb_ctx* ctx, int k, int B, int trials, uint64_t seed, double* out);
+
 /* ---- Task profiles for the Jigsaw simulator (profile.hpp:20-40) -----------------
  * One worker task on this GPU: forward + head over `rows` samples, then the
  * truncated backward of the top `suffix` layers (partial_backprop,

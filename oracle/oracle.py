@@ -227,6 +227,8 @@ class Ref(_Common):
         L.ref_time_steps.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_int,
                                      C.c_int, C.c_int]
         L.ref_profile_query.argtypes = [C.c_char_p, C.c_char_p, C.c_double, C.POINTER(C.c_double)]
+        for n in ("ref_empirical_variance", "ref_variance_oracle"):
+            getattr(L, n).argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_double)]
 
     def _check(self, st: int, what: str = ""):
         if st != ST_OK:
@@ -298,6 +300,20 @@ class RefModel:
         avg = np.zeros(iters, dtype=np.float64)
         self.ref._check(self.ref.lib.ref_sgd_run(self.h, k, B, lr, iters, seed, _dp(avg)), "sgd_run")
         return avg
+
+    def empirical_variance(self, k: int, B: int, trials: int, seed: int) -> dict:
+        """empirical_variance (spb.cpp:212-265) at the current iterate."""
+        out = np.zeros(4 + 2 * k, dtype=np.float64)
+        self.ref._check(self.ref.lib.ref_empirical_variance(self.h, k, B, trials, seed, _dp(out)), "empirical_variance")
+        return dict(spb=out[0], spb_se=out[1], baseline=out[2], baseline_se=out[3], p_hat=out[4:4 + k],
+                    p_se=out[4 + k:])
+
+    def variance_oracle(self, k: int, B: int, trials: int, seed: int) -> dict:
+        """The reference's independent brute-force oracle (oracle.cpp:240-326)."""
+        out = np.zeros(4 + 2 * k, dtype=np.float64)
+        self.ref._check(self.ref.lib.ref_variance_oracle(self.h, k, B, trials, seed, _dp(out)), "variance_oracle")
+        return dict(spb=out[0], spb_se=out[1], harmonic_sum=out[2], harmonic_sum_se=out[3], p_hat=out[4:4 + k],
+                    p_se=out[4 + k:])
 
     def time_steps(self, k, B, lr, seed, s0, steps, full=False, threads=1) -> float:
         return float(self.ref.lib.ref_time_steps(self.h, k, B, lr, seed, s0, steps, int(full), threads))

@@ -7,6 +7,8 @@
 //   spb_sgd_run       spb.hpp:82-83  (spb.cpp:164-210)
 //   suffix/chunk bookkeeping spb.hpp:39-49 (spb.cpp:16-49)
 //   make_random_chain_mlp    model.hpp:240-241 (model.cpp:208-231)
+//   empirical_variance spb.hpp:100-101 (spb.cpp:212-265) and the reference's
+//   independent variance_oracle (oracle.hpp:57-62, oracle.cpp:240-326)
 //   ProfileTable::from_csv + forward_time / backward_time / peak_memory /
 //   task_demand  profile.hpp:43-80 (profile.cpp:67-171): parses and queries
 //                the task profiles the B200 emitter writes
@@ -25,6 +27,7 @@
 
 #include "jigsaw/cost/profile.hpp"
 #include "jigsaw/errors.hpp"
+#include "jigsaw/oracle/oracle.hpp"
 #include "jigsaw/rng.hpp"
 #include "jigsaw/spb/model.hpp"
 #include "jigsaw/spb/spb.hpp"
@@ -288,6 +291,34 @@ double ref_time_steps(void* p, int k, int B, double lr, uint64_t seed, int s0, i
   for (int s = s0; s < s0 + steps; ++s)
     if (ref_step(p, k, B, lr, seed, s, full, threads) != kOk) return -1.0;
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// empirical_variance at the handle's iterate: out = {spb, spb_se, baseline,
+// baseline_se, p_hat[0..k), p_se[0..k)}.
+int ref_empirical_variance(void* p, int k, int B, int trials, uint64_t seed, double* out) {
+  auto* h = static_cast<Handle*>(p);
+  return guard([&] {
+    SpbConfig cfg;
+    cfg.k = k;
+    cfg.B = B;
+    auto e = empirical_variance(*h->model, cfg, h->x, trials, seed);
+    out[0] = e.spb, out[1] = e.spb_se, out[2] = e.baseline, out[3] = e.baseline_se;
+    for (int m = 0; m < k; ++m) out[4 + m] = e.p_hat[m], out[4 + k + m] = e.p_se[m];
+  });
+}
+
+// variance_oracle at the handle's iterate: out = {spb, spb_se, harmonic_sum,
+// harmonic_sum_se, p_hat[0..k), p_se[0..k)}.
+int ref_variance_oracle(void* p, int k, int B, int trials, uint64_t seed, double* out) {
+  auto* h = static_cast<Handle*>(p);
+  return guard([&] {
+    SpbConfig cfg;
+    cfg.k = k;
+    cfg.B = B;
+    auto e = jigsaw::oracle::variance_oracle(*h->model, cfg, h->x, trials, seed);
+    out[0] = e.spb, out[1] = e.spb_se, out[2] = e.harmonic_sum, out[3] = e.harmonic_sum_se;
+    for (int m = 0; m < k; ++m) out[4 + m] = e.p_hat[m], out[4 + k + m] = e.p_se[m];
+  });
 }
 
 // Parses `csv` with the reference's ProfileTable::from_csv (which validates

@@ -19,11 +19,13 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
 #include <mutex>
+#include <numeric>
 #include <string>
 #include <vector>
 
@@ -1441,6 +1443,101 @@ spb_status spb_profile_task(spb_ctx* ctx, int rows, int suffix, int reps, float*
     bytes += 4.0 * rows * (e.w[0] + 2.0 * e.nout + 2.0);
     if (suffix > 0) bytes += 3.0 * 8.0 * rows * static_cast<double>(e.ldd);
     *peak_mem_gb = bytes / 1e9;
+  });
+}
+
+spb_status spb_empirical_variance(spb_ctx* ctx, int k, int B, int trials, uint64_t seed, double* out) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    if (!e.X) throw spb::ConfigError("empirical_variance: no dataset");
+    if (k < 1) throw spb::ArgumentError("SpbConfig: k must be >= 1");  // spb.cpp:11-14
+    if (B < 1 || B % k != 0) throw spb::ArgumentError("SpbConfig: B must be positive and divisible by k");
+    if (trials < 1) throw spb::ArgumentError("empirical_variance: trials must be >= 1");
+    if (k != e.k || B / k != e.bw)
+      throw spb::ArgumentError("empirical_variance: cfg.k and cfg.B / cfg.k must match the context");
+    if (e.comm) throw spb::ConfigError("empirical_variance: single-GPU contexts only");
+    const int L = e.L, N = e.N, rows = k * e.bw;
+    e.ensure_rows(std::max(N, rows));
+    float* G = Engine::alloc<float>(e.nflat);
+    const long nd = static_cast<long>(2 + k) * trials;
+    double* dist = Engine::alloc<double>(nd);
+    int* samp = Engine::alloc<int>(static_cast<long>(k) * trials);
+    cudaStream_t st = e.st;
+    try {
+      // grad f(x): the mean gradient over the whole dataset (full_gradient,
+      // spb.cpp:267-271), one pass over all N rows.
+      std::vector<int> iota(N);
+      std::iota(iota.begin(), iota.end(), 0);
+      SPB_CUDA(cudaMemcpyAsync(e.idx_in, iota.data(), N * sizeof(int), cudaMemcpyHostToDevice, st));
+      spb::launch_gather(e.X, e.ld[0], e.Y, e.w[0], e.nout, N, N, N, e.workers_dev, nullptr, 0, nullptr, 0, e.idx_in, e.idx,
+                         e.Hh[0], e.Hl[0], e.ld[0], e.ybatch, st);
+      {
+        std::vector<int> row0(L + 1, 0);
+        std::vector<float> alpha(L + 1, 1.0f / static_cast<float>(N));
+        e.enqueue_pass(N, row0, alpha, st);
+      }
+      SPB_CUDA(cudaMemcpyAsync(G, e.grad, e.nflat * sizeof(float), cudaMemcpyDeviceToDevice, st));
+      // Trials (spb.cpp:219-229): trial r's worker j draws its batch from
+      // Rng(seed).split(kWorkerDrawTag).split(r).split(j) -- the device
+      // gather's Rng(seed').split(step).split(j) with seed' = the first split
+      // and step = r. The SPB estimate and the full-backprop baseline use the
+      // same batches.
+      const uint64_t wseed = spb::Rng::mix(seed, 0x5D17);  // kWorkerDrawTag, spb.hpp:86
+      e.set_workers_all();
+      std::vector<int> r0s, r0f;
+      std::vector<float> as, af;
+      e.step_plan(false, r0s, as);
+      e.step_plan(true, r0f, af);
+      for (int r = 1; r <= trials; ++r) {
+        spb::launch_gather(e.X, e.ld[0], e.Y, e.w[0], e.nout, N, rows, e.bw, e.workers_dev, nullptr, wseed, nullptr, r,
+                           nullptr, e.idx, e.Hh[0], e.Hl[0], e.ld[0], e.ybatch, st);
+        e.enqueue_pass(rows, r0s, as, st);
+        spb::launch_sqdist(G, e.grad, e.nflat, dist + (r - 1), st);
+        e.enqueue_pass(rows, r0f, af, st);
+        spb::launch_sqdist(G, e.grad, e.nflat, dist + trials + (r - 1), st);
+      }
+      // Per-chunk p_i (spb.cpp:240-262): single-sample gradients drawn from
+      // Rng(seed).split(kChunkDrawTag).split(m), restricted to chunk m.
+      auto spans = spb::chunk_layout(k, L);
+      std::vector<int> hs(static_cast<size_t>(k) * trials);
+      for (int m = 1; m <= k; ++m) {
+        spb::Rng cs = spb::Rng(seed).split(0xC410).split(static_cast<uint64_t>(m));  // kChunkDrawTag, spb.hpp:87
+        for (int t = 0; t < trials; ++t) hs[static_cast<size_t>(m - 1) * trials + t] = static_cast<int>(cs.next_below(N));
+      }
+      SPB_CUDA(cudaMemcpyAsync(samp, hs.data(), hs.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+      for (int m = 1; m <= k; ++m) {
+        const int first = spans[m - 1].first, last = spans[m - 1].second;
+        if (first > last) continue;  // empty chunk: d = 0 every trial
+        std::vector<int> row0(L + 1, 1);
+        for (int l = first; l <= L; ++l) row0[l] = 0;
+        std::vector<float> alpha(L + 1, 1.0f);
+        const long a = e.w_off[first], b = e.b_off[last] + spb::round_up(e.w[last], 32);
+        for (int t = 0; t < trials; ++t) {
+          spb::launch_gather(e.X, e.ld[0], e.Y, e.w[0], e.nout, N, 1, 1, e.workers_dev, nullptr, 0, nullptr, 0,
+                             samp + static_cast<long>(m - 1) * trials + t, e.idx, e.Hh[0], e.Hl[0], e.ld[0], e.ybatch, st);
+          e.enqueue_pass(1, row0, alpha, st);
+          spb::launch_sqdist(G + a, e.grad + a, b - a, dist + static_cast<long>(2 + m - 1) * trials + t, st);
+        }
+      }
+      std::vector<double> h(nd);
+      SPB_CUDA(cudaMemcpyAsync(h.data(), dist, nd * sizeof(double), cudaMemcpyDeviceToHost, st));
+      SPB_CUDA(cudaStreamSynchronize(st));
+      auto finish = [&](const double* d, double& mean, double& se) {  // spb.cpp:230-234
+        double sum = 0.0, sumsq = 0.0;
+        for (int t = 0; t < trials; ++t) sum += d[t], sumsq += d[t] * d[t];
+        mean = sum / trials;
+        const double var = std::max(0.0, sumsq / trials - mean * mean);
+        se = std::sqrt(var / trials);
+      };
+      finish(h.data(), out[0], out[1]);
+      finish(h.data() + trials, out[2], out[3]);
+      for (int m = 0; m < k; ++m) finish(h.data() + static_cast<long>(2 + m) * trials, out[4 + m], out[4 + k + m]);
+    } catch (...) {
+      cudaStreamSynchronize(st);
+      cudaFree(G), cudaFree(dist), cudaFree(samp);
+      throw;
+    }
+    cudaFree(G), cudaFree(dist), cudaFree(samp);
   });
 }
 

@@ -4,7 +4,9 @@
 // contributor average used by the aggregator entry point.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <stdexcept>
 
 #include "launch.hpp"
 #include "ptx.cuh"
@@ -363,6 +365,38 @@ void launch_sgd_update(float* p_hi, float* p_lo, const float* grad, float* mom, 
   sgd_update_kernel<<<ctas > 0 ? ctas : grid_for(n4, 256), 256, 0, s>>>(
       reinterpret_cast<float4*>(p_hi), reinterpret_cast<float4*>(p_lo), reinterpret_cast<const float4*>(grad),
       reinterpret_cast<float4*>(mom), n4, lr, momentum, wd);
+  SPB_CUDA(cudaGetLastError());
+}
+
+// out[slot] += sum_i (a_i - b_i)^2 over [0, n), fp64 accumulation
+// (block_distance_sq, spb.cpp:110-118).
+__global__ void __launch_bounds__(256) sqdist_kernel(const float* __restrict__ a, const float* __restrict__ b, long n4,
+                                                     double* __restrict__ out) {
+  double acc = 0.0;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 x = reinterpret_cast<const float4*>(a)[i];
+    const float4 y = reinterpret_cast<const float4*>(b)[i];
+    const double d0 = static_cast<double>(x.x) - y.x, d1 = static_cast<double>(x.y) - y.y;
+    const double d2 = static_cast<double>(x.z) - y.z, d3 = static_cast<double>(x.w) - y.w;
+    acc += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += part[w];
+    atomicAdd(out, t);
+  }
+}
+
+void launch_sqdist(const float* a, const float* b, long n, double* out, cudaStream_t s) {
+  if (n <= 0) return;
+  if (n % 4) throw std::invalid_argument("sqdist: n must be a multiple of 4");
+  sqdist_kernel<<<static_cast<int>(std::min<long>((n / 4 + 255) / 256, 148L * 4)), 256, 0, s>>>(a, b, n / 4, out);
   SPB_CUDA(cudaGetLastError());
 }
 

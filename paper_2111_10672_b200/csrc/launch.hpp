@@ -82,6 +82,8 @@ void launch_sgd_update(float* p_hi, float* p_lo, const float* grad, float* mom, 
                        float wd, cudaStream_t s, int ctas = 0);
 // out[c] = (sum_{w} src[w][c]) / m for w ascending (aggregate, spb.cpp:97-103).
 void launch_aggregate(const float* const* srcs_dev, int m, long n, float* out, cudaStream_t s);
+// *out += sum over [0, n) of (a - b)^2 in fp64 (n a multiple of 4).
+void launch_sqdist(const float* a, const float* b, long n, double* out, cudaStream_t s);
 void launch_split(const float* in, long n, float* hi, float* lo, cudaStream_t s);
 void launch_join(const float* hi, const float* lo, long n, float* out, cudaStream_t s);
 // Also advances *step_dev (nullable): the next step's Rng stream.

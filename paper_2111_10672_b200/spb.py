@@ -108,6 +108,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "spb_comm_selftest": (i, [vp, C.POINTER(C.c_longlong)]),
         "spb_comm_bench": (i, [vp, C.c_longlong, i]),
         "spb_profile_task": (i, [vp, i, i, i, fp, fp, C.POINTER(C.c_double)]),
+        "spb_empirical_variance": (i, [vp, i, i, i, u64, C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -124,6 +125,7 @@ EXPORTED = [
     "spb_last_batch", "spb_launches_per_step", "spb_make_random_chain_mlp",
     "spb_get_grads", "spb_profile_step", "spb_time_train_steps", "spb_bucket_plan", "spb_set_fused_update",
     "spb_comm_mode", "spb_comm_selftest", "spb_comm_bench", "spb_profile_task",
+    "spb_empirical_variance",
 ]
 
 PROFILE_CLASSES = ["gemm_fwd", "gemm_wgrad", "gemm_dgrad", "head", "colreduce", "update", "gather", "comm"]
@@ -245,6 +247,16 @@ class BackpropStats:
 class StepSchedule(Enum):
     Theorem1 = 0
     Constant = 1
+
+
+@dataclass
+class VarianceEstimate:  # spb.hpp:91-98
+    spb: float = 0.0  # E || grad f - g_spb ||^2
+    spb_se: float = 0.0
+    baseline: float = 0.0  # same, with every worker computing the full gradient
+    baseline_se: float = 0.0
+    p_hat: List[float] = field(default_factory=list)  # per-chunk single-sample variances p_i
+    p_se: List[float] = field(default_factory=list)
 
 
 @dataclass
@@ -524,6 +536,23 @@ def aggregate(grads: Sequence[PartialGradient], k: int) -> List[np.ndarray]:
     ctx = _aggregator_ctx()
     _check(load_library().spb_aggregate(ctx, k, L, pin, _ip(dims), _ip(cov), pout), ctx)
     return [o[:s] for o, s in zip(out, sizes)]
+
+
+def empirical_variance(model: ChainMlp, cfg: SpbConfig, x, trials: int, seed: int) -> VarianceEstimate:
+    """empirical_variance (spb.cpp:212-265) on the GPU, with the reference's
+    sampling protocol (kWorkerDrawTag / kChunkDrawTag streams) sample for
+    sample. The model's workspace must match (cfg.k, cfg.B)."""
+    cfg.validate()
+    if trials < 1:
+        raise ArgumentError("empirical_variance: trials must be >= 1")
+    if x is not None:
+        model.set_params(x)
+    out = np.zeros(4 + 2 * cfg.k, dtype=np.float64)
+    _check(load_library().spb_empirical_variance(model.ctx, cfg.k, cfg.B, trials, seed,
+                                                 out.ctypes.data_as(C.POINTER(C.c_double))), model.ctx)
+    k = cfg.k
+    return VarianceEstimate(float(out[0]), float(out[1]), float(out[2]), float(out[3]),
+                            [float(v) for v in out[4:4 + k]], [float(v) for v in out[4 + k:4 + 2 * k]])
 
 
 def spb_sgd_run(model: ChainMlp, cfg: SpbConfig, iterations: int, schedule: StepSchedule, seed: int,
