@@ -1,4 +1,4 @@
-"""The N>1 protocol on CPU with torch.distributed gloo (world sizes 2 and 4).
+"""The N>1 protocol on CPU with torch.distributed gloo (world sizes 2, 4 and 8).
 
 Every rank hosts the workers spb_rank_workers(k, L, rank, N) assigns it,
 computes its local per-layer contribution with the CPU oracle (the mean of
@@ -68,7 +68,7 @@ def _worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_bucket_protocol_matches_single_process_aggregate(tmp_path, world, orc):
     mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, start_method="spawn")
     L = len(WIDTHS) - 1
