@@ -86,6 +86,19 @@ SPB_API spb_status spb_make_random_chain_mlp(const int* widths, int n_widths, in
  * variant). k workers of per_worker_batch samples each may run per step. */
 SPB_API spb_status spb_create(const int* widths, int n_widths, int k, int per_worker_batch, int device,
                       spb_ctx** out);
+/* ConvNet (BASELINE configs[3]: CIFAR10-shaped, ResNet18
+ * widths): layers 1..nconv are 3x3 convolutions (padding 1) with tanh,
+ * lowered to the same tcgen05 GEMMs via im2col; layer nconv+1 is the affine
+ * head (nout <= 16) on the globally average-pooled features; per-sample loss
+ * 0.5 ||out - y||^2, the ChainMlp's. geom = {in_h, in_w, in_c, then
+ * (c_out, stride in {1, 2}) per convolution}. Parameter block l is W_l
+ * [c_out x 9 c_in] row-major with columns (ky * 3 + kx) * c_in + ci, then b_l;
+ * samples are NHWC images (in_h * in_w * in_c floats). Every other entry
+ * point (dataset, params, train_steps, partial_backprop, multi-GPU, profile)
+ * takes the context as for a ChainMlp; rows count samples. No reference
+ * counterpart: the reference has no convolutional model (parity unpinned). */
+SPB_API spb_status spb_create_conv(const int* geom, int nconv, int nout, int k, int per_worker_batch, int device,
+                                   spb_ctx** out);
 SPB_API spb_status spb_destroy(spb_ctx* ctx);
 /* ChainMlp's dataset (model.cpp:86-101), uploaded to HBM. */
 SPB_API spb_status spb_set_dataset(spb_ctx* ctx, const float* X, const float* Y, int N);

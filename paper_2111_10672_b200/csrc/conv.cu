@@ -1,0 +1,247 @@
+// Data-movement kernels of the convolutional SPB model (ConvNet, engine.cu):
+// the GEMM work (forward, wgrad, dgrad) runs on the same tcgen05 3xTF32
+// kernels as the MLP; these kernels lower the 3x3 convolutions onto them.
+//
+// Layout: activations NHWC, one GEMM row per pixel ([samples * h * w, ld(c)],
+// split pairs hi + lo). im2col rows: [samples * h_out * w_out, ld(9 c_in)],
+// column (ky * 3 + kx) * c_in + ci. Padding 1, stride 1 or 2.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <stdexcept>
+
+#include "conv.hpp"
+#include "launch.hpp"
+
+namespace spb {
+namespace {
+
+__device__ __forceinline__ float tf32r(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t a, uint64_t b) {  // rng.hpp:47-53
+  uint64_t z = a ^ (b + 0x9E3779B97F4A7C15ULL + (a << 6) + (a >> 2));
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// One block per sample slot: draw (or take) the sample index, copy its
+// h*w*c NHWC image into pixel rows of H0 (split pair, row stride ldh) and its
+// target into ybatch.
+__global__ void conv_gather_kernel(const float* __restrict__ X, long ldx, const float* __restrict__ Y, int pix, int c0,
+                                   int nout, int N, int bw, const int* __restrict__ workers,
+                                   const uint64_t* __restrict__ seed_dev, uint64_t seed_host,
+                                   const int* __restrict__ step_dev, int step_host, const int* __restrict__ idx_in,
+                                   int* __restrict__ idx_out, float* __restrict__ h_hi, float* __restrict__ h_lo,
+                                   long ldh, float* __restrict__ ybatch) {
+  const int r = blockIdx.x;
+  int idx;
+  if (idx_in) {
+    idx = idx_in[r];
+  } else {  // Rng(seed).split(step).split(worker), draw r % bw (same as gather_kernel)
+    const int step = step_dev ? *step_dev : step_host;
+    const uint64_t seed = seed_dev ? *seed_dev : seed_host;
+    const uint64_t key = mix64(mix64(seed, static_cast<uint64_t>(step)), static_cast<uint64_t>(workers[r / bw]));
+    const uint64_t u = mix64(key, static_cast<uint64_t>(r % bw) + 1);
+    idx = static_cast<int>(__umul64hi(u, static_cast<uint64_t>(N)));
+  }
+  if (threadIdx.x == 0 && idx_out) idx_out[r] = idx;
+  const float* src = X + static_cast<long>(idx) * ldx;
+  const long base = static_cast<long>(r) * pix;
+  for (int e = threadIdx.x; e < pix * c0; e += blockDim.x) {
+    const int p = e / c0, c = e - p * c0;
+    const float v = src[e];
+    const float h = tf32r(v);
+    h_hi[(base + p) * ldh + c] = h;
+    h_lo[(base + p) * ldh + c] = v - h;
+  }
+  if (threadIdx.x < nout) ybatch[r * nout + threadIdx.x] = Y[static_cast<long>(idx) * nout + threadIdx.x];
+}
+
+// Flat over (output row, tap, channel vector): consecutive threads move
+// consecutive VEC-channel vectors, coalesced on both sides. VEC = 4 when
+// c_in % 4 == 0 (every layer but the RGB input).
+template <int VEC>
+__global__ void __launch_bounds__(256) im2col_kernel(const float* __restrict__ in_hi, const float* __restrict__ in_lo,
+                                                     long ldin, ConvGeom g, long row0, long rows,
+                                                     float* __restrict__ col_hi, float* __restrict__ col_lo, long ldk) {
+  const int cv = g.c_in / VEC;
+  const long total = rows * 9 * cv;
+  const int opix = g.out_h * g.out_w;
+  for (long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(t % cv);
+    const long rt = t / cv;
+    const int tap = static_cast<int>(rt % 9);
+    const long orow = row0 + rt / 9;
+    const long s = orow / opix;
+    const int rem = static_cast<int>(orow - s * opix);
+    const int oy = rem / g.out_w, ox = rem - oy * g.out_w;
+    const int ky = tap / 3, kx = tap - ky * 3;
+    const int iy = oy * g.stride + ky - 1, ix = ox * g.stride + kx - 1;
+    const bool inside = iy >= 0 && iy < g.in_h && ix >= 0 && ix < g.in_w;
+    const long src = ((s * g.in_h + iy) * g.in_w + ix) * ldin + c * VEC;
+    const long dst = orow * ldk + tap * g.c_in + c * VEC;
+    if constexpr (VEC == 4) {
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(col_hi + dst) = inside ? *reinterpret_cast<const float4*>(in_hi + src) : z;
+      *reinterpret_cast<float4*>(col_lo + dst) = inside ? *reinterpret_cast<const float4*>(in_lo + src) : z;
+    } else {
+      col_hi[dst] = inside ? in_hi[src] : 0.f;
+      col_lo[dst] = inside ? in_lo[src] : 0.f;
+    }
+  }
+}
+
+// Delta_{l-1}[(s, y, x), ci] = (1 - H^2) * sum over taps of dcol[(s, oy, ox),
+// tap * c_in + ci] for the output pixels (oy, ox) whose window covers (y, x);
+// fixed tap order (deterministic). Flat over (input row, channel vector).
+template <int VEC>
+__global__ void __launch_bounds__(256) col2im_tanh_kernel(const float* __restrict__ dcol, long ldk, ConvGeom g,
+                                                          long row0, long rows, const float* __restrict__ h_hi,
+                                                          const float* __restrict__ h_lo, long ldh,
+                                                          float* __restrict__ d_hi, float* __restrict__ d_lo,
+                                                          long ldd) {
+  const int cv = g.c_in / VEC;
+  const long total = rows * cv;
+  const int ipix = g.in_h * g.in_w;
+  for (long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(t % cv);
+    const long irow = row0 + t / cv;
+    const long s = irow / ipix;
+    const int rem = static_cast<int>(irow - s * ipix);
+    const int y = rem / g.in_w, x = rem - y * g.in_w;
+    float acc[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
+    for (int ky = 0; ky < 3; ++ky) {
+      const int ty = y + 1 - ky;
+      if (ty < 0 || ty % g.stride) continue;
+      const int oy = ty / g.stride;
+      if (oy >= g.out_h) continue;
+      for (int kx = 0; kx < 3; ++kx) {
+        const int tx = x + 1 - kx;
+        if (tx < 0 || tx % g.stride) continue;
+        const int ox = tx / g.stride;
+        if (ox >= g.out_w) continue;
+        const float* src = dcol + ((s * g.out_h + oy) * g.out_w + ox) * ldk + (ky * 3 + kx) * g.c_in + c * VEC;
+        if constexpr (VEC == 4) {
+          const float4 q = *reinterpret_cast<const float4*>(src);
+          acc[0] += q.x, acc[1] += q.y, acc[2] += q.z, acc[3] += q.w;
+        } else {
+          acc[0] += src[0];
+        }
+      }
+    }
+    const long at = irow * ldh + c * VEC, ad = irow * ldd + c * VEC;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      const float h = h_hi[at + v] + h_lo[at + v];
+      const float r = acc[v] * (1.0f - h * h);
+      const float rh = tf32r(r);
+      d_hi[ad + v] = rh;
+      d_lo[ad + v] = r - rh;
+    }
+  }
+}
+
+int flat_grid(long total) { return static_cast<int>(std::max<long>(1, std::min<long>((total + 255) / 256, 148L * 16))); }
+
+// pooled[s, c] = mean over the pix pixel rows of sample s (split pair out).
+__global__ void avgpool_kernel(const float* __restrict__ h_hi, const float* __restrict__ h_lo, long ldh, int pix,
+                               int c, float* __restrict__ p_hi, float* __restrict__ p_lo, long ldp) {
+  const int s = blockIdx.x;
+  const float inv = 1.0f / static_cast<float>(pix);
+  for (int ch = threadIdx.x; ch < c; ch += blockDim.x) {
+    float acc = 0.f;
+    for (int p = 0; p < pix; ++p) {
+      const long r = static_cast<long>(s) * pix + p;
+      acc += h_hi[r * ldh + ch] + h_lo[r * ldh + ch];
+    }
+    const float v = acc * inv;
+    const float vh = tf32r(v);
+    p_hi[static_cast<long>(s) * ldp + ch] = vh;
+    p_lo[static_cast<long>(s) * ldp + ch] = v - vh;
+  }
+}
+
+// Delta[(s, p), c] = g[s, c] / pix * (1 - H[(s, p), c]^2) for samples >= s0.
+__global__ void unpool_tanh_kernel(const float* __restrict__ g_hi, const float* __restrict__ g_lo, long ldg, int pix,
+                                   int c, int s0, const float* __restrict__ h_hi, const float* __restrict__ h_lo,
+                                   long ldh, float* __restrict__ d_hi, float* __restrict__ d_lo, long ldd) {
+  const long r = static_cast<long>(s0) * pix + blockIdx.x;
+  const long s = r / pix;
+  const float inv = 1.0f / static_cast<float>(pix);
+  for (int ch = threadIdx.x; ch < c; ch += blockDim.x) {
+    const float gv = (g_hi[s * ldg + ch] + g_lo[s * ldg + ch]) * inv;
+    const float h = h_hi[r * ldh + ch] + h_lo[r * ldh + ch];
+    const float v = gv * (1.0f - h * h);
+    const float vh = tf32r(v);
+    d_hi[r * ldd + ch] = vh;
+    d_lo[r * ldd + ch] = v - vh;
+  }
+}
+
+int threads_for(int c) { return c >= 256 ? 256 : (c >= 128 ? 128 : (c >= 64 ? 64 : 32)); }
+
+}  // namespace
+
+void launch_conv_gather(const float* X, long ldx, const float* Y, int pix, int c0, int nout, int N, int samples, int bw,
+                        const int* workers, const uint64_t* seed_dev, uint64_t seed_host, const int* step_dev,
+                        int step_host, const int* idx_in, int* idx_out, float* h_hi, float* h_lo, long ldh,
+                        float* ybatch, cudaStream_t s) {
+  if (samples <= 0) return;
+  conv_gather_kernel<<<samples, 256, 0, s>>>(X, ldx, Y, pix, c0, nout, N, bw, workers, seed_dev, seed_host, step_dev,
+                                             step_host, idx_in, idx_out, h_hi, h_lo, ldh, ybatch);
+  SPB_CUDA(cudaGetLastError());
+}
+
+void launch_im2col(const float* in_hi, const float* in_lo, long ldin, const ConvGeom& g, int row0, int rows,
+                   float* col_hi, float* col_lo, long ldk, cudaStream_t s) {
+  if (rows <= 0) return;
+  if (g.c_in % 4 == 0 && ldin % 4 == 0 && ldk % 4 == 0)
+    im2col_kernel<4><<<flat_grid(static_cast<long>(rows) * 9 * (g.c_in / 4)), 256, 0, s>>>(in_hi, in_lo, ldin, g, row0,
+                                                                                          rows, col_hi, col_lo, ldk);
+  else
+    im2col_kernel<1><<<flat_grid(static_cast<long>(rows) * 9 * g.c_in), 256, 0, s>>>(in_hi, in_lo, ldin, g, row0, rows,
+                                                                                   col_hi, col_lo, ldk);
+  SPB_CUDA(cudaGetLastError());
+}
+
+void launch_col2im_tanh(const float* dcol, long ldk, const ConvGeom& g, int row0, int rows, const float* h_hi,
+                        const float* h_lo, long ldh, float* d_hi, float* d_lo, long ldd, cudaStream_t s) {
+  if (rows <= 0) return;
+  if (g.c_in % 4 == 0 && ldk % 4 == 0)
+    col2im_tanh_kernel<4><<<flat_grid(static_cast<long>(rows) * (g.c_in / 4)), 256, 0, s>>>(
+        dcol, ldk, g, row0, rows, h_hi, h_lo, ldh, d_hi, d_lo, ldd);
+  else
+    col2im_tanh_kernel<1><<<flat_grid(static_cast<long>(rows) * g.c_in), 256, 0, s>>>(dcol, ldk, g, row0, rows, h_hi,
+                                                                                    h_lo, ldh, d_hi, d_lo, ldd);
+  SPB_CUDA(cudaGetLastError());
+}
+
+void launch_avgpool(const float* h_hi, const float* h_lo, long ldh, int samples, int pix, int c, float* p_hi,
+                    float* p_lo, long ldp, cudaStream_t s) {
+  if (samples <= 0) return;
+  avgpool_kernel<<<samples, threads_for(c), 0, s>>>(h_hi, h_lo, ldh, pix, c, p_hi, p_lo, ldp);
+  SPB_CUDA(cudaGetLastError());
+}
+
+void launch_unpool_tanh(const float* g_hi, const float* g_lo, long ldg, int samples, int s0, int pix, int c,
+                        const float* h_hi, const float* h_lo, long ldh, float* d_hi, float* d_lo, long ldd,
+                        cudaStream_t s) {
+  const long rows = static_cast<long>(samples - s0) * pix;
+  if (rows <= 0) return;
+  unpool_tanh_kernel<<<static_cast<unsigned>(rows), threads_for(c), 0, s>>>(g_hi, g_lo, ldg, pix, c, s0, h_hi, h_lo,
+                                                                             ldh, d_hi, d_lo, ldd);
+  SPB_CUDA(cudaGetLastError());
+}
+
+}  // namespace spb

@@ -31,6 +31,7 @@
 
 #include "../../include/spb_b200.h"
 #include "gemm_tf32x3.cuh"
+#include "conv.hpp"
 #include "launch.hpp"
 #include "nvls.hpp"
 #include "p2p.hpp"
@@ -117,6 +118,21 @@ struct Engine {
   int k = 1, bw = 1;
   std::vector<long> ld;            // ld[l] = round_up(n_l, 4)
   std::vector<long> w_off, b_off;  // index 1..L
+  // Weight geometry of layer l (1..L): W_l is [w[l] x fan[l]] stored with row
+  // stride ldf[l]. ChainMlp: fan[l] = w[l-1], ldf[l] = ld[l-1].
+  std::vector<int> fan;
+  std::vector<long> ldf;
+  // ConvNet (conv_model): layers 1..L-1 are 3x3 convolutions (cg[l]) over
+  // NHWC pixel rows, pix[l] pixels per sample (pix[0] = the input image);
+  // layer L is the affine head on the globally average-pooled features.
+  bool conv_model = false;
+  std::vector<ConvGeom> cg;
+  std::vector<long> pix;
+  std::vector<float*> Ch, Cl;  // im2col split pairs, [samples * pix[l] x ldf[l]], kept for wgrad
+  float *Ph = nullptr, *Pl = nullptr, *Gh = nullptr, *Gl = nullptr;  // pooled features / their gradient
+  float* dcol = nullptr;  // dgrad columns (fp32), reused per layer
+  int* iota_dev = nullptr;
+  long ldx = 0;  // dataset row stride
   long nflat = 0, ldd = 0;
   float *p_hi = nullptr, *p_lo = nullptr, *grad = nullptr, *mom = nullptr;
   float lr = 0.01f, mu = 0.f, wd = 0.f;
@@ -269,6 +285,9 @@ struct Engine {
         f(stage);
     for (auto p : Hh) f(p);
     for (auto p : Hl) f(p);
+    for (auto p : Ch) f(p);
+    for (auto p : Cl) f(p);
+    f(Ph), f(Pl), f(Gh), f(Gl), f(dcol), f(iota_dev);
     for (int i = 0; i < kDbuf; ++i) f(Dh[i]), f(Dl[i]);
     if (st) cudaStreamDestroy(st);
     st = nullptr;
@@ -302,15 +321,71 @@ struct Engine {
     long ldmax = 0;
     for (int l = 0; l <= L; ++l) ld[l] = round_up(w[l], 4), ldmax = std::max(ldmax, ld[l]);
     ldd = ldmax;
+    ldx = ld[0];
+    pix.assign(L + 1, 1);
+    fan.assign(L + 1, 0);
+    ldf.assign(L + 1, 0);
+    for (int l = 1; l <= L; ++l) fan[l] = w[l - 1], ldf[l] = ld[l - 1];
+    allocate_params();
+    ensure_rows(k * bw);
+  }
+
+  // ConvNet: geom = {in_h, in_w, in_c, then (c_out, stride) per conv layer}.
+  void init_conv(const int* geom, int nconv, int nout_, int k_, int bw_, int device) {
+    if (nconv < 1) throw ArgumentError("convnet: need at least one convolution");
+    if (geom[0] < 1 || geom[1] < 1 || geom[2] < 1) throw ArgumentError("convnet: bad input geometry");
+    if (nout_ < 1 || nout_ > 16) throw ArgumentError("convnet: output width must be in [1, 16]");
+    if (k_ < 1 || bw_ < 1) throw ArgumentError("SpbConfig: k and per-worker batch must be >= 1");
+    conv_model = true;
+    L = nconv + 1;
+    nout = nout_;
+    k = k_;
+    bw = bw_;
+    dev = device;
+    SPB_CUDA(cudaSetDevice(dev));
+    SPB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    SPB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    SPB_CUDA(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
+    w.assign(L + 1, 0);
+    pix.assign(L + 1, 1);
+    cg.assign(L, ConvGeom{});
+    int h = geom[0], wd_ = geom[1];
+    w[0] = geom[2];
+    pix[0] = static_cast<long>(h) * wd_;
+    for (int l = 1; l <= nconv; ++l) {
+      const int c = geom[3 + 2 * (l - 1)], stride = geom[4 + 2 * (l - 1)];
+      if (c < 1 || (stride != 1 && stride != 2)) throw ArgumentError("convnet: channels >= 1, stride 1 or 2");
+      ConvGeom g{h, wd_, w[l - 1], (h - 1) / stride + 1, (wd_ - 1) / stride + 1, c, stride};
+      cg[l] = g;
+      w[l] = c;
+      h = g.out_h, wd_ = g.out_w;
+      pix[l] = static_cast<long>(h) * wd_;
+    }
+    w[L] = nout;
+    ld.resize(L + 1);
+    for (int l = 0; l <= L; ++l) ld[l] = round_up(w[l], 4);
+    ldd = 0;
+    fan.assign(L + 1, 0);
+    ldf.assign(L + 1, 0);
+    for (int l = 1; l <= L; ++l) {
+      fan[l] = l < L ? 9 * w[l - 1] : w[L - 1];
+      ldf[l] = round_up(fan[l], 4);
+    }
+    ldx = pix[0] * w[0];
+    allocate_params();
+    ensure_rows(k * bw);
+  }
+
+  void allocate_params() {
     w_off.assign(L + 1, 0);
     b_off.assign(L + 1, 0);
     long cur = 0, maxblk = 0;
     for (int l = 1; l <= L; ++l) {
       w_off[l] = cur;
-      cur += round_up(w[l] * ld[l - 1], 32);
+      cur += round_up(w[l] * ldf[l], 32);
       b_off[l] = cur;
       cur += round_up(w[l], 32);
-      maxblk = std::max(maxblk, w[l] * ld[l - 1] + w[l]);
+      maxblk = std::max(maxblk, w[l] * ldf[l] + w[l]);
     }
     nflat = cur;
     p_hi = alloc<float>(nflat);
@@ -323,7 +398,6 @@ struct Engine {
     loss_dev = alloc<float>(1);
     workers_dev = alloc<int>(k);
     set_workers_all();
-    ensure_rows(k * bw);
   }
 
   void set_workers(const std::vector<int>& ws) {
@@ -347,6 +421,7 @@ struct Engine {
     if (rows <= cap_rows) return;
     SPB_CUDA(cudaStreamSynchronize(st));
     invalidate_graphs();
+    if (conv_model) return ensure_samples_conv(rows);
     for (auto p : Hh) cudaFree(p);
     for (auto p : Hl) cudaFree(p);
     Hh.assign(L, nullptr);
@@ -379,6 +454,183 @@ struct Engine {
     idx_in = alloc<int>(rows);
   }
 
+  // ConvNet workspace for `samples` samples (rows = pixel rows per layer).
+  void ensure_samples_conv(int samples) {
+    auto f = [](void* p) {
+      if (p) cudaFree(p);
+    };
+    for (auto p : Hh) f(p);
+    for (auto p : Hl) f(p);
+    for (auto p : Ch) f(p);
+    for (auto p : Cl) f(p);
+    for (int i = 0; i < kDbuf; ++i) f(Dh[i]), f(Dl[i]);
+    for (void* p : {(void*)delta, (void*)row_loss, (void*)ybatch, (void*)scratch, (void*)scratch2, (void*)xin, (void*)idx,
+                    (void*)idx_in, (void*)Ph, (void*)Pl, (void*)Gh, (void*)Gl, (void*)dcol, (void*)iota_dev})
+      f(p);
+    cap_rows = samples;
+    const long S = samples;
+    Hh.assign(L, nullptr);
+    Hl.assign(L, nullptr);
+    Ch.assign(L, nullptr);
+    Cl.assign(L, nullptr);
+    long dmax = 1, cmax = 1, sc = colreduce_scratch(samples, static_cast<int>(ld[L - 1]), nout);
+    for (int l = 0; l < L; ++l) {
+      Hh[l] = alloc<float>(S * pix[l] * ld[l]);
+      Hl[l] = alloc<float>(S * pix[l] * ld[l]);
+      if (l >= 1) {
+        Ch[l] = alloc<float>(S * pix[l] * ldf[l]);
+        Cl[l] = alloc<float>(S * pix[l] * ldf[l]);
+        dmax = std::max(dmax, S * pix[l] * ld[l]);
+        cmax = std::max(cmax, S * pix[l] * ldf[l]);
+        sc = std::max(sc, colreduce_scratch(static_cast<int>(S * pix[l]), w[l], 1));
+      }
+    }
+    for (int i = 0; i < kDbuf; ++i) Dh[i] = alloc<float>(dmax), Dl[i] = alloc<float>(dmax);
+    dcol = alloc<float>(cmax);
+    Ph = alloc<float>(S * ld[L - 1]);
+    Pl = alloc<float>(S * ld[L - 1]);
+    Gh = alloc<float>(S * ld[L - 1]);
+    Gl = alloc<float>(S * ld[L - 1]);
+    delta = alloc<float>(S * nout);
+    row_loss = alloc<float>(S);
+    ybatch = alloc<float>(S * nout);
+    scratch_n = sc;
+    scratch = alloc<float>(sc);
+    scratch2 = alloc<float>(sc);
+    xin = alloc<float>(S * ldx);
+    idx = alloc<int>(S);
+    idx_in = alloc<int>(S);
+    iota_dev = alloc<int>(S);
+    std::vector<int> io(samples);
+    std::iota(io.begin(), io.end(), 0);
+    SPB_CUDA(cudaMemcpy(iota_dev, io.data(), S * sizeof(int), cudaMemcpyHostToDevice));
+  }
+
+  // Gathers `rows` samples (ChainMlp: rows; ConvNet: pixel rows of the
+  // samples) into H_0 and ybatch: from idx_in, or drawn on the device.
+  void enqueue_gather(const float* Xsrc, long ldxs, int rows, int bw_, const uint64_t* seed_dev, uint64_t seed_host,
+                      const int* step_dev, int step_host, const int* idx_in_, cudaStream_t s) {
+    if (conv_model)
+      launch_conv_gather(Xsrc, ldxs, Y, static_cast<int>(pix[0]), w[0], nout, N, rows, bw_, workers_dev, seed_dev,
+                         seed_host, step_dev, step_host, idx_in_, idx, Hh[0], Hl[0], ld[0], ybatch, s);
+    else
+      launch_gather(Xsrc, ldxs, Y, w[0], nout, N, rows, bw_, workers_dev, seed_dev, seed_host, step_dev, step_host,
+                    idx_in_, idx, Hh[0], Hl[0], ld[0], ybatch, s);
+  }
+
+  // ConvNet pass (same contract as enqueue_pass; rows, row0 and alpha count
+  // samples). Forward: im2col -> GEMM (bias + tanh) per convolution, global
+  // average pool, head. Backward over the contributor samples' pixel rows:
+  // wgrad = GEMM(Delta^T, im2col) scaled by alpha_l, bias column sums,
+  // dgrad = GEMM(Delta, W) into columns -> col2im * (1 - H^2). One stream.
+  int enqueue_pass_conv(int samples, const std::vector<int>& row0, const std::vector<float>& alpha, cudaStream_t s,
+                        const std::function<int(int, cudaStream_t)>& on_grad, int* step_dev,
+                        const std::function<void(int, cudaStream_t)>& on_layer) {
+    int n = 0;
+    const int Lc = L - 1;
+    for (int l = 1; l <= Lc; ++l) {
+      const int M = static_cast<int>(samples * pix[l]);
+      pbeg(s);
+      launch_im2col(Hh[l - 1], Hl[l - 1], ld[l - 1], cg[l], 0, M, Ch[l], Cl[l], ldf[l], s);
+      pend(kClsGather, 0, s);
+      Operand A{Ch[l], Cl[l], ldf[l], M, fan[l], false};
+      Operand B{p_hi + w_off[l], p_lo + w_off[l], ldf[l], w[l], fan[l], false};
+      GemmEpilogue ep{};
+      ep.out_hi = Hh[l];
+      ep.out_lo = Hl[l];
+      ep.ld_out = ld[l];
+      ep.bias_hi = p_hi + b_off[l];
+      ep.bias_lo = p_lo + b_off[l];
+      ep.M = M;
+      ep.N = w[l];
+      ep.splitk_ws = splitk_ws;
+      ep.splitk_ws_floats = kSplitkWsFloats;
+      pbeg(s);
+      n += 1 + gemm_tf32x3(A, B, kEpiFwdTanh, ep, s);
+      pend(kClsFwd, 2.0 * M * w[l] * fan[l], s);
+    }
+    const bool has_next = Lc >= 1 && row0[Lc] < samples;
+    pbeg(s);
+    launch_avgpool(Hh[Lc], Hl[Lc], ld[Lc], samples, static_cast<int>(pix[Lc]), w[Lc], Ph, Pl, ld[Lc], s);
+    launch_head(Ph, Pl, ld[Lc], samples, w[Lc], nout, p_hi + w_off[L], p_lo + w_off[L], ldf[L], p_hi + b_off[L],
+                p_lo + b_off[L], ybatch, delta, row_loss, has_next ? Gh : nullptr, has_next ? Gl : nullptr, ld[Lc],
+                has_next ? row0[Lc] : samples, false, s, /*dn_act=*/false);
+    launch_sum_loss(row_loss, samples, 1.0f / static_cast<float>(samples), loss_dev, step_dev, s);
+    pend(kClsHead, 0, s);
+    n += 3;
+    if (row0[L] < samples) {
+      pbeg(s);
+      launch_colreduce(Ph, Pl, ld[Lc], row0[L], samples, w[Lc], delta, nout, nout, alpha[L], grad + w_off[L], ldf[L],
+                       scratch, s);
+      launch_colreduce(delta, nullptr, nout, row0[L], samples, nout, nullptr, 1, 0, alpha[L], grad + b_off[L], 0,
+                       scratch, s);
+      pend(kClsColred, 0, s);
+      n += 4;
+    }
+    if (on_grad) n += on_grad(L, s);
+    if (on_layer) on_layer(L, s);
+    if (has_next) {
+      launch_unpool_tanh(Gh, Gl, ld[Lc], samples, row0[Lc], static_cast<int>(pix[Lc]), w[Lc], Hh[Lc], Hl[Lc], ld[Lc],
+                         Dh[Lc % kDbuf], Dl[Lc % kDbuf], ld[Lc], s);
+      ++n;
+    }
+    int l = Lc;
+    for (; l >= 1; --l) {
+      if (row0[l] >= samples) break;
+      const int b = l % kDbuf, bn = (l - 1) % kDbuf;
+      const long r0 = row0[l] * pix[l], cnt = (samples - row0[l]) * pix[l];
+      if (l > 1 && row0[l - 1] < samples) {  // dgrad into columns, then col2im * (1 - H^2)
+        const long q0 = row0[l - 1] * pix[l], qn = (samples - row0[l - 1]) * pix[l];
+        Operand A{Dh[b] + q0 * ld[l], Dl[b] + q0 * ld[l], ld[l], static_cast<int>(qn), w[l], false};
+        Operand B{p_hi + w_off[l], p_lo + w_off[l], ldf[l], fan[l], w[l], true};
+        GemmEpilogue ep{};
+        ep.out_hi = dcol + q0 * ldf[l];
+        ep.ld_out = ldf[l];
+        ep.alpha = 1.f;
+        ep.M = static_cast<int>(qn);
+        ep.N = fan[l];
+        ep.splitk_ws = splitk_ws;
+        ep.splitk_ws_floats = kSplitkWsFloats;
+        pbeg(s);
+        n += gemm_tf32x3(A, B, kEpiStoreScaled, ep, s);
+        pend(kClsDgrad, 2.0 * qn * w[l] * fan[l], s);
+        pbeg(s);
+        launch_col2im_tanh(dcol, ldf[l], cg[l], static_cast<int>(row0[l - 1] * pix[l - 1]),
+                           static_cast<int>((samples - row0[l - 1]) * pix[l - 1]), Hh[l - 1], Hl[l - 1], ld[l - 1],
+                           Dh[bn], Dl[bn], ld[l - 1], s);
+        pend(kClsColred, 0, s);
+        ++n;
+      }
+      {  // wgrad: dW_l = alpha_l * Delta_l[r0:]^T col_l[r0:]
+        Operand A{Dh[b] + r0 * ld[l], Dl[b] + r0 * ld[l], ld[l], w[l], static_cast<int>(cnt), true};
+        Operand B{Ch[l] + r0 * ldf[l], Cl[l] + r0 * ldf[l], ldf[l], fan[l], static_cast<int>(cnt), true};
+        GemmEpilogue ep{};
+        ep.out_hi = grad + w_off[l];
+        ep.ld_out = ldf[l];
+        ep.alpha = alpha[l];
+        ep.M = w[l];
+        ep.N = fan[l];
+        ep.splitk_ws = splitk_ws;  // few output tiles, K = pixel rows: split K (single stream)
+        ep.splitk_ws_floats = kSplitkWsFloats;
+        pbeg(s);
+        n += gemm_tf32x3(A, B, kEpiStoreScaled, ep, s);
+        pend(kClsWgrad, 2.0 * cnt * w[l] * fan[l], s);
+      }
+      pbeg(s);
+      launch_colreduce(Dh[b], Dl[b], ld[l], static_cast<int>(r0), static_cast<int>(samples * pix[l]), w[l], nullptr, 1,
+                       0, alpha[l], grad + b_off[l], 0, scratch, s);
+      pend(kClsColred, 0, s);
+      n += 2;
+      if (on_grad) n += on_grad(l, s);
+      if (on_layer) on_layer(l, s);
+    }
+    for (; l >= 1 && on_grad; --l) {
+      n += on_grad(l, s);
+      if (on_layer) on_layer(l, s);
+    }
+    return n;
+  }
+
   // ---- the per-step launch program ----------------------------------------
   // row0[l] (l = 1..L): first row contributing to layer l (rows when none).
   // alpha[l]: the averaging factor 1/(m_l * per_worker_batch) of layer l.
@@ -392,6 +644,7 @@ struct Engine {
   int enqueue_pass(int rows, const std::vector<int>& row0, const std::vector<float>& alpha, cudaStream_t s,
                    const std::function<int(int, cudaStream_t)>& on_grad = nullptr, bool fused = false,
                    int* step_dev = nullptr, const std::function<void(int, cudaStream_t)>& on_layer = nullptr) {
+    if (conv_model) return enqueue_pass_conv(rows, row0, alpha, s, on_grad, step_dev, on_layer);
     int n = 0;
     // Forward, hidden layers (mlp_forward model.cpp:108-128 batched).
     for (int l = 1; l < L; ++l) {
@@ -796,11 +1049,15 @@ struct Engine {
     const int rows = static_cast<int>(workers.size()) * bw;
     int n = 0;
     pbeg(s);
-    if (host_rows) {
+    if (host_rows && conv_model) {
+      // Host images already in xin (spb_step_host): identity index, and no
+      // target copy (nout = 0: ybatch was uploaded directly).
+      launch_conv_gather(xin, ldx, nullptr, static_cast<int>(pix[0]), w[0], 0, rows, rows, rows, workers_dev, nullptr, 0,
+                         nullptr, 0, iota_dev, nullptr, Hh[0], Hl[0], ld[0], nullptr, s);
+    } else if (host_rows) {
       launch_split_rows(xin, w[0], rows, w[0], Hh[0], Hl[0], ld[0], s);
     } else {
-      launch_gather(X, ld[0], Y, w[0], nout, N, rows, bw, workers_dev, &ctl->seed, 0, &ctl->step, 0, nullptr, idx, Hh[0], Hl[0],
-                    ld[0], ybatch, s);
+      enqueue_gather(X, ldx, rows, bw, &ctl->seed, 0, &ctl->step, 0, nullptr, s);
     }
     pend(kClsGather, 0, s);
     ++n;
@@ -811,7 +1068,8 @@ struct Engine {
     // the layer's gradient is final (wgrad on s2, or its NCCL bucket on cst)
     // and its last reader dgrad_l (on s) is done, so the HBM-bound update
     // runs beside the remaining backward GEMMs instead of after them.
-    const bool per_layer = comm || !fused_update;
+    const bool fused_ok = fused_update && !conv_model;  // the conv pass has no fused epilogue
+    const bool per_layer = comm || !fused_ok;
     cudaStream_t us = concurrent ? s3 : s;
     auto fork = [&](cudaStream_t to, int e) {
       SPB_CUDA(cudaEventRecord(ev(e), s));
@@ -870,7 +1128,7 @@ struct Engine {
                         false, &ctl->step, on_layer);
       join(cst, kEvStepJoin);
     } else {
-      n += enqueue_pass(rows, row0, alpha, s, nullptr, fused_update, &ctl->step,
+      n += enqueue_pass(rows, row0, alpha, s, nullptr, fused_ok, &ctl->step,
                         per_layer ? std::function<void(int, cudaStream_t)>(on_layer) : nullptr);
     }
     if (per_layer && concurrent) join(s3, kEvUpdJoin);
@@ -990,6 +1248,15 @@ spb_status spb_create(const int* widths, int n_widths, int k, int per_worker_bat
   return s;
 }
 
+spb_status spb_create_conv(const int* geom, int nconv, int nout, int k, int per_worker_batch, int device,
+                           spb_ctx** out) {
+  *out = nullptr;
+  auto ctx = std::make_unique<spb_ctx>();
+  spb_status s = guard(nullptr, [&] { ctx->e.init_conv(geom, nconv, nout, k, per_worker_batch, device); });
+  if (s == SPB_OK) *out = ctx.release();
+  return s;
+}
+
 spb_status spb_destroy(spb_ctx* ctx) {
   if (ctx) {
     cudaSetDevice(ctx->e.dev);
@@ -1005,9 +1272,10 @@ spb_status spb_set_dataset(spb_ctx* ctx, const float* X, const float* Y, int N) 
     if (N < 1) throw spb::ArgumentError("mlp: dataset shape mismatch");
     SPB_CUDA(cudaStreamSynchronize(e.st));
     if (e.X) cudaFree(e.X), cudaFree(e.Y);
-    e.X = Engine::alloc<float>(static_cast<long>(N) * e.ld[0]);
+    const long row = e.conv_model ? e.ldx : e.w[0];  // values per sample (ConvNet: an NHWC image)
+    e.X = Engine::alloc<float>(static_cast<long>(N) * e.ldx);
     e.Y = Engine::alloc<float>(static_cast<long>(N) * e.nout);
-    SPB_CUDA(cudaMemcpy2D(e.X, e.ld[0] * 4, X, e.w[0] * 4, e.w[0] * 4, N, cudaMemcpyHostToDevice));
+    SPB_CUDA(cudaMemcpy2D(e.X, e.ldx * 4, X, row * 4, row * 4, N, cudaMemcpyHostToDevice));
     SPB_CUDA(cudaMemcpy(e.Y, Y, static_cast<size_t>(N) * e.nout * 4, cudaMemcpyHostToDevice));
     e.N = N;
     e.invalidate_graphs();
@@ -1018,11 +1286,11 @@ spb_status spb_set_params(spb_ctx* ctx, const float* const* blocks) {
   return guard(ctx, [&] {
     auto& e = ctx->e;
     for (int l = 1; l <= e.L; ++l) {
-      const int no = e.w[l], ni = e.w[l - 1];
+      const int no = e.w[l], ni = e.fan[l];
       SPB_CUDA(cudaMemsetAsync(e.tmp, 0, e.tmp_n * 4, e.st));
-      SPB_CUDA(cudaMemcpy2DAsync(e.tmp, e.ld[l - 1] * 4, blocks[l - 1], ni * 4, ni * 4, no, cudaMemcpyHostToDevice,
+      SPB_CUDA(cudaMemcpy2DAsync(e.tmp, e.ldf[l] * 4, blocks[l - 1], ni * 4, ni * 4, no, cudaMemcpyHostToDevice,
                                  e.st));
-      spb::launch_split(e.tmp, no * e.ld[l - 1], e.p_hi + e.w_off[l], e.p_lo + e.w_off[l], e.st);
+      spb::launch_split(e.tmp, no * e.ldf[l], e.p_hi + e.w_off[l], e.p_lo + e.w_off[l], e.st);
       SPB_CUDA(cudaMemcpyAsync(e.tmp, blocks[l - 1] + static_cast<long>(no) * ni, no * 4, cudaMemcpyHostToDevice,
                                e.st));
       spb::launch_split(e.tmp, no, e.p_hi + e.b_off[l], e.p_lo + e.b_off[l], e.st);
@@ -1037,9 +1305,9 @@ spb_status spb_get_params(spb_ctx* ctx, float* const* blocks) {
   return guard(ctx, [&] {
     auto& e = ctx->e;
     for (int l = 1; l <= e.L; ++l) {
-      const int no = e.w[l], ni = e.w[l - 1];
-      spb::launch_join(e.p_hi + e.w_off[l], e.p_lo + e.w_off[l], no * e.ld[l - 1], e.tmp, e.st);
-      SPB_CUDA(cudaMemcpy2DAsync(blocks[l - 1], ni * 4, e.tmp, e.ld[l - 1] * 4, ni * 4, no, cudaMemcpyDeviceToHost,
+      const int no = e.w[l], ni = e.fan[l];
+      spb::launch_join(e.p_hi + e.w_off[l], e.p_lo + e.w_off[l], no * e.ldf[l], e.tmp, e.st);
+      SPB_CUDA(cudaMemcpy2DAsync(blocks[l - 1], ni * 4, e.tmp, e.ldf[l] * 4, ni * 4, no, cudaMemcpyDeviceToHost,
                                  e.st));
       SPB_CUDA(cudaStreamSynchronize(e.st));
       spb::launch_join(e.p_hi + e.b_off[l], e.p_lo + e.b_off[l], no, e.tmp, e.st);
@@ -1055,8 +1323,8 @@ spb_status spb_get_grads(spb_ctx* ctx, float* const* blocks) {
     auto& e = ctx->e;
     for (int l = 1; l <= e.L; ++l) {
       if (!blocks[l - 1]) continue;
-      const int no = e.w[l], ni = e.w[l - 1];
-      SPB_CUDA(cudaMemcpy2DAsync(blocks[l - 1], ni * 4, e.grad + e.w_off[l], e.ld[l - 1] * 4, ni * 4, no,
+      const int no = e.w[l], ni = e.fan[l];
+      SPB_CUDA(cudaMemcpy2DAsync(blocks[l - 1], ni * 4, e.grad + e.w_off[l], e.ldf[l] * 4, ni * 4, no,
                                  cudaMemcpyDeviceToHost, e.st));
       SPB_CUDA(cudaMemcpyAsync(blocks[l - 1] + static_cast<long>(no) * ni, e.grad + e.b_off[l], no * 4,
                                cudaMemcpyDeviceToHost, e.st));
@@ -1096,16 +1364,15 @@ spb_status spb_partial_backprop(spb_ctx* ctx, const int* batch, int len, int suf
     e.ensure_rows(len);
     const int stop = L - suffix + 1;
     SPB_CUDA(cudaMemcpyAsync(e.idx_in, batch, len * sizeof(int), cudaMemcpyHostToDevice, e.st));
-    spb::launch_gather(e.X, e.ld[0], e.Y, e.w[0], e.nout, e.N, len, len, e.workers_dev, nullptr, 0, nullptr, 0, e.idx_in,
-                       e.idx, e.Hh[0], e.Hl[0], e.ld[0], e.ybatch, e.st);
+    e.enqueue_gather(e.X, e.ldx, len, len, nullptr, 0, nullptr, 0, e.idx_in, e.st);
     std::vector<int> row0(L + 1, len);
     std::vector<float> alpha(L + 1, 1.0f / static_cast<float>(len));
     for (int l = stop; l <= L; ++l) row0[l] = 0;
     e.enqueue_pass(len, row0, alpha, e.st);
     for (int l = stop; l <= L; ++l) {
       if (!out_blocks[l - 1]) continue;
-      const int no = e.w[l], ni = e.w[l - 1];
-      SPB_CUDA(cudaMemcpy2DAsync(out_blocks[l - 1], ni * 4, e.grad + e.w_off[l], e.ld[l - 1] * 4, ni * 4, no,
+      const int no = e.w[l], ni = e.fan[l];
+      SPB_CUDA(cudaMemcpy2DAsync(out_blocks[l - 1], ni * 4, e.grad + e.w_off[l], e.ldf[l] * 4, ni * 4, no,
                                  cudaMemcpyDeviceToHost, e.st));
       SPB_CUDA(cudaMemcpyAsync(out_blocks[l - 1] + static_cast<long>(no) * ni, e.grad + e.b_off[l], no * 4,
                                cudaMemcpyDeviceToHost, e.st));
@@ -1114,8 +1381,8 @@ spb_status spb_partial_backprop(spb_ctx* ctx, const int* batch, int len, int suf
     if (covered_from) *covered_from = stop;
     if (layer_ops)  // model.cpp:165-184, per sample
       for (int l = stop; l <= L; ++l) {
-        long long ops = static_cast<long long>(e.w[l]) * (e.w[l - 1] + 1);
-        if (l > stop) ops += static_cast<long long>(e.w[l]) * e.w[l - 1] + e.w[l - 1];
+        long long ops = static_cast<long long>(e.w[l]) * (e.fan[l] + 1);
+        if (l > stop) ops += static_cast<long long>(e.w[l]) * e.fan[l] + e.fan[l];
         layer_ops[l - 1] += ops * len;
       }
   });
@@ -1190,7 +1457,8 @@ spb_status spb_step_host(spb_ctx* ctx, const float* X_rows, const float* Y_rows,
     const int rows = static_cast<int>(e.workers.size()) * e.bw;
     e.ensure_rows(rows);
     cudaGraphExec_t g = e.get_graph(full_backprop != 0, true);
-    SPB_CUDA(cudaMemcpyAsync(e.xin, X_rows, static_cast<size_t>(rows) * e.w[0] * 4, cudaMemcpyHostToDevice, e.st));
+    const size_t per = e.conv_model ? static_cast<size_t>(e.ldx) : static_cast<size_t>(e.w[0]);
+    SPB_CUDA(cudaMemcpyAsync(e.xin, X_rows, static_cast<size_t>(rows) * per * 4, cudaMemcpyHostToDevice, e.st));
     SPB_CUDA(cudaMemcpyAsync(e.ybatch, Y_rows, static_cast<size_t>(rows) * e.nout * 4, cudaMemcpyHostToDevice, e.st));
     SPB_CUDA(cudaGraphLaunch(g, e.st));
     SPB_CUDA(cudaMemcpyAsync(loss_out, e.loss_dev, 4, cudaMemcpyDeviceToHost, e.st));
@@ -1211,8 +1479,7 @@ spb_status spb_loss(spb_ctx* ctx, double* out) {
       const int rows = std::min(chunk, e.N - s0);
       for (int i = 0; i < rows; ++i) iota[i] = s0 + i;
       SPB_CUDA(cudaMemcpyAsync(e.idx_in, iota.data(), rows * sizeof(int), cudaMemcpyHostToDevice, e.st));
-      spb::launch_gather(e.X, e.ld[0], e.Y, e.w[0], e.nout, e.N, rows, rows, e.workers_dev, nullptr, 0, nullptr, 0, e.idx_in,
-                         e.idx, e.Hh[0], e.Hl[0], e.ld[0], e.ybatch, e.st);
+      e.enqueue_gather(e.X, e.ldx, rows, rows, nullptr, 0, nullptr, 0, e.idx_in, e.st);
       std::vector<int> row0(e.L + 1, rows);  // forward + head only
       std::vector<float> alpha(e.L + 1, 0.f);
       e.enqueue_pass(rows, row0, alpha, e.st);
@@ -1394,8 +1661,7 @@ spb_status spb_profile_task(spb_ctx* ctx, int rows, int suffix, int reps, float*
     std::vector<int> iota(rows);
     for (int i = 0; i < rows; ++i) iota[i] = i % e.N;
     SPB_CUDA(cudaMemcpyAsync(e.idx_in, iota.data(), rows * sizeof(int), cudaMemcpyHostToDevice, e.st));
-    spb::launch_gather(e.X, e.ld[0], e.Y, e.w[0], e.nout, e.N, rows, rows, e.workers_dev, nullptr, 0, nullptr, 0, e.idx_in,
-                       e.idx, e.Hh[0], e.Hl[0], e.ld[0], e.ybatch, e.st);
+    e.enqueue_gather(e.X, e.ldx, rows, rows, nullptr, 0, nullptr, 0, e.idx_in, e.st);
     // One worker task (partial_backprop, spb.cpp:51-68, on one batch): the
     // forward + head, then dgrad / wgrad of the top `suffix` layers. Each
     // variant is captured into a graph and replayed `reps` times.
@@ -1438,10 +1704,17 @@ spb_status spb_profile_task(spb_ctx* ctx, int rows, int suffix, int reps, float*
     // blocks of the covered layers, the activations (split pairs) and, when
     // backpropagating, the three Delta buffers.
     double bytes = 8.0 * static_cast<double>(e.nflat);
-    for (int l = L - suffix + 1; l <= L; ++l) bytes += 4.0 * static_cast<double>(e.w[l]) * (e.w[l - 1] + 1);
-    for (int l = 0; l < L; ++l) bytes += 8.0 * rows * static_cast<double>(e.ld[l]);
-    bytes += 4.0 * rows * (e.w[0] + 2.0 * e.nout + 2.0);
-    if (suffix > 0) bytes += 3.0 * 8.0 * rows * static_cast<double>(e.ldd);
+    for (int l = L - suffix + 1; l <= L; ++l) bytes += 4.0 * static_cast<double>(e.w[l]) * (e.fan[l] + 1);
+    for (int l = 0; l < L; ++l) bytes += 8.0 * rows * e.pix[l] * static_cast<double>(e.ld[l]);
+    if (e.conv_model)  // im2col pairs kept for wgrad, plus the dgrad columns when backpropagating
+      for (int l = 1; l < L; ++l) bytes += 8.0 * rows * e.pix[l] * static_cast<double>(e.ldf[l]);
+    bytes += 4.0 * rows * (static_cast<double>(e.ldx) + 2.0 * e.nout + 2.0);
+    if (suffix > 0) {
+      double dmax = e.ldd, cmax = 0;
+      for (int l = 1; l < L; ++l)
+        dmax = std::max(dmax, e.pix[l] * static_cast<double>(e.ld[l])), cmax = std::max(cmax, e.pix[l] * static_cast<double>(e.ldf[l]));
+      bytes += 3.0 * 8.0 * rows * dmax + (e.conv_model ? 4.0 * rows * cmax : 0.0);
+    }
     *peak_mem_gb = bytes / 1e9;
   });
 }
@@ -1469,8 +1742,7 @@ spb_status spb_empirical_variance(spb_ctx* ctx, int k, int B, int trials, uint64
       std::vector<int> iota(N);
       std::iota(iota.begin(), iota.end(), 0);
       SPB_CUDA(cudaMemcpyAsync(e.idx_in, iota.data(), N * sizeof(int), cudaMemcpyHostToDevice, st));
-      spb::launch_gather(e.X, e.ld[0], e.Y, e.w[0], e.nout, N, N, N, e.workers_dev, nullptr, 0, nullptr, 0, e.idx_in, e.idx,
-                         e.Hh[0], e.Hl[0], e.ld[0], e.ybatch, st);
+      e.enqueue_gather(e.X, e.ldx, N, N, nullptr, 0, nullptr, 0, e.idx_in, st);
       {
         std::vector<int> row0(L + 1, 0);
         std::vector<float> alpha(L + 1, 1.0f / static_cast<float>(N));
@@ -1489,8 +1761,7 @@ spb_status spb_empirical_variance(spb_ctx* ctx, int k, int B, int trials, uint64
       e.step_plan(false, r0s, as);
       e.step_plan(true, r0f, af);
       for (int r = 1; r <= trials; ++r) {
-        spb::launch_gather(e.X, e.ld[0], e.Y, e.w[0], e.nout, N, rows, e.bw, e.workers_dev, nullptr, wseed, nullptr, r,
-                           nullptr, e.idx, e.Hh[0], e.Hl[0], e.ld[0], e.ybatch, st);
+        e.enqueue_gather(e.X, e.ldx, rows, e.bw, nullptr, wseed, nullptr, r, nullptr, st);
         e.enqueue_pass(rows, r0s, as, st);
         spb::launch_sqdist(G, e.grad, e.nflat, dist + (r - 1), st);
         e.enqueue_pass(rows, r0f, af, st);
@@ -1513,8 +1784,7 @@ spb_status spb_empirical_variance(spb_ctx* ctx, int k, int B, int trials, uint64
         std::vector<float> alpha(L + 1, 1.0f);
         const long a = e.w_off[first], b = e.b_off[last] + spb::round_up(e.w[last], 32);
         for (int t = 0; t < trials; ++t) {
-          spb::launch_gather(e.X, e.ld[0], e.Y, e.w[0], e.nout, N, 1, 1, e.workers_dev, nullptr, 0, nullptr, 0,
-                             samp + static_cast<long>(m - 1) * trials + t, e.idx, e.Hh[0], e.Hl[0], e.ld[0], e.ybatch, st);
+          e.enqueue_gather(e.X, e.ldx, 1, 1, nullptr, 0, nullptr, 0, samp + static_cast<long>(m - 1) * trials + t, st);
           e.enqueue_pass(1, row0, alpha, st);
           spb::launch_sqdist(G + a, e.grad + a, b - a, dist + static_cast<long>(2 + m - 1) * trials + t, st);
         }

@@ -189,7 +189,10 @@ Plan plan_gemm(int M, int N, int K, long ws_floats, bool can_split) {
   if (g_force_variant >= 0) return {g_force_variant == 1, 1};
   Plan best{false, 1};
   double best_t = 1e30;
-  for (int sp = 1; sp <= 8; ++sp) {
+  // Split counts: up to 8 for the MLP shapes; far more for the few-tile,
+  // huge-K wgrad GEMMs of the conv model (K = pixel rows, up to ~1M).
+  static const int kSplits[] = {1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 32, 48, 64, 96, 128, 148, 192, 256, 296};
+  for (int sp : kSplits) {
     if (sp > 1 && (!can_split || static_cast<long>(sp) * M * round_up(N, 4) > ws_floats || kb < 8 * sp)) break;
     const int kbs = (kb + sp - 1) / sp;
     const long units = t1 * ((kb + kbs - 1) / kbs);
@@ -228,12 +231,13 @@ int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue&
   static const bool no_split = std::getenv("SPB_NO_SPLITK") != nullptr;  // tuning experiments
   const Plan plan = plan_gemm(A.mn, B.mn, A.k, ep.splitk_ws && !no_split ? ep.splitk_ws_floats : 0,
                               ep.splitk_ws != nullptr && (epi == kEpiFwdTanh || epi == kEpiDgradTanh ||
-                                                          epi == kEpiFwdLinear));
+                                                          epi == kEpiFwdLinear || epi == kEpiStoreScaled));
   if (plan.splits > 1) {
     switch (epi) {
       case kEpiFwdTanh: launch_splitk<kEpiFwdTanh>(A, B, ep, s, plan.splits); break;
       case kEpiDgradTanh: launch_splitk<kEpiDgradTanh>(A, B, ep, s, plan.splits); break;
       case kEpiFwdLinear: launch_splitk<kEpiFwdLinear>(A, B, ep, s, plan.splits); break;
+      case kEpiStoreScaled: launch_splitk<kEpiStoreScaled>(A, B, ep, s, plan.splits); break;
       default: throw std::invalid_argument("gemm: split-K not supported for this epilogue");
     }
     return 2;

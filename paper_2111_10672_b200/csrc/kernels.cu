@@ -85,7 +85,7 @@ __global__ void head_kernel(const float* __restrict__ h_hi, const float* __restr
                             long ldw, const float* __restrict__ b_hi, const float* __restrict__ b_lo,
                             const float* __restrict__ y, float* __restrict__ delta, float* __restrict__ row_loss,
                             float* __restrict__ dn_hi, float* __restrict__ dn_lo, long ldd, int cont_row0,
-                            int tanh_out) {
+                            int tanh_out, int dn_act) {
   const int warps = blockDim.x / 32;
   const int r = blockIdx.x * warps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
@@ -144,8 +144,13 @@ __global__ void head_kernel(const float* __restrict__ h_hi, const float* __restr
         sv.w = fmaf(d[o], wa.w + wb.w, sv.w);
       }
       const float4 a = hh[c], b = hl[c];
-      float v[4] = {sv.x * (1.0f - (a.x + b.x) * (a.x + b.x)), sv.y * (1.0f - (a.y + b.y) * (a.y + b.y)),
-                    sv.z * (1.0f - (a.z + b.z) * (a.z + b.z)), sv.w * (1.0f - (a.w + b.w) * (a.w + b.w))};
+      float v[4] = {sv.x, sv.y, sv.z, sv.w};
+      if (dn_act) {
+        v[0] *= 1.0f - (a.x + b.x) * (a.x + b.x);
+        v[1] *= 1.0f - (a.y + b.y) * (a.y + b.y);
+        v[2] *= 1.0f - (a.z + b.z) * (a.z + b.z);
+        v[3] *= 1.0f - (a.w + b.w) * (a.w + b.w);
+      }
       const float4 vh = make_float4(tf32_rna(v[0]), tf32_rna(v[1]), tf32_rna(v[2]), tf32_rna(v[3]));
       oh[c] = vh;
       ol[c] = make_float4(v[0] - vh.x, v[1] - vh.y, v[2] - vh.z, v[3] - vh.w);
@@ -154,24 +159,26 @@ __global__ void head_kernel(const float* __restrict__ h_hi, const float* __restr
 }
 
 constexpr int kColThreads = 256;
-constexpr int kRowsPerSplit = 32;
+// Rows per partial-sum split: 32, growing for very tall inputs (conv pixel
+// rows) so pass 2 sums at most ~1024 partials per column.
+inline int rows_per_split(int rows) { return std::max(32, static_cast<int>(round_up((rows + 1023) / 1024, 32))); }
 
 // Pass 1: partial[split][o][c] = sum over this split's rows.
 __global__ void colreduce_partial_kernel(const float* __restrict__ hi, const float* __restrict__ lo, long ld, int r0,
                                          int r1, int ncols, const float* __restrict__ rowvec, int nvec, long ldv,
-                                         float* __restrict__ partial) {
+                                         float* __restrict__ partial, int rps) {
   const int c = blockIdx.x * kColThreads + threadIdx.x;
   const int split = blockIdx.y;
-  const int ra = r0 + split * kRowsPerSplit;
-  const int rb = min(r1, ra + kRowsPerSplit);
+  const int ra = r0 + split * rps;
+  const int rb = min(r1, ra + rps);
   if (c >= ncols) return;
   float acc[kMaxOut];
 #pragma unroll
   for (int o = 0; o < kMaxOut; ++o) acc[o] = 0.f;
 #pragma unroll 8
   for (int r = ra; r < rb; ++r) {
-    float v = hi[r * ld + c];
-    if (lo) v += lo[r * ld + c];
+    float v = hi[static_cast<long>(r) * ld + c];
+    if (lo) v += lo[static_cast<long>(r) * ld + c];
     if (!rowvec) {
       acc[0] += v;
     } else {
@@ -325,18 +332,19 @@ void launch_split_rows(const float* x, long ldx_in, int rows, int cols, float* h
 void launch_head(const float* h_hi, const float* h_lo, long ldh, int rows, int n_in, int n_out, const float* w_hi,
                  const float* w_lo, long ldw, const float* b_hi, const float* b_lo, const float* y, float* delta,
                  float* row_loss, float* dn_hi, float* dn_lo, long ldd, int cont_row0, bool tanh_out,
-                 cudaStream_t s) {
+                 cudaStream_t s, bool dn_act) {
   if (rows <= 0) return;
   if (n_out > kMaxOut) throw std::invalid_argument("head: n_out > 16");
   const int warps = 8;
   head_kernel<<<(rows + warps - 1) / warps, warps * 32, 0, s>>>(h_hi, h_lo, ldh, rows, n_in, n_out, w_hi, w_lo, ldw,
                                                                 b_hi, b_lo, y, delta, row_loss, dn_hi, dn_lo, ldd,
-                                                                cont_row0, tanh_out ? 1 : 0);
+                                                                cont_row0, tanh_out ? 1 : 0, dn_act ? 1 : 0);
   SPB_CUDA(cudaGetLastError());
 }
 
 long colreduce_scratch(int rows, int ncols, int nvec) {
-  const long nsplit = (rows + kRowsPerSplit - 1) / kRowsPerSplit;
+  const int rps = rows_per_split(rows);
+  const long nsplit = (rows + rps - 1) / rps;
   return (nsplit < 1 ? 1 : nsplit) * nvec * static_cast<long>(ncols);
 }
 
@@ -346,9 +354,10 @@ void launch_colreduce(const float* hi, const float* lo, long ld, int r0, int r1,
   if (nvec > kMaxOut) throw std::invalid_argument("colreduce: nvec > 16");
   const int rows = r1 - r0;
   if (rows <= 0 || ncols <= 0) return;
-  const int nsplit = (rows + kRowsPerSplit - 1) / kRowsPerSplit;
+  const int rps = rows_per_split(rows);
+  const int nsplit = (rows + rps - 1) / rps;
   dim3 g1((ncols + kColThreads - 1) / kColThreads, nsplit);
-  colreduce_partial_kernel<<<g1, kColThreads, 0, s>>>(hi, lo, ld, r0, r1, ncols, rowvec, nvec, ldv, scratch);
+  colreduce_partial_kernel<<<g1, kColThreads, 0, s>>>(hi, lo, ld, r0, r1, ncols, rowvec, nvec, ldv, scratch, rps);
   SPB_CUDA(cudaGetLastError());
   const long tot = static_cast<long>(nvec) * ncols;
   UpdArgs u{nullptr, nullptr, 0.f, 0.f, 0.f};

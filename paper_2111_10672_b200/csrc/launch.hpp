@@ -57,11 +57,12 @@ void launch_gather(const float* X, long ldx, const float* Y, int n0, int nout, i
 void launch_split_rows(const float* x, long ldx_in, int rows, int cols, float* hi, float* lo, long ld,
                        cudaStream_t s);
 // Head layer L (n_out <= 16): out = H W^T + b, delta = out - y, row_loss,
-// and for rows >= cont_row0: dnext = (delta W) * (1 - H^2) as a split pair.
+// and for rows >= cont_row0: dnext = (delta W) * (1 - H^2) as a split pair
+// (dn_act = false: dnext = delta W, for the pooled conv features).
 void launch_head(const float* h_hi, const float* h_lo, long ldh, int rows, int n_in, int n_out, const float* w_hi,
                  const float* w_lo, long ldw, const float* b_hi, const float* b_lo, const float* y,
                  float* delta, float* row_loss, float* dn_hi, float* dn_lo, long ldd, int cont_row0,
-                 bool tanh_out, cudaStream_t s);
+                 bool tanh_out, cudaStream_t s, bool dn_act = true);
 // out[o * ld_out + c] = alpha * sum_{r in [r0,r1)} vec(r,o) * (hi + lo)[r, c]
 // (vec = 1 when rowvec == nullptr, nvec = 1), deterministic two-pass column
 // reduction. scratch must hold colreduce_scratch(...) floats.

@@ -109,6 +109,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "spb_comm_bench": (i, [vp, C.c_longlong, i]),
         "spb_profile_task": (i, [vp, i, i, i, fp, fp, C.POINTER(C.c_double)]),
         "spb_empirical_variance": (i, [vp, i, i, i, u64, C.POINTER(C.c_double)]),
+        "spb_create_conv": (i, [ip, i, i, i, i, i, C.POINTER(vp)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -125,7 +126,7 @@ EXPORTED = [
     "spb_last_batch", "spb_launches_per_step", "spb_make_random_chain_mlp",
     "spb_get_grads", "spb_profile_step", "spb_time_train_steps", "spb_bucket_plan", "spb_set_fused_update",
     "spb_comm_mode", "spb_comm_selftest", "spb_comm_bench", "spb_profile_task",
-    "spb_empirical_variance",
+    "spb_empirical_variance", "spb_create_conv",
 ]
 
 PROFILE_CLASSES = ["gemm_fwd", "gemm_wgrad", "gemm_dgrad", "head", "colreduce", "update", "gather", "comm"]
@@ -461,6 +462,74 @@ def make_random_chain_mlp(widths: Sequence[int], samples: int, seed: int, **kw) 
     tanh(sum x) + 0.1 N(0,1)), evaluated by the C++ host generator."""
     X, Y, blocks = gen_chain_mlp(widths, samples, seed)
     return ChainMlp(widths, X, Y, blocks, **kw)
+
+
+class ConvNet(ChainMlp):
+    """CIFAR10-shaped convolutional SPB model on one B200 (SURVEY.md 8f-1,
+    BASELINE configs[3]): 3x3 convolutions (padding 1, stride 1 or 2) with
+    tanh, lowered to the tcgen05 GEMMs by im2col; global average pool; affine
+    head; per-sample loss 0.5 ||out - y||^2. The reference has no conv model:
+    this mirrors its LayeredModel interface (layer_count, block_dims,
+    partial_backprop, loss) and its SPB rules apply unchanged.
+
+    in_shape = (h, w, c); convs = [(c_out, stride), ...]; samples are NHWC
+    images; block l = W_l [c_out x 9 c_in] (columns (ky*3+kx)*c_in + ci), b_l."""
+
+    kind = "ConvNet"
+
+    def __init__(self, in_shape, convs, nout: int, inputs, targets, weights, k: int = 1, per_worker_batch: int = 1,
+                 device: int = 0):
+        lib = load_library()
+        self.in_shape = tuple(int(v) for v in in_shape)
+        self.convs = [(int(c), int(st)) for c, st in convs]
+        self.nout = int(nout)
+        self._dims = convnet_block_dims(self.in_shape, self.convs, self.nout)
+        h, w, c = self.in_shape
+        X = np.ascontiguousarray(inputs, dtype=np.float32).reshape(len(inputs), -1)
+        Y = np.ascontiguousarray(targets, dtype=np.float32).reshape(len(targets), -1)
+        if X.shape[0] == 0 or X.shape[0] != Y.shape[0] or X.shape[1] != h * w * c or Y.shape[1] != self.nout:
+            raise ArgumentError("convnet: dataset shape mismatch")
+        if len(weights) != len(self._dims) or any(np.size(wb) != d for wb, d in zip(weights, self._dims)):
+            raise ArgumentError("convnet: weight block size mismatch")
+        geom = np.asarray([h, w, c] + [v for cs in self.convs for v in cs], dtype=np.int32)
+        ctx = C.c_void_p()
+        _check(lib.spb_create_conv(_ip(geom), len(self.convs), self.nout, k, per_worker_batch, device, C.byref(ctx)))
+        self._ctx = ctx
+        self.widths = [c] + [cs[0] for cs in self.convs] + [self.nout]
+        self.k, self.per_worker_batch = k, per_worker_batch
+        _check(lib.spb_set_dataset(ctx, _fp(X), _fp(Y), X.shape[0]), ctx)
+        self._N = X.shape[0]
+        self._initial = [np.asarray(b, dtype=np.float32).copy() for b in weights]
+        self.set_params(self._initial)
+
+
+def convnet_block_dims(in_shape, convs, nout: int) -> List[int]:
+    c = in_shape[2]
+    dims = []
+    for co, _ in convs:
+        dims.append(co * 9 * c + co)
+        c = co
+    dims.append(nout * c + nout)
+    return dims
+
+
+def gen_convnet(in_shape, convs, nout: int, samples: int, seed: int):
+    """Synthetic CIFAR-shaped data and a random init (numpy, deterministic):
+    images uniform in [-1, 1), targets uniform in [-1, 1), weights
+    N(0, 1/fan_in), biases 0.01 N(0, 1). Returns X [samples, h*w*c], Y, blocks."""
+    rng = np.random.default_rng(seed)
+    h, w, c = in_shape
+    X = rng.uniform(-1, 1, size=(samples, h * w * c)).astype(np.float32)
+    Y = rng.uniform(-1, 1, size=(samples, nout)).astype(np.float32)
+    blocks = []
+    cin = c
+    for co, _ in convs:
+        Wl = rng.standard_normal((co, 9 * cin)) / np.sqrt(9 * cin)
+        blocks.append(np.concatenate([Wl.ravel(), 0.01 * rng.standard_normal(co)]).astype(np.float32))
+        cin = co
+    Wl = rng.standard_normal((nout, cin)) / np.sqrt(cin)
+    blocks.append(np.concatenate([Wl.ravel(), 0.01 * rng.standard_normal(nout)]).astype(np.float32))
+    return X, Y, blocks
 
 
 def gen_chain_mlp(widths: Sequence[int], samples: int, seed: int):
