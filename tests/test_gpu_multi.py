@@ -159,3 +159,57 @@ def test_nvls_multicast_selftest(tmp_path):
     for r in range(world):
         bad, on = np.load(tmp_path / f"s{r}.npy")
         assert on == 1 and bad == 0
+
+
+CSHAPE, CCONVS, CNOUT = (8, 8, 3), [(8, 1), (12, 2), (16, 1)], 3
+
+
+def _rank_conv(rank, world, port, out_dir, mode):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+
+    from paper_2111_10672_b200 import spb
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["SPB_COMM"] = mode
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    X, Y, W = spb.gen_convnet(CSHAPE, CCONVS, CNOUT, N, DSEED)
+    m = spb.ConvNet(CSHAPE, CCONVS, CNOUT, X, Y, W, k=K, per_worker_batch=BW, device=rank)
+    m.comm_init_torch(dist, rank, world)
+    assert m.comm_mode == mode
+    m.set_optimizer(LR)
+    m.train_steps(SEED, 1, 3)
+    np.savez(os.path.join(out_dir, f"c{rank}.npz"), *m.get_params())
+    dist.barrier()
+    m.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["p2p", "nvls", "nccl"])
+def test_multi_gpu_convnet_matches_oracle(tmp_path, orc, mode):
+    """The ConvNet (cfg4 shape family) on 2-4 GPUs: 3 SPB steps equal the
+    single-process fp64 conv oracle (1e-4) and are bit-identical across ranks."""
+    world = min(_gpus(), 4)
+    if world < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import torch.multiprocessing as mp
+
+    from oracle.conv_oracle import ConvOracle
+    from paper_2111_10672_b200 import spb
+
+    mp.start_processes(_rank_conv, args=(world, _free_port(), str(tmp_path), mode), nprocs=world, start_method="spawn")
+    X, Y, W = spb.gen_convnet(CSHAPE, CCONVS, CNOUT, N, DSEED)
+    o = ConvOracle(CSHAPE, CCONVS, CNOUT)
+    B = [w.astype(np.float64) for w in W]
+    for s in range(1, 4):
+        o.spb_step(B, X.astype(np.float64), Y.astype(np.float64), K, BW, LR, SEED, s, orc)
+    outs = [np.load(os.path.join(tmp_path, f"c{r}.npz")) for r in range(world)]
+    for l in range(o.L):
+        got = outs[0][f"arr_{l}"]
+        assert np.linalg.norm(got - B[l]) / np.linalg.norm(B[l]) <= 1e-4
+        for r in range(world):
+            assert np.array_equal(outs[r][f"arr_{l}"], got)
