@@ -263,6 +263,48 @@ def spb_savings(widths, k, bw, world):
             "saved_exchange_bytes_frac": round(1 - out["spb"][1] / out["full"][1], 4)}
 
 
+CFG4 = dict(workload="cfg4: ConvNet 32x32x3 (CIFAR10 shape), 3x3 convs at ResNet18 widths "
+                     "64,64,128/2,128,256/2,256,512/2,512 + global avg pool + head 10, k=8 SPB workers, batch 128/worker",
+            shape=(32, 32, 3), convs=[(64, 1), (64, 1), (128, 2), (128, 1), (256, 2), (256, 1), (512, 2), (512, 1)],
+            nout=10, k=8, bw=128, N=8192, data_seed=7, step_seed=11, lr=0.01, momentum=0.9, weight_decay=1e-4)
+
+
+def run_cfg4(world, rank, local, dist, K, W_):
+    """BASELINE configs[3] on the same engine: SPB vs full backprop samples/s
+    (CUDA events on the step stream, max over ranks) and the eager per-class
+    breakdown. Reported beside the cfg3 headline, not as it."""
+    from paper_2111_10672_b200 import spb
+
+    c = CFG4
+    X, Y, W = spb.gen_convnet(c["shape"], c["convs"], c["nout"], c["N"], c["data_seed"])
+    m = spb.ConvNet(c["shape"], c["convs"], c["nout"], X, Y, W, k=c["k"], per_worker_batch=c["bw"], device=local)
+    if world > 1:
+        m.comm_init_torch(dist, rank, world)
+    m.set_optimizer(c["lr"], c["momentum"], c["weight_decay"])
+    out = {"workload": c["workload"], "params": int(sum(spb.convnet_block_dims(c["shape"], c["convs"], c["nout"]))),
+           "data": "synthetic (numpy uniform images/targets, seed 7)", "lowering": "im2col + tcgen05 3xTF32 GEMMs"}
+    for full in (False, True):
+        m.set_params(m.initial_params())
+        m.train_steps(c["step_seed"], 1, W_, full_backprop=full)
+        m.synchronize()
+        barrier(dist)
+        ms = m.time_train_steps(c["step_seed"], 1 + W_, K, full_backprop=full)
+        barrier(dist)
+        ms = max_over_ranks(dist, ms)
+        prof, _ = m.profile_step(c["step_seed"], 1000, full_backprop=full)
+        gemm_ms = sum(prof[q]["ms"] for q in ("gemm_fwd", "gemm_wgrad", "gemm_dgrad"))
+        gemm_fl = sum(prof[q]["work"] for q in ("gemm_fwd", "gemm_wgrad", "gemm_dgrad"))
+        out["full_backprop" if full else "spb"] = {
+            "value": round(K * c["k"] * c["bw"] / (ms * 1e-3), 2), "unit": UNIT, "ms_per_step": round(ms / K, 4),
+            "launches_per_step": m.launches_per_step(),
+            "gemm_alg_tflops": round(gemm_fl / max(gemm_ms, 1e-9) / 1e9, 1),
+            "phase_ms": {q: round(prof[q]["ms"], 3) for q in prof if prof[q]["launches"]}}
+    out["spb_speedup"] = round(out["spb"]["value"] / out["full_backprop"]["value"], 4)
+    barrier(dist)
+    m.close()
+    return out
+
+
 def run_b200(args, world, rank, local, dist):
     from paper_2111_10672_b200 import spb
 
@@ -365,6 +407,11 @@ def run_b200(args, world, rank, local, dist):
     barrier(dist)
     m.close()
     del m
+    if not args.no_conv:
+        try:
+            line["cfg4_convnet"] = run_cfg4(world, rank, local, dist, min(K, 10), W_)
+        except Exception as ex:  # noqa: BLE001
+            line["cfg4_convnet"] = {"error": repr(ex)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, kind, cores, sample = cpu_reference(cfg, 1, 0, REF_BW)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
@@ -379,6 +426,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-conv", action="store_true", help="skip the cfg4 ConvNet sub-measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         world = int(os.environ.get("WORLD_SIZE", "1"))

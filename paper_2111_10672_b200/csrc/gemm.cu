@@ -196,7 +196,7 @@ Plan plan_gemm(int M, int N, int K, long ws_floats, bool can_split) {
     if (sp > 1 && (!can_split || static_cast<long>(sp) * M * round_up(N, 4) > ws_floats || kb < 8 * sp)) break;
     const int kbs = (kb + sp - 1) / sp;
     const long units = t1 * ((kb + kbs - 1) / kbs);
-    double t = static_cast<double>((units + sms - 1) / sms) * (0.62 * kbs + 2.8);
+    double t = static_cast<double>((units + sms - 1) / sms) * ((N <= 64 && sp == 1 ? 0.31 : 0.62) * kbs + 2.8);
     if (sp > 1) t += 3.0 + (sp + 2.0) * M * static_cast<double>(N) * 4.0 / 4.0e6;
     if (t < best_t) best_t = t, best = {false, sp};
   }
@@ -255,6 +255,16 @@ int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue&
       case kEpiDgradTanh: dispatch_2sm<kEpiDgradTanh>(A, B, ep, s); break;
       case kEpiFwdLinear: dispatch_2sm<kEpiFwdLinear>(A, B, ep, s); break;
       case kEpiWgradUpdate: launch_2sm<true, true, kEpiWgradUpdate>(A, B, ep, s); break;
+      default: throw std::invalid_argument("gemm: bad epilogue");
+    }
+    return 1;
+  }
+  if (B.mn <= 64 && epi != kEpiWgradUpdate) {  // narrow outputs (64-channel convs): 128 x 64 tiles, no idle MMA half
+    switch (epi) {
+      case kEpiFwdTanh: dispatch_major<64, kEpiFwdTanh>(A, B, ep, s); break;
+      case kEpiStoreScaled: dispatch_major<64, kEpiStoreScaled>(A, B, ep, s); break;
+      case kEpiDgradTanh: dispatch_major<64, kEpiDgradTanh>(A, B, ep, s); break;
+      case kEpiFwdLinear: dispatch_major<64, kEpiFwdLinear>(A, B, ep, s); break;
       default: throw std::invalid_argument("gemm: bad epilogue");
     }
     return 1;
