@@ -478,8 +478,10 @@ struct Engine {
       Hh[l] = alloc<float>(S * pix[l] * ld[l]);
       Hl[l] = alloc<float>(S * pix[l] * ld[l]);
       if (l >= 1) {
-        Ch[l] = alloc<float>(S * pix[l] * ldf[l]);
-        Cl[l] = alloc<float>(S * pix[l] * ldf[l]);
+        if (!conv_tma(l)) {  // implicit-GEMM layers read H_{l-1} through TMA im2col maps instead
+          Ch[l] = alloc<float>(S * pix[l] * ldf[l]);
+          Cl[l] = alloc<float>(S * pix[l] * ldf[l]);
+        }
         dmax = std::max(dmax, S * pix[l] * ld[l]);
         cmax = std::max(cmax, S * pix[l] * ldf[l]);
         sc = std::max(sc, colreduce_scratch(static_cast<int>(S * pix[l]), w[l], 1));
@@ -506,6 +508,13 @@ struct Engine {
     SPB_CUDA(cudaMemcpy(iota_dev, io.data(), S * sizeof(int), cudaMemcpyHostToDevice));
   }
 
+  // Convolution l runs as an implicit GEMM (TMA im2col, no column matrix)
+  // when its input channels fill whole 128-byte TMA boxes.
+  bool conv_tma(int l) const {
+    static const bool off = std::getenv("SPB_CONV_IM2COL") != nullptr;  // A/B experiments: materialise columns
+    return !off && cg[l].c_in % 32 == 0 && ld[l - 1] % 32 == 0;
+  }
+
   // Gathers `rows` samples (ChainMlp: rows; ConvNet: pixel rows of the
   // samples) into H_0 and ybatch: from idx_in, or drawn on the device.
   void enqueue_gather(const float* Xsrc, long ldxs, int rows, int bw_, const uint64_t* seed_dev, uint64_t seed_host,
@@ -530,9 +539,13 @@ struct Engine {
     const int Lc = L - 1;
     for (int l = 1; l <= Lc; ++l) {
       const int M = static_cast<int>(samples * pix[l]);
-      pbeg(s);
-      launch_im2col(Hh[l - 1], Hl[l - 1], ld[l - 1], cg[l], 0, M, Ch[l], Cl[l], ldf[l], s);
-      pend(kClsGather, 0, s);
+      const bool tma = conv_tma(l);
+      if (!tma) {
+        pbeg(s);
+        launch_im2col(Hh[l - 1], Hl[l - 1], ld[l - 1], cg[l], 0, M, Ch[l], Cl[l], ldf[l], s);
+        pend(kClsGather, 0, s);
+        ++n;
+      }
       Operand A{Ch[l], Cl[l], ldf[l], M, fan[l], false};
       Operand B{p_hi + w_off[l], p_lo + w_off[l], ldf[l], w[l], fan[l], false};
       GemmEpilogue ep{};
@@ -546,7 +559,12 @@ struct Engine {
       ep.splitk_ws = splitk_ws;
       ep.splitk_ws_floats = kSplitkWsFloats;
       pbeg(s);
-      n += 1 + gemm_tf32x3(A, B, kEpiFwdTanh, ep, s);
+      if (tma) {
+        ConvSrc src{Hh[l - 1], Hl[l - 1], ld[l - 1], samples, cg[l]};
+        n += gemm_conv_fwd(src, B, ep, s);
+      } else {
+        n += gemm_tf32x3(A, B, kEpiFwdTanh, ep, s);
+      }
       pend(kClsFwd, 2.0 * M * w[l] * fan[l], s);
     }
     const bool has_next = Lc >= 1 && row0[Lc] < samples;
@@ -603,7 +621,9 @@ struct Engine {
       }
       {  // wgrad: dW_l = alpha_l * Delta_l[r0:]^T col_l[r0:]
         Operand A{Dh[b] + r0 * ld[l], Dl[b] + r0 * ld[l], ld[l], w[l], static_cast<int>(cnt), true};
-        Operand B{Ch[l] + r0 * ldf[l], Cl[l] + r0 * ldf[l], ldf[l], fan[l], static_cast<int>(cnt), true};
+        const bool tma = conv_tma(l);
+        Operand B{tma ? nullptr : Ch[l] + r0 * ldf[l], tma ? nullptr : Cl[l] + r0 * ldf[l], ldf[l], fan[l],
+                  static_cast<int>(cnt), true};
         GemmEpilogue ep{};
         ep.out_hi = grad + w_off[l];
         ep.ld_out = ldf[l];
@@ -613,7 +633,12 @@ struct Engine {
         ep.splitk_ws = splitk_ws;  // few output tiles, K = pixel rows: split K (single stream)
         ep.splitk_ws_floats = kSplitkWsFloats;
         pbeg(s);
-        n += gemm_tf32x3(A, B, kEpiStoreScaled, ep, s);
+        if (tma) {
+          ConvSrc src{Hh[l - 1], Hl[l - 1], ld[l - 1], samples, cg[l]};
+          n += gemm_conv_wgrad(A, src, r0, ep, s);
+        } else {
+          n += gemm_tf32x3(A, B, kEpiStoreScaled, ep, s);
+        }
         pend(kClsWgrad, 2.0 * cnt * w[l] * fan[l], s);
       }
       pbeg(s);

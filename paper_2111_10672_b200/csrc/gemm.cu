@@ -10,6 +10,7 @@
 
 #include "gemm_2sm.cuh"
 #include "gemm_tf32x3.cuh"
+#include "conv.hpp"
 #include "launch.hpp"
 
 namespace spb {
@@ -27,6 +28,42 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   });
   if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
   return fn;
+}
+
+PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col_fn() {
+  static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(p);
+  });
+  if (!fn) throw CudaError("cuTensorMapEncodeIm2col unavailable");
+  return fn;
+}
+
+// im2col map of an NHWC activation tensor (row stride ld floats per pixel)
+// for a 3x3 / padding-1 convolution: the window of output pixel (p, q)
+// starts at (q*s - 1, p*s - 1); bounding box corners -1 / -1 (so the walk
+// covers exactly out_w x out_h window origins per image, CUTLASS's
+// q = (W + upper - lower - 1) / s + 1), traversal stride s, 32 channels per
+// pixel, `pixels` pixels per box, zero fill outside the image.
+CUtensorMap im2col_map(const float* base, const ConvSrc& src, int pixels, CUtensorMapSwizzle swz) {
+  CUtensorMap m;
+  const ConvGeom& g = src.g;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.c_in), static_cast<cuuint64_t>(g.in_w),
+                        static_cast<cuuint64_t>(g.in_h), static_cast<cuuint64_t>(src.samples)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(src.ld) * 4, static_cast<cuuint64_t>(src.ld) * 4 * g.in_w,
+                           static_cast<cuuint64_t>(src.ld) * 4 * g.in_w * g.in_h};
+  int lower[2] = {-1, -1}, upper[2] = {-1, -1};
+  cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(g.stride), static_cast<cuuint32_t>(g.stride), 1};
+  CUresult r = encode_im2col_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, lower,
+                                  upper, 32, static_cast<cuuint32_t>(pixels), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeIm2col failed: " + std::to_string(static_cast<int>(r)));
+  return m;
 }
 
 // 2D fp32 tensor map, 128-byte swizzle (16 B or 32 B atoms), zero fill out of bounds.
@@ -62,17 +99,19 @@ CUtensorMap operand_map(const Operand& X, const float* base, int tile_rows) {
   return tmap2d(base, X.mn, X.k, X.ld, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
-template <int BN, bool AM, bool BM_, int EPI, bool TMA_UPD = false>
-void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, int splits = 1) {
-  auto kern = gemm_tf32x3_kernel<BN, AM, BM_, EPI, TMA_UPD>;
+template <int BN, bool AM, bool BM_, int EPI, bool TMA_UPD = false, int IC = 0>
+void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, int splits = 1,
+                 const CUtensorMap* ic_a = nullptr, const CUtensorMap* ic_b = nullptr, ConvTmaArgs ic = {}) {
+  auto kern = gemm_tf32x3_kernel<BN, AM, BM_, EPI, TMA_UPD, IC>;
   constexpr int smem = GemmCfg<BN, TMA_UPD>::kSmem;
   static bool configured = false;
   if (!configured) {
     SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  CUtensorMap ah = operand_map(A, A.hi, kBM), al = operand_map(A, A.lo, kBM);
-  CUtensorMap bh = operand_map(B, B.hi, BN), bl = operand_map(B, B.lo, BN);
+  // IC == 1: A comes from ic_a[0..1] (im2col hi / lo); IC == 2: B from ic_b.
+  CUtensorMap ah = IC == 1 ? ic_a[0] : operand_map(A, A.hi, kBM), al = IC == 1 ? ic_a[1] : operand_map(A, A.lo, kBM);
+  CUtensorMap bh = IC == 2 ? ic_b[0] : operand_map(B, B.hi, BN), bl = IC == 2 ? ic_b[1] : operand_map(B, B.lo, BN);
   const int num_kb = (A.k + kBK - 1) / kBK;
   const int num_m = (A.mn + kBM - 1) / kBM, num_n = (B.mn + BN - 1) / BN;
   const int tiles = num_m * num_n;
@@ -85,7 +124,7 @@ void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cud
     wl = tmap2d(ep.out_lo, B.mn, A.mn, ep.ld_out, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
     wm = ep.mom ? tmap2d(ep.mom, B.mn, A.mn, ep.ld_out, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B) : wh;
   }
-  kern<<<grid, 256, smem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, ep, wh, wl, wm);
+  kern<<<grid, 256, smem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, ep, wh, wl, wm, ic);
   SPB_CUDA(cudaGetLastError());
 }
 
@@ -219,6 +258,52 @@ void dispatch_major(const Operand& A, const Operand& B, const GemmEpilogue& ep, 
 }  // namespace
 
 void gemm_force_variant(int v) { g_force_variant = v; }
+
+int gemm_conv_fwd(const ConvSrc& src, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
+  const ConvGeom& g = src.g;
+  if (g.c_in % 32 || src.ld % 32) throw std::invalid_argument("gemm_conv_fwd: c_in and ld must be multiples of 32");
+  const int M = src.samples * g.out_h * g.out_w, K = 9 * g.c_in;
+  if (B.k != K || B.mn_major) throw std::invalid_argument("gemm_conv_fwd: B must be K-major [c_out x 9 c_in]");
+  CUtensorMap a[2] = {im2col_map(src.hi, src, kBM, CU_TENSOR_MAP_SWIZZLE_128B),
+                      im2col_map(src.lo, src, kBM, CU_TENSOR_MAP_SWIZZLE_128B)};
+  const ConvTmaArgs ic{g.out_h * g.out_w, g.out_w, g.stride, g.c_in, 0};
+  Operand A{nullptr, nullptr, 4, M, K, false};  // shape only: tiles come from the im2col maps
+  if (B.mn <= 64)
+    launch_inst<64, false, false, kEpiFwdTanh, false, 1>(A, B, ep, s, 1, a, nullptr, ic);
+  else
+    launch_inst<128, false, false, kEpiFwdTanh, false, 1>(A, B, ep, s, 1, a, nullptr, ic);
+  return 1;
+}
+
+int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const GemmEpilogue& ep, cudaStream_t s) {
+  const ConvGeom& g = src.g;
+  if (g.c_in % 32 || src.ld % 32) throw std::invalid_argument("gemm_conv_wgrad: c_in and ld must be multiples of 32");
+  if (!A.mn_major) throw std::invalid_argument("gemm_conv_wgrad: A (Delta) must be MN-major");
+  const int N = 9 * g.c_in;
+  CUtensorMap b[2] = {im2col_map(src.hi, src, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B),
+                      im2col_map(src.lo, src, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)};
+  const ConvTmaArgs ic{g.out_h * g.out_w, g.out_w, g.stride, g.c_in, pixel0};
+  Operand B{nullptr, nullptr, 4, N, A.k, true};  // shape only
+  const Plan plan = plan_gemm(A.mn, N, A.k, ep.splitk_ws ? ep.splitk_ws_floats : 0, ep.splitk_ws != nullptr);
+  if (plan.splits > 1) {
+    const long ldw = round_up(N, 4), stride = static_cast<long>(A.mn) * ldw;
+    GemmEpilogue part{};
+    part.out_hi = ep.splitk_ws;
+    part.ld_out = ldw;
+    part.alpha = 1.0f;
+    part.M = A.mn;
+    part.N = N;
+    part.split_stride = stride;
+    launch_inst<128, true, true, kEpiStoreScaled, false, 2>(A, B, part, s, plan.splits, nullptr, b, ic);
+    const long n = static_cast<long>(A.mn) * N;
+    const int grid = static_cast<int>(std::min<long>((n + 255) / 256, 148L * 16));
+    splitk_fixup_kernel<kEpiStoreScaled><<<grid, 256, 0, s>>>(ep.splitk_ws, plan.splits, stride, ldw, ep);
+    SPB_CUDA(cudaGetLastError());
+    return 2;
+  }
+  launch_inst<128, true, true, kEpiStoreScaled, false, 2>(A, B, ep, s, 1, nullptr, b, ic);
+  return 1;
+}
 
 void gemm_reserve_sms(int n) { g_reserved_sms = n < 0 ? 0 : n; }
 

@@ -288,13 +288,36 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
 // is then bounded independently of K.
 constexpr int kChunkKb = 4;  // 128 of K per TMEM chunk
 
-template <int BN, bool A_MN, bool B_MN, int EPI, bool TMA_UPD = false>
+// Implicit-GEMM convolution operands (3x3, padding 1, NHWC, c_in % 32 == 0):
+// the tensor maps are TMA im2col maps of the activation tensor and the tile
+// loads compute window origins and filter-tap offsets instead of reading a
+// materialised column matrix.
+//   IC == 1: A = columns of the output-pixel rows [m0, m0 + 128) (forward:
+//            K-major, K = tap * c_in + ci), one 128-pixel box per k-block.
+//   IC == 2: B = columns of the pixel rows k_base + [kb*32, kb*32 + 32)
+//            (wgrad: MN-major, N = tap * c_in + ci), one 32 x 32 box per
+//            32-column chunk.
+struct ConvTmaArgs {
+  int opix, out_w, stride, c_in;
+  long k_base;
+};
+
+__device__ __forceinline__ void conv_origin(const ConvTmaArgs& ic, long pixel, int& w, int& h, int& n) {
+  n = static_cast<int>(pixel / ic.opix);
+  const int rem = static_cast<int>(pixel - static_cast<long>(n) * ic.opix);
+  const int p = rem / ic.out_w, q = rem - p * ic.out_w;
+  w = q * ic.stride - 1;
+  h = p * ic.stride - 1;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI, bool TMA_UPD = false, int IC = 0>
 __global__ void __launch_bounds__(256, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                        const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                        int num_kb, int num_m_tiles, int num_tiles, int kb_per_split, int num_units,
                        const __grid_constant__ GemmEpilogue ep, const __grid_constant__ CUtensorMap tw_hi,
-                       const __grid_constant__ CUtensorMap tw_lo, const __grid_constant__ CUtensorMap tw_mom) {
+                       const __grid_constant__ CUtensorMap tw_lo, const __grid_constant__ CUtensorMap tw_mom,
+                       const ConvTmaArgs ic) {
   using Cfg = GemmCfg<BN, TMA_UPD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -354,10 +377,32 @@ __global__ void __launch_bounds__(256, 1)
           mbar_wait(&empty_bar[s], ph ^ 1u);
           mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
           uint8_t* base = smem + s * Cfg::kStageBytes;
-          load_operand<A_MN, kBM>(base, &ta_hi, &full_bar[s], m0, kb * kBK);
-          load_operand<A_MN, kBM>(base + Cfg::kABytes, &ta_lo, &full_bar[s], m0, kb * kBK);
-          load_operand<B_MN, BN>(base + 2 * Cfg::kABytes, &tb_hi, &full_bar[s], n0, kb * kBK);
-          load_operand<B_MN, BN>(base + 2 * Cfg::kABytes + Cfg::kBBytes, &tb_lo, &full_bar[s], n0, kb * kBK);
+          if constexpr (IC == 1) {
+            const int k = kb * kBK, tap = k / ic.c_in, c = k - tap * ic.c_in;
+            int w, h, n;
+            conv_origin(ic, m0, w, h, n);
+            const uint16_t ox = static_cast<uint16_t>(tap % 3), oy = static_cast<uint16_t>(tap / 3);
+            tma_load_im2col_4d(base, &ta_hi, &full_bar[s], c, w, h, n, ox, oy);
+            tma_load_im2col_4d(base + Cfg::kABytes, &ta_lo, &full_bar[s], c, w, h, n, ox, oy);
+          } else {
+            load_operand<A_MN, kBM>(base, &ta_hi, &full_bar[s], m0, kb * kBK);
+            load_operand<A_MN, kBM>(base + Cfg::kABytes, &ta_lo, &full_bar[s], m0, kb * kBK);
+          }
+          if constexpr (IC == 2) {
+            int w, h, n;
+            conv_origin(ic, ic.k_base + kb * kBK, w, h, n);
+#pragma unroll
+            for (int cc = 0; cc < BN / 32; ++cc) {
+              const int col = n0 + cc * 32, tap = col / ic.c_in, c = col - tap * ic.c_in;
+              const uint16_t ox = static_cast<uint16_t>(tap % 3), oy = static_cast<uint16_t>(tap / 3);
+              tma_load_im2col_4d(base + 2 * Cfg::kABytes + cc * 4096, &tb_hi, &full_bar[s], c, w, h, n, ox, oy);
+              tma_load_im2col_4d(base + 2 * Cfg::kABytes + Cfg::kBBytes + cc * 4096, &tb_lo, &full_bar[s], c, w, h, n,
+                                 ox, oy);
+            }
+          } else {
+            load_operand<B_MN, BN>(base + 2 * Cfg::kABytes, &tb_hi, &full_bar[s], n0, kb * kBK);
+            load_operand<B_MN, BN>(base + 2 * Cfg::kABytes + Cfg::kBBytes, &tb_lo, &full_bar[s], n0, kb * kBK);
+          }
         }
       }
     }

@@ -39,6 +39,21 @@ struct GemmEpilogue;  // gemm_tf32x3.cuh
 // D = epi(A * B^T) over M = A.mn, N = B.mn, K = A.k. Returns kernels launched.
 // Picks the 1-CTA 128x128 or the CTA-pair 256x256 kernel by wave-quantised cost.
 int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue& ep, cudaStream_t s);
+// Implicit-GEMM 3x3 convolutions straight from the NHWC split pair through
+// TMA im2col maps (c_in and ld multiples of 32; conv.hpp ConvGeom).
+struct ConvGeom;
+struct ConvSrc {
+  const float* hi;
+  const float* lo;
+  long ld;      // floats per pixel row
+  int samples;  // images in the tensor
+  const ConvGeom& g;
+};
+// Forward: out = tanh(im2col(src) W^T + b) (kEpiFwdTanh epilogue `ep`).
+int gemm_conv_fwd(const ConvSrc& src, const Operand& B, const GemmEpilogue& ep, cudaStream_t s);
+// wgrad: D[c_out x 9 c_in] = A^T im2col(src) over pixel rows [pixel0, pixel0 + A.k)
+// (A = Delta, MN-major; kEpiStoreScaled epilogue, split-K when ep has a workspace).
+int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const GemmEpilogue& ep, cudaStream_t s);
 // Test hook: -1 automatic choice, 0 force 1-CTA, 1 force CTA pair.
 void gemm_force_variant(int v);
 // Persistent GEMM grids leave n SMs free (for NCCL kernels running beside them).

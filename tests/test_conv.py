@@ -16,6 +16,16 @@ SHAPE, CONVS, NOUT = (8, 8, 3), [(8, 1), (12, 2), (16, 1), (16, 2)], 3
 N, K, BW, LR, SEED, DSEED = 64, 4, 4, 0.05, 5, 9
 
 
+# "tall": 16 x 16 images, so the layer-1 wgrad GEMM has K = 16 samples x 256
+# pixel rows = 4096 against a single 8 x 36 output tile -> the split-K path.
+# "tma": 32 / 64-channel inputs -> implicit GEMM through TMA im2col maps
+# (forward A operand and wgrad B operand), strides 1 and 2; "tma_tall": the
+# im2col-B wgrad with K = 4096 pixel rows -> split-K.
+CASES = {"small": (SHAPE, CONVS, NOUT), "tall": ((16, 16, 4), [(8, 1), (8, 2), (12, 1)], 2),
+         "tma": ((8, 8, 3), [(32, 1), (32, 2), (64, 1), (32, 2)], 3),
+         "tma_tall": ((16, 16, 3), [(32, 1), (32, 1), (64, 2)], 2)}
+
+
 def _data():
     from paper_2111_10672_b200 import spb
 
@@ -78,13 +88,15 @@ def _rel(a, b):
 
 
 @pytest.mark.gpu
-def test_conv_loss_and_partial_backprop_match_oracle():
+@pytest.mark.parametrize("case", ["small", "tma"])
+def test_conv_loss_and_partial_backprop_match_oracle(case):
     from paper_2111_10672_b200 import spb
 
-    X, Y, W = _data()
-    o = ConvOracle(SHAPE, CONVS, NOUT)
+    shape, convs, nout = CASES[case]
+    X, Y, W = spb.gen_convnet(shape, convs, nout, N, DSEED)
+    o = ConvOracle(shape, convs, nout)
     B = [w.astype(np.float64) for w in W]
-    m = spb.ConvNet(SHAPE, CONVS, NOUT, X, Y, W, k=K, per_worker_batch=BW)
+    m = spb.ConvNet(shape, convs, nout, X, Y, W, k=K, per_worker_batch=BW)
     try:
         assert m.loss() == pytest.approx(o.loss(B, X, Y), rel=1e-5)
         batch = np.array([3, 17, 5, 60, 41, 8, 8, 22], dtype=np.int32)
@@ -100,13 +112,8 @@ def test_conv_loss_and_partial_backprop_match_oracle():
         m.close()
 
 
-# "tall": 16 x 16 images, so the layer-1 wgrad GEMM has K = 16 samples x 256
-# pixel rows = 4096 against a single 8 x 36 output tile -> the split-K path.
-CASES = {"small": (SHAPE, CONVS, NOUT), "tall": ((16, 16, 4), [(8, 1), (8, 2), (12, 1)], 2)}
-
-
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["small", "tall"])
+@pytest.mark.parametrize("case", ["small", "tall", "tma", "tma_tall"])
 @pytest.mark.parametrize("full", [False, True])
 def test_conv_spb_steps_match_oracle(orc, full, case):
     from paper_2111_10672_b200 import spb
