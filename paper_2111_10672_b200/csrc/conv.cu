@@ -152,6 +152,23 @@ __global__ void __launch_bounds__(256) col2im_tanh_kernel(const float* __restric
   }
 }
 
+// Wf[ci, (ky*3 + kx) * c_out + co] = W[co, ((2-ky)*3 + (2-kx)) * c_in + ci]
+// for both halves of the split pair (a permutation: exact).
+__global__ void conv_flip_kernel(const float* __restrict__ w_hi, const float* __restrict__ w_lo, long ldw, int c_out,
+                                 int c_in, float* __restrict__ f_hi, float* __restrict__ f_lo, long ldf) {
+  const long total = static_cast<long>(c_in) * 9 * c_out;
+  for (long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int co = static_cast<int>(t % c_out);
+    const long r = t / c_out;
+    const int tap = static_cast<int>(r % 9), ci = static_cast<int>(r / 9);
+    const long src = static_cast<long>(co) * ldw + (8 - tap) * c_in + ci;
+    const long dst = static_cast<long>(ci) * ldf + tap * c_out + co;
+    f_hi[dst] = w_hi[src];
+    f_lo[dst] = w_lo[src];
+  }
+}
+
 int flat_grid(long total) { return static_cast<int>(std::max<long>(1, std::min<long>((total + 255) / 256, 148L * 16))); }
 
 // pooled[s, c] = mean over the pix pixel rows of sample s (split pair out).
@@ -224,6 +241,13 @@ void launch_col2im_tanh(const float* dcol, long ldk, const ConvGeom& g, int row0
   else
     col2im_tanh_kernel<1><<<flat_grid(static_cast<long>(rows) * g.c_in), 256, 0, s>>>(dcol, ldk, g, row0, rows, h_hi,
                                                                                     h_lo, ldh, d_hi, d_lo, ldd);
+  SPB_CUDA(cudaGetLastError());
+}
+
+void launch_conv_flip(const float* w_hi, const float* w_lo, long ldw, int c_out, int c_in, float* f_hi, float* f_lo,
+                      long ldf, cudaStream_t s) {
+  const long total = static_cast<long>(c_in) * 9 * c_out;
+  conv_flip_kernel<<<flat_grid(total), 256, 0, s>>>(w_hi, w_lo, ldw, c_out, c_in, f_hi, f_lo, ldf);
   SPB_CUDA(cudaGetLastError());
 }
 

@@ -23,6 +23,9 @@ void launch_im2col(const float* in_hi, const float* in_lo, long ldin, const Conv
 // Delta of the layer below for input pixel rows [row0, row0 + rows).
 void launch_col2im_tanh(const float* dcol, long ldk, const ConvGeom& g, int row0, int rows, const float* h_hi,
                         const float* h_lo, long ldh, float* d_hi, float* d_lo, long ldd, cudaStream_t s);
+// Spatially flipped, channel-transposed kernel for the stride-1 implicit dgrad.
+void launch_conv_flip(const float* w_hi, const float* w_lo, long ldw, int c_out, int c_in, float* f_hi, float* f_lo,
+                      long ldf, cudaStream_t s);
 void launch_avgpool(const float* h_hi, const float* h_lo, long ldh, int samples, int pix, int c, float* p_hi,
                     float* p_lo, long ldp, cudaStream_t s);
 // Pixel rows of samples [s0, samples).

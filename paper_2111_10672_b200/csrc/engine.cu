@@ -131,6 +131,7 @@ struct Engine {
   std::vector<float*> Ch, Cl;  // im2col split pairs, [samples * pix[l] x ldf[l]], kept for wgrad
   float *Ph = nullptr, *Pl = nullptr, *Gh = nullptr, *Gl = nullptr;  // pooled features / their gradient
   float* dcol = nullptr;  // dgrad columns (fp32), reused per layer
+  float *Fh = nullptr, *Fl = nullptr;  // flipped kernel of the current implicit dgrad
   int* iota_dev = nullptr;
   long ldx = 0;  // dataset row stride
   long nflat = 0, ldd = 0;
@@ -287,7 +288,7 @@ struct Engine {
     for (auto p : Hl) f(p);
     for (auto p : Ch) f(p);
     for (auto p : Cl) f(p);
-    f(Ph), f(Pl), f(Gh), f(Gl), f(dcol), f(iota_dev);
+    f(Ph), f(Pl), f(Gh), f(Gl), f(dcol), f(iota_dev), f(Fh), f(Fl);
     for (int i = 0; i < kDbuf; ++i) f(Dh[i]), f(Dl[i]);
     if (st) cudaStreamDestroy(st);
     st = nullptr;
@@ -489,6 +490,9 @@ struct Engine {
     }
     for (int i = 0; i < kDbuf; ++i) Dh[i] = alloc<float>(dmax), Dl[i] = alloc<float>(dmax);
     dcol = alloc<float>(cmax);
+    long fmax = 1;
+    for (int l = 2; l < L; ++l) fmax = std::max(fmax, static_cast<long>(w[l - 1]) * round_up(9L * w[l], 4));
+    if (!Fh) Fh = alloc<float>(fmax), Fl = alloc<float>(fmax);
     Ph = alloc<float>(S * ld[L - 1]);
     Pl = alloc<float>(S * ld[L - 1]);
     Gh = alloc<float>(S * ld[L - 1]);
@@ -510,6 +514,13 @@ struct Engine {
 
   // Convolution l runs as an implicit GEMM (TMA im2col, no column matrix)
   // when its input channels fill whole 128-byte TMA boxes.
+  // dgrad of convolution l as an implicit GEMM over Delta_l (stride 1, its
+  // output channels filling whole TMA boxes).
+  bool conv_tma_dgrad(int l) const {
+    static const bool off = std::getenv("SPB_CONV_IM2COL") != nullptr;
+    return !off && cg[l].stride == 1 && w[l] % 32 == 0 && ld[l] % 32 == 0;
+  }
+
   bool conv_tma(int l) const {
     static const bool off = std::getenv("SPB_CONV_IM2COL") != nullptr;  // A/B experiments: materialise columns
     return !off && cg[l].c_in % 32 == 0 && ld[l - 1] % 32 == 0;
@@ -597,7 +608,27 @@ struct Engine {
       if (row0[l] >= samples) break;
       const int b = l % kDbuf, bn = (l - 1) % kDbuf;
       const long r0 = row0[l] * pix[l], cnt = (samples - row0[l]) * pix[l];
-      if (l > 1 && row0[l - 1] < samples) {  // dgrad into columns, then col2im * (1 - H^2)
+      if (l > 1 && row0[l - 1] < samples && conv_tma_dgrad(l)) {
+        // Delta_{l-1} = conv(Delta_l, flipped W_l) * (1 - H_{l-1}^2), rows of the continuing samples.
+        const long q0 = row0[l - 1] * pix[l - 1], qn = (samples - row0[l - 1]) * pix[l - 1];
+        const long ldfl = round_up(9L * w[l], 4);
+        pbeg(s);
+        launch_conv_flip(p_hi + w_off[l], p_lo + w_off[l], ldf[l], w[l], w[l - 1], Fh, Fl, ldfl, s);
+        ConvGeom gd{cg[l].out_h, cg[l].out_w, w[l], cg[l].in_h, cg[l].in_w, w[l - 1], 1};
+        ConvSrc src{Dh[b], Dl[b], ld[l], samples, gd};
+        Operand B{Fh, Fl, ldfl, w[l - 1], 9 * w[l], false};
+        GemmEpilogue ep{};
+        ep.out_hi = Dh[bn] + q0 * ld[l - 1];
+        ep.out_lo = Dl[bn] + q0 * ld[l - 1];
+        ep.ld_out = ld[l - 1];
+        ep.h_hi = Hh[l - 1] + q0 * ld[l - 1];
+        ep.h_lo = Hl[l - 1] + q0 * ld[l - 1];
+        ep.ld_h = ld[l - 1];
+        ep.M = static_cast<int>(qn);
+        ep.N = w[l - 1];
+        n += 1 + gemm_conv_dgrad(src, q0, static_cast<int>(qn), B, ep, s);
+        pend(kClsDgrad, 2.0 * qn * w[l] * fan[l], s);
+      } else if (l > 1 && row0[l - 1] < samples) {  // dgrad into columns, then col2im * (1 - H^2)
         const long q0 = row0[l - 1] * pix[l], qn = (samples - row0[l - 1]) * pix[l];
         Operand A{Dh[b] + q0 * ld[l], Dl[b] + q0 * ld[l], ld[l], static_cast<int>(qn), w[l], false};
         Operand B{p_hi + w_off[l], p_lo + w_off[l], ldf[l], fan[l], w[l], true};

@@ -266,12 +266,29 @@ int gemm_conv_fwd(const ConvSrc& src, const Operand& B, const GemmEpilogue& ep, 
   if (B.k != K || B.mn_major) throw std::invalid_argument("gemm_conv_fwd: B must be K-major [c_out x 9 c_in]");
   CUtensorMap a[2] = {im2col_map(src.hi, src, kBM, CU_TENSOR_MAP_SWIZZLE_128B),
                       im2col_map(src.lo, src, kBM, CU_TENSOR_MAP_SWIZZLE_128B)};
-  const ConvTmaArgs ic{g.out_h * g.out_w, g.out_w, g.stride, g.c_in, 0};
+  const ConvTmaArgs ic{g.out_h * g.out_w, g.out_w, g.stride, g.c_in, 0, 0};
   Operand A{nullptr, nullptr, 4, M, K, false};  // shape only: tiles come from the im2col maps
   if (B.mn <= 64)
     launch_inst<64, false, false, kEpiFwdTanh, false, 1>(A, B, ep, s, 1, a, nullptr, ic);
   else
     launch_inst<128, false, false, kEpiFwdTanh, false, 1>(A, B, ep, s, 1, a, nullptr, ic);
+  return 1;
+}
+
+int gemm_conv_dgrad(const ConvSrc& src, long pixel0, int rows, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
+  const ConvGeom& g = src.g;
+  if (g.c_in % 32 || src.ld % 32 || g.stride != 1)
+    throw std::invalid_argument("gemm_conv_dgrad: stride 1, c_in and ld multiples of 32");
+  const int K = 9 * g.c_in;
+  if (B.k != K || B.mn_major) throw std::invalid_argument("gemm_conv_dgrad: B must be K-major [c_out x 9 c_in]");
+  CUtensorMap a[2] = {im2col_map(src.hi, src, kBM, CU_TENSOR_MAP_SWIZZLE_128B),
+                      im2col_map(src.lo, src, kBM, CU_TENSOR_MAP_SWIZZLE_128B)};
+  const ConvTmaArgs ic{g.out_h * g.out_w, g.out_w, 1, g.c_in, 0, pixel0};
+  Operand A{nullptr, nullptr, 4, rows, K, false};
+  if (B.mn <= 64)
+    launch_inst<64, false, false, kEpiDgradTanh, false, 1>(A, B, ep, s, 1, a, nullptr, ic);
+  else
+    launch_inst<128, false, false, kEpiDgradTanh, false, 1>(A, B, ep, s, 1, a, nullptr, ic);
   return 1;
 }
 
@@ -282,7 +299,7 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
   const int N = 9 * g.c_in;
   CUtensorMap b[2] = {im2col_map(src.hi, src, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B),
                       im2col_map(src.lo, src, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)};
-  const ConvTmaArgs ic{g.out_h * g.out_w, g.out_w, g.stride, g.c_in, pixel0};
+  const ConvTmaArgs ic{g.out_h * g.out_w, g.out_w, g.stride, g.c_in, pixel0, 0};
   Operand B{nullptr, nullptr, 4, N, A.k, true};  // shape only
   const Plan plan = plan_gemm(A.mn, N, A.k, ep.splitk_ws ? ep.splitk_ws_floats : 0, ep.splitk_ws != nullptr);
   if (plan.splits > 1) {

@@ -299,7 +299,8 @@ constexpr int kChunkKb = 4;  // 128 of K per TMEM chunk
 //            32-column chunk.
 struct ConvTmaArgs {
   int opix, out_w, stride, c_in;
-  long k_base;
+  long k_base;  // IC == 2: first pixel row of K
+  long m_base;  // IC == 1: first pixel row of M
 };
 
 __device__ __forceinline__ void conv_origin(const ConvTmaArgs& ic, long pixel, int& w, int& h, int& n) {
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(256, 1)
           if constexpr (IC == 1) {
             const int k = kb * kBK, tap = k / ic.c_in, c = k - tap * ic.c_in;
             int w, h, n;
-            conv_origin(ic, m0, w, h, n);
+            conv_origin(ic, ic.m_base + m0, w, h, n);
             const uint16_t ox = static_cast<uint16_t>(tap % 3), oy = static_cast<uint16_t>(tap / 3);
             tma_load_im2col_4d(base, &ta_hi, &full_bar[s], c, w, h, n, ox, oy);
             tma_load_im2col_4d(base + Cfg::kABytes, &ta_lo, &full_bar[s], c, w, h, n, ox, oy);

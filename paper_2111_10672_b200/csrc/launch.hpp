@@ -54,6 +54,11 @@ int gemm_conv_fwd(const ConvSrc& src, const Operand& B, const GemmEpilogue& ep, 
 // wgrad: D[c_out x 9 c_in] = A^T im2col(src) over pixel rows [pixel0, pixel0 + A.k)
 // (A = Delta, MN-major; kEpiStoreScaled epilogue, split-K when ep has a workspace).
 int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const GemmEpilogue& ep, cudaStream_t s);
+// dgrad of a stride-1 convolution as a convolution of Delta: out rows
+// [pixel0, pixel0 + rows) of the layer below = (im2col(Delta) Wf^T) * (1 - H^2)
+// (kEpiDgradTanh), Wf = the spatially flipped, channel-transposed kernel
+// [c_below x 9 c_out] (launch_conv_flip). src.g describes Delta as input.
+int gemm_conv_dgrad(const ConvSrc& src, long pixel0, int rows, const Operand& B, const GemmEpilogue& ep, cudaStream_t s);
 // Test hook: -1 automatic choice, 0 force 1-CTA, 1 force CTA pair.
 void gemm_force_variant(int v);
 // Persistent GEMM grids leave n SMs free (for NCCL kernels running beside them).
