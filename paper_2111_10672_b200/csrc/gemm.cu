@@ -211,8 +211,10 @@ int g_force_variant = -1;  // -1 auto, 0 = 1-CTA 128x128, 1 = CTA pair 256x256
 // Launch plan: the 1-CTA kernel with `splits` K-splits, or the CTA-pair
 // kernel. Wave-quantised cost model (microseconds) calibrated on B200 with
 // tests/native/gemm_bench.cu: a 1-CTA 128x128 work unit costs
-// 0.62 us per k-block + 2.8 us; a 256x256 pair tile 1.0 us per k-block +
-// 5.6 us on 2 SMs; a split-K fixup streams (splits + 2) M x N floats.
+// 0.62 us per k-block + 2.8 us; a 256x256 pair tile 1.07 us per k-block +
+// 7 us on 2 SMs (recalibrated: the pair loses the SPB wgrad shapes with
+// K <= 512 to the 1-CTA kernel by 8-19 %); a split-K fixup streams
+// (splits + 2) M x N floats.
 struct Plan {
   bool two_sm;
   int splits;
@@ -242,7 +244,7 @@ Plan plan_gemm(int M, int N, int K, long ws_floats, bool can_split) {
   const int pn = pair_n_for(M, N);
   const long t2n = static_cast<long>((M + 255) / 256) * ((N + pn - 1) / pn);
   (void)t2;
-  const double t_two = static_cast<double>((t2n + sms / 2 - 1) / (sms / 2)) * (1.0 * kb + 5.6) * pn / 256.0;
+  const double t_two = static_cast<double>((t2n + sms / 2 - 1) / (sms / 2)) * (1.07 * kb + 7.0) * pn / 256.0;
   if (t_two < best_t) best = {true, 1};
   return best;
 }

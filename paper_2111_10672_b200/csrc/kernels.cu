@@ -190,7 +190,7 @@ __global__ void colreduce_partial_kernel(const float* __restrict__ hi, const flo
   for (int o = 0; o < nvec; ++o) partial[(static_cast<long>(split) * nvec + o) * ncols + c] = acc[o];
 }
 
-// Pass 2: g = alpha * sum over splits, in split order; either stored to
+// Pass 2: g = alpha * sum over splits (warp per output, fixed order); either stored to
 // out, or (upd != nullptr) applied as the optimizer step to the split pair
 // out/out_lo in place (single-GPU fused update of biases and the head).
 struct UpdArgs {
@@ -200,11 +200,18 @@ struct UpdArgs {
 };
 __global__ void colreduce_final_kernel(const float* __restrict__ partial, int nsplit, int nvec, int ncols, float alpha,
                                        float* __restrict__ out, long ld_out, UpdArgs upd, int update) {
-  const long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // One warp per output (o, c): lane i sums splits i, i + 32, ... in order,
+  // then a fixed xor-shuffle tree -- deterministic, and parallel even when a
+  // tall input (conv pixel rows) leaves ~1000 partials per column.
+  const long t = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (t >= static_cast<long>(nvec) * ncols) return;
   const int o = static_cast<int>(t / ncols), c = static_cast<int>(t % ncols);
   float s = 0.f;
-  for (int sp = 0; sp < nsplit; ++sp) s += partial[(static_cast<long>(sp) * nvec + o) * ncols + c];
+  for (int sp = lane; sp < nsplit; sp += 32) s += partial[(static_cast<long>(sp) * nvec + o) * ncols + c];
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+  if (lane) return;
   const long at = o * ld_out + c;
   if (!update) {
     out[at] = alpha * s;
@@ -362,8 +369,8 @@ void launch_colreduce(const float* hi, const float* lo, long ld, int r0, int r1,
   const long tot = static_cast<long>(nvec) * ncols;
   UpdArgs u{nullptr, nullptr, 0.f, 0.f, 0.f};
   if (upd) u = UpdArgs{upd->lo, upd->mom, upd->lr, upd->mu, upd->wd};
-  colreduce_final_kernel<<<static_cast<int>((tot + 255) / 256), 256, 0, s>>>(scratch, nsplit, nvec, ncols, alpha, out,
-                                                                             ld_out, u, upd ? 1 : 0);
+  colreduce_final_kernel<<<static_cast<int>((tot * 32 + 255) / 256), 256, 0, s>>>(scratch, nsplit, nvec, ncols, alpha,
+                                                                                  out, ld_out, u, upd ? 1 : 0);
   SPB_CUDA(cudaGetLastError());
 }
 

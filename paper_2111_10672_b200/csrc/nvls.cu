@@ -244,6 +244,7 @@ McBuffer nvls_alloc(size_t bytes, int device, int rank, int nranks, const std::s
   barrier();
   b.device = cudev;
   SPB_CUDA(cudaMemset(reinterpret_cast<void*>(b.uc), 0, b.size));
+  SPB_CUDA(cudaDeviceSynchronize());  // the zeroing (legacy stream) before any use on other streams
   barrier();
   return b;
 }

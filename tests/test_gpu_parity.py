@@ -335,3 +335,32 @@ def test_deep_wide_step_properties():
     ls = m.train_steps(11, 3, 20, losses=True)
     assert np.isfinite(ls).all()
     assert ls[-5:].mean() < l0
+
+
+def test_aggregate_repeated_calls_are_exact():
+    """Regression: spb_aggregate's staging buffer was zeroed on the legacy
+    default stream, unordered with the copies on the context's stream, and
+    lost a worker's block about once in 15 calls. 40 calls on random blocks
+    must all equal the host mean over contributors (spb.cpp:97-103)."""
+    widths = [96, 80, 64, 1]
+    k = 4
+    X, Y, W = spb.gen_chain_mlp(widths, 64, 3)
+    m = spb.ChainMlp(widths, X, Y, W, k=k, per_worker_batch=4)
+    L = len(widths) - 1
+    rng = np.random.default_rng(0)
+    dims = spb.block_dims(widths)
+    try:
+        for _ in range(40):
+            pgs = []
+            for j in range(1, k + 1):
+                s = spb.suffix_layers(j, k, L)
+                blocks = [rng.standard_normal(d).astype(np.float32) if l >= L - s else np.zeros(0, np.float32)
+                          for l, d in enumerate(dims)]
+                pgs.append(spb.PartialGradient(blocks, L - s + 1))
+            got = spb.aggregate(pgs, k)
+            for l in range(L):
+                contrib = [pg.blocks[l] for pg in pgs if pg.blocks[l].size]
+                want = np.sum(np.stack(contrib).astype(np.float64), axis=0) / len(contrib)
+                assert np.allclose(got[l], want, rtol=1e-6, atol=1e-7)
+    finally:
+        m.close()
