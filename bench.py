@@ -269,20 +269,8 @@ CFG4 = dict(workload="cfg4: ConvNet 32x32x3 (CIFAR10 shape), 3x3 convs at ResNet
             nout=10, k=8, bw=128, N=8192, data_seed=7, step_seed=11, lr=0.01, momentum=0.9, weight_decay=1e-4)
 
 
-def run_cfg4(world, rank, local, dist, K, W_):
-    """BASELINE configs[3] on the same engine: SPB vs full backprop samples/s
-    (CUDA events on the step stream, max over ranks) and the eager per-class
-    breakdown. Reported beside the cfg3 headline, not as it."""
-    from paper_2111_10672_b200 import spb
-
-    c = CFG4
-    X, Y, W = spb.gen_convnet(c["shape"], c["convs"], c["nout"], c["N"], c["data_seed"])
-    m = spb.ConvNet(c["shape"], c["convs"], c["nout"], X, Y, W, k=c["k"], per_worker_batch=c["bw"], device=local)
-    if world > 1:
-        m.comm_init_torch(dist, rank, world)
-    m.set_optimizer(c["lr"], c["momentum"], c["weight_decay"])
-    out = {"workload": c["workload"], "params": int(sum(spb.convnet_block_dims(c["shape"], c["convs"], c["nout"]))),
-           "data": "synthetic (numpy uniform images/targets, seed 7)", "lowering": "im2col + tcgen05 3xTF32 GEMMs"}
+def _measure_sub(m, c, out, world, dist, K, W_):
+    """SPB vs full backprop on one model: CUDA events on the step stream, max over ranks."""
     for full in (False, True):
         m.set_params(m.initial_params())
         m.train_steps(c["step_seed"], 1, W_, full_backprop=full)
@@ -300,6 +288,46 @@ def run_cfg4(world, rank, local, dist, K, W_):
             "gemm_alg_tflops": round(gemm_fl / max(gemm_ms, 1e-9) / 1e9, 1),
             "phase_ms": {q: round(prof[q]["ms"], 3) for q in prof if prof[q]["launches"]}}
     out["spb_speedup"] = round(out["spb"]["value"] / out["full_backprop"]["value"], 4)
+    return out
+
+
+def run_cfg4(world, rank, local, dist, K, W_):
+    """BASELINE configs[3] on the same engine: SPB vs full backprop samples/s
+    and the eager per-class breakdown. Reported beside the cfg3 headline."""
+    from paper_2111_10672_b200 import spb
+
+    c = CFG4
+    X, Y, W = spb.gen_convnet(c["shape"], c["convs"], c["nout"], c["N"], c["data_seed"])
+    m = spb.ConvNet(c["shape"], c["convs"], c["nout"], X, Y, W, k=c["k"], per_worker_batch=c["bw"], device=local)
+    if world > 1:
+        m.comm_init_torch(dist, rank, world)
+    m.set_optimizer(c["lr"], c["momentum"], c["weight_decay"])
+    out = {"workload": c["workload"], "params": int(sum(spb.convnet_block_dims(c["shape"], c["convs"], c["nout"]))),
+           "data": "synthetic (numpy uniform images/targets, seed 7)",
+           "lowering": "implicit GEMM via TMA im2col (c_in % 32 == 0), im2col for the RGB layer; tcgen05 3xTF32"}
+    _measure_sub(m, c, out, world, dist, K, W_)
+    barrier(dist)
+    m.close()
+    return out
+
+
+def run_cfg2(world, rank, local, dist, K, W_):
+    """BASELINE configs[1] (the reference's MLP, 4 workers) on the same engine.
+    At 1 GPU the 4 workers are time-sliced rows of one step; with more ranks
+    than workers it is skipped (spb_comm_init needs ranks <= k)."""
+    from paper_2111_10672_b200 import spb
+
+    c = CFG2
+    if world > c["k"]:
+        return {"workload": c["workload"], "skipped": f"{world} ranks > k = {c['k']} workers"}
+    X, Y, W = spb.gen_chain_mlp(c["widths"], c["N"], c["data_seed"])
+    m = spb.ChainMlp(c["widths"], X, Y, W, k=c["k"], per_worker_batch=c["bw"], device=local)
+    if world > 1:
+        m.comm_init_torch(dist, rank, world)
+    m.set_optimizer(c["lr"], c["momentum"], c["weight_decay"])
+    out = {"workload": c["workload"], "data": "synthetic (reference generator make_random_chain_mlp, seed 7)",
+           "reference_cpu_samples_per_s_1core": "834 SPB / 636 full (BASELINE.md section 2, survey container)"}
+    _measure_sub(m, c, out, world, dist, K, W_)
     barrier(dist)
     m.close()
     return out
@@ -412,6 +440,10 @@ def run_b200(args, world, rank, local, dist):
             line["cfg4_convnet"] = run_cfg4(world, rank, local, dist, min(K, 10), W_)
         except Exception as ex:  # noqa: BLE001
             line["cfg4_convnet"] = {"error": repr(ex)}
+    try:
+        line["cfg2_mlp"] = run_cfg2(world, rank, local, dist, K, W_)
+    except Exception as ex:  # noqa: BLE001
+        line["cfg2_mlp"] = {"error": repr(ex)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, kind, cores, sample = cpu_reference(cfg, 1, 0, REF_BW)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
