@@ -174,12 +174,15 @@ SPB_API void* spb_stream(spb_ctx* ctx);
  *    epoch-stamped device flags (no NCCL in the step);
  *  - "nvls": parameters and gradients in NVSwitch multicast memory; each rank
  *    reduces its shard in the switch, updates it and multicasts the weights;
+ *  - "rs": NCCL reduce-scatter of each layer's gradient, the optimizer on
+ *    this rank's shard, NCCL all-gather of the fp32 weights (a layer with one
+ *    contributing rank: that rank updates it and broadcasts the weights);
  *  - "nccl" (default for more than 2 ranks): per-layer NCCL buckets
  *    (broadcast / all-reduce), then the local optimizer update on every rank.
  * Ranks of one node only. */
 SPB_API spb_status spb_comm_unique_id(void* out128);
 SPB_API spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int nranks);
-/* Active aggregation mode: 0 nccl, 1 nvls, 2 p2p (-1 before spb_comm_init). */
+/* Active aggregation mode: 0 nccl, 1 nvls, 2 p2p, 3 rs (-1 before spb_comm_init). */
 SPB_API spb_status spb_comm_mode(spb_ctx* ctx, int* mode);
 /* Collective diagnostic of the NVLS path: multicast reduce + broadcast of a
  * known pattern over all ranks; *mismatches = wrong elements seen here. */

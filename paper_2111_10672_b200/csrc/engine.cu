@@ -53,6 +53,7 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
   ncclResult_t (*CommFinalize)(ncclComm_t);
   ncclResult_t (*CommDestroy)(ncclComm_t);
   ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*);
@@ -81,6 +82,7 @@ const NcclApi& nccl() {
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
     api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
     api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+    api.ReduceScatter = reinterpret_cast<decltype(api.ReduceScatter)>(sym("ncclReduceScatter"));
     api.CommFinalize = reinterpret_cast<decltype(api.CommFinalize)>(sym("ncclCommFinalize"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
     api.CommGetAsyncError = reinterpret_cast<decltype(api.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
@@ -173,7 +175,8 @@ struct Engine {
   std::vector<cudaEvent_t> evs;    // fork/join events (reused)
   bool fused_update = false;       // single-GPU: optimizer inside the wgrad epilogue (opt-in)
   // Multi-GPU aggregation mode: 0 = NCCL buckets, 1 = NVLS multicast,
-  // 2 = peer-to-peer copy-engine pulls (p2p.cu; the default).
+  // 2 = peer-to-peer copy-engine pulls (p2p.cu), 3 = NCCL reduce-scatter +
+  // sharded update + all-gather of the fp32 weights ("rs").
   int comm_mode = 0;
   // p2p mode: fp32 weights (own shards published to the peers), epoch-stamped
   // flags [2 * (L + 1)][nranks], gradient staging [2][nranks - 1][shard], and
@@ -989,6 +992,73 @@ struct Engine {
     return n;
   }
 
+  // "rs" mode, layer l, on cst after the layer's gradient is final (gs) and
+  // dgrad_l (s) has read W_l:
+  //  - several contributing ranks: ncclReduceScatter of the gradient (zeros
+  //    from non-contributors) -> this rank's shard updated (p2p_update_kernel:
+  //    hi, lo, momentum, fp32 w32) -> ncclAllGather of w32 -> the other shards
+  //    split into (hi, lo) on s3;
+  //  - one contributing rank: it updates the whole layer, ncclBroadcast of
+  //    w32, the others split it.
+  // Per rank the optimizer streams 28 B / N + 12 B (N-1) / N per parameter
+  // instead of 28 B, for the same NCCL bytes as the all-reduce buckets.
+  int enqueue_rs_layer(int l, bool full, cudaStream_t gs, cudaStream_t s) {
+    const Bucket* bk = nullptr;
+    for (auto& b : buckets[full])
+      if (b.l_lo <= l && l <= b.l_hi) bk = &b;
+    if (!bk) throw ConfigError("comm: no bucket for layer");
+    const bool mine = std::find(bk->ranks.begin(), bk->ranks.end(), rank) != bk->ranks.end();
+    const long off = w_off[l], cnt = b_off[l] + round_up(w[l], 32) - w_off[l];
+    auto evl = [&](int k) { return ev(kEvP2pLayer + 32 * l + k); };
+    SPB_CUDA(cudaEventRecord(ev(kEvBucket + l), gs));
+    SPB_CUDA(cudaStreamWaitEvent(cst, ev(kEvBucket + l), 0));
+    SPB_CUDA(cudaEventRecord(evl(0), s));  // dgrad_l issued on s before this point
+    SPB_CUDA(cudaStreamWaitEvent(cst, evl(0), 0));
+    int n = 0;
+    long a = 0, b = cnt;  // the range this rank updates itself
+    pbeg(cst);
+    if (bk->kind == 1) {
+      if (rank == bk->root) {
+        PeerPtrs<const float> src{};
+        src.p[0] = grad + off;
+        launch_p2p_update(src, 1, p_hi + off, p_lo + off, mom ? mom + off : nullptr, w32 + off, cnt, lr, mu, wd, cst);
+        ++n;
+      } else {
+        a = b = 0;
+      }
+      nccl_check(nccl().Broadcast(w32 + off, w32 + off, cnt, ncclFloat32, bk->root, comm, cst));
+    } else {
+      if (cnt % nranks) throw ConfigError("rs: layer segment not divisible by the rank count");
+      const long sh = cnt / nranks;
+      a = sh * rank, b = a + sh;
+      if (!mine) SPB_CUDA(cudaMemsetAsync(grad + off, 0, cnt * sizeof(float), cst));
+      nccl_check(nccl().ReduceScatter(grad + off, stage, sh, ncclFloat32, ncclSum, comm, cst));
+      PeerPtrs<const float> src{};
+      src.p[0] = stage;
+      launch_p2p_update(src, 1, p_hi + off + a, p_lo + off + a, mom ? mom + off + a : nullptr, w32 + off + a, sh, lr, mu,
+                        wd, cst);
+      ++n;
+      nccl_check(nccl().AllGather(w32 + off + a, w32 + off, sh, ncclFloat32, comm, cst));
+    }
+    pend(kClsComm, static_cast<double>(cnt) * 4.0, cst);
+    SPB_CUDA(cudaEventRecord(evl(1), cst));
+    SPB_CUDA(cudaStreamWaitEvent(s3, evl(1), 0));
+    pbeg(s3);
+    launch_p2p_split(w32 + off, p_hi + off, p_lo + off, cnt, a, b, s3);
+    pend(kClsUpdate, static_cast<double>(cnt - (b - a)) * 12.0, s3);
+    return n + 1;
+  }
+
+  void setup_rs() {
+    w32 = alloc<float>(nflat);
+    long maxcnt = 0;
+    for (int l = 1; l <= L; ++l) maxcnt = std::max(maxcnt, b_off[l] + round_up(w[l], 32) - w_off[l]);
+    stage_shard = (maxcnt + nranks - 1) / nranks;
+    stage = alloc<float>(stage_shard);
+    comm_mode = 3;
+    invalidate_graphs();
+  }
+
   // Collective over the ranks (spb_comm_init): allocate the p2p buffers and
   // map every peer's grad / w32 / flags through CUDA IPC.
   void setup_p2p() {
@@ -1141,6 +1211,16 @@ struct Engine {
       SPB_CUDA(cudaEventRecord(ev(e), from));
       SPB_CUDA(cudaStreamWaitEvent(s, ev(e), 0));
     };
+    if (comm && comm_mode == 3) {
+      fork(cst, kEvStepFork);
+      fork(s3, kEvUpdFork);
+      n += enqueue_pass(rows, row0, alpha, s,
+                        [&](int l, cudaStream_t from) { return enqueue_rs_layer(l, full, from, s); }, false,
+                        &ctl->step, nullptr);
+      join(cst, kEvStepJoin);
+      join(s3, kEvUpdJoin);
+      return n;
+    }
     if (comm && comm_mode == 2) {
       // Per layer (top down): G signal on the gradient stream, gradient and
       // weight pulls on per-peer copy streams, shard update on s3, split on
@@ -1593,9 +1673,10 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     // pattern (~450 GB/s per GPU) no longer beats NCCL's rings.
     const char* cm = std::getenv("SPB_COMM");
     const std::string mode = cm ? cm : (nranks == 2 ? "p2p" : "nccl");
-    if (mode != "p2p" && mode != "nccl" && mode != "nvls")
-      throw spb::ArgumentError("comm: SPB_COMM must be p2p, nccl or nvls");
+    if (mode != "p2p" && mode != "nccl" && mode != "nvls" && mode != "rs")
+      throw spb::ArgumentError("comm: SPB_COMM must be p2p, nccl, rs or nvls");
     if (nranks > 1 && mode == "p2p") e.setup_p2p();
+    if (nranks > 1 && mode == "rs") e.setup_rs();
     if (nranks > 1 && mode == "nvls") {
       // Socket names derive from the unique id, shared by all ranks.
       uint64_t h = 1469598103934665603ull;

@@ -66,7 +66,7 @@ def _rank(rank, world, port, out_dir, full, mode="p2p", mu=0.0, wd=0.0):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["p2p", "nvls", "nccl"])
+@pytest.mark.parametrize("mode", ["p2p", "rs", "nvls", "nccl"])
 @pytest.mark.parametrize("full", [False, True])
 def test_multi_gpu_step_matches_oracle(tmp_path, orc, full, mode):
     world = min(_gpus(), 4)
@@ -110,14 +110,14 @@ def test_multi_gpu_momentum_sharded_matches_nccl(tmp_path):
     import torch.multiprocessing as mp
 
     res = {}
-    for mode in ("p2p", "nvls", "nccl"):
+    for mode in ("p2p", "rs", "nvls", "nccl"):
         d = tmp_path / mode
         d.mkdir()
         mp.start_processes(_rank_momentum, args=(world, _free_port(), str(d), mode), nprocs=world,
                            start_method="spawn")
         res[mode] = [np.load(d / f"r{r}.npz") for r in range(world)]
     L = len(WIDTHS) - 1
-    for mode in ("p2p", "nvls"):
+    for mode in ("p2p", "rs", "nvls"):
         for l in range(L):
             a, b = res[mode][0][f"arr_{l + 1}"], res["nccl"][0][f"arr_{l + 1}"]
             assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-5
@@ -189,7 +189,7 @@ def _rank_conv(rank, world, port, out_dir, mode):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["p2p", "nvls", "nccl"])
+@pytest.mark.parametrize("mode", ["p2p", "rs", "nvls", "nccl"])
 def test_multi_gpu_convnet_matches_oracle(tmp_path, orc, mode):
     """The ConvNet (cfg4 shape family) on 2-4 GPUs: 3 SPB steps equal the
     single-process fp64 conv oracle (1e-4) and are bit-identical across ranks."""
