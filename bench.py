@@ -349,8 +349,8 @@ def run_b200(args, world, rank, local, dist):
     workers = spb.rank_workers(k, L, rank, world) if world > 1 else list(range(1, k + 1))
     rows = len(workers) * bw
     m.set_optimizer(cfg["lr"], cfg["momentum"], cfg["weight_decay"])
-    if os.environ.get("SPB_FUSED") is not None:
-        m.set_fused_update(os.environ["SPB_FUSED"] == "1")
+    if os.environ.get("SPB_FUSED") is not None:  # optimizer placement 0 / 1 / 2 (default 2)
+        m.set_fused_update(int(os.environ["SPB_FUSED"]))
     seed = cfg["step_seed"]
     W_ = max(3, args.warmup)
     K = max(1, args.steps)

@@ -105,11 +105,15 @@ SPB_API spb_status spb_set_dataset(spb_ctx* ctx, const float* X, const float* Y,
 /* Params in / out (LayeredModel::initial_params, spb_sgd_run's iterate x). */
 SPB_API spb_status spb_set_params(spb_ctx* ctx, const float* const* blocks);
 SPB_API spb_status spb_get_params(spb_ctx* ctx, float* const* blocks);
-/* fused = 1: single-GPU steps apply the optimizer inside the backward pass
- * (the wgrad GEMM epilogue updates W in place; the aggregated gradient is then
- * not materialised). fused = 0 (default): aggregate into the gradient buffer,
- * readable with spb_get_grads, then one fused update kernel over all params.
- * Multi-GPU steps are always unfused (buckets are reduced first). */
+/* Where single-GPU steps apply the optimizer:
+ *   0: aggregate every layer into the gradient buffer (readable with
+ *      spb_get_grads), then one update kernel per layer beside the backward;
+ *   1: inside every wgrad GEMM epilogue (W updated in place; the aggregated
+ *      gradient is not materialised);
+ *   2 (default): inside the epilogue of the layers whose wgrad covers <= 512
+ *      contributor rows (where that is cheaper), per-layer kernels otherwise.
+ * spb_get_grads after a step is complete only in mode 0. Multi-GPU steps and
+ * the ConvNet always use per-layer updates. */
 SPB_API spb_status spb_set_fused_update(spb_ctx* ctx, int fused);
 /* Optimizer: x -= lr * g (spb.cpp:196) when momentum = weight_decay = 0;
  * otherwise momentum SGD + weight decay (PyTorch semantics). */

@@ -353,8 +353,10 @@ class ChainMlp:
         _check(load_library().spb_get_grads(self._ctx, p), self._ctx)
         return out
 
-    def set_fused_update(self, fused: bool):
-        """Single-GPU: optimizer inside the wgrad epilogue, or a separate pass (default)."""
+    def set_fused_update(self, fused):
+        """Single-GPU optimizer placement: False / 0 per-layer update kernels
+        (gradients readable with get_grads), True / 1 inside every wgrad
+        epilogue, 2 (the default) inside the cheap (<= 512-row) wgrads only."""
         _check(load_library().spb_set_fused_update(self._ctx, int(fused)), self._ctx)
 
     def set_optimizer(self, lr: float, momentum: float = 0.0, weight_decay: float = 0.0):

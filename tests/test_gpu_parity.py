@@ -145,13 +145,15 @@ def test_aggregate_hand_example():
     assert agg[0][0] == -2.5
 
 
-@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("fused", [0, 1, 2])
 @pytest.mark.parametrize("widths,N,k,bw", [([3, 5, 4, 1], 32, 3, 2), ([37, 33, 20, 1], 100, 4, 5),
-                                          ([128, 96, 80, 64, 48, 1], 256, 8, 16), ([784, 512, 512, 1], 4096, 4, 128)])
+                                          ([128, 96, 80, 64, 48, 1], 256, 8, 16), ([784, 512, 512, 1], 4096, 4, 128),
+                                          ([300, 257, 129, 96, 1], 2048, 4, 192)])
 def test_spb_step_batches_grads_and_weights(orc, widths, N, k, bw, fused):
     """One device SPB step: batch indices bit-exact, the aggregated gradient
     (unfused path) within 1e-5 of the oracle's aggregate, weights within 1e-4
-    (fused and unfused optimizer); then 5 steps."""
+    (optimizer placement 0 / 1 / 2; the 192-row case mixes fused and unfused
+    layers under the default 2); then 5 steps."""
     m, X, Y, W = make(widths, N, 13, k=k, bw=bw)
     L = len(widths) - 1
     lr, seed = 0.05, 11
@@ -261,7 +263,7 @@ def test_k1_spb_equals_full_backprop_bitwise():
         assert np.array_equal(x, y)
 
 
-@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("fused", [0, 1, 2])
 def test_momentum_weight_decay_restatement(orc, fused):
     """Momentum SGD + wd (parity unpinned by the reference):
     device update (separate kernel, or fused into the wgrad epilogue) vs the
