@@ -69,11 +69,15 @@ class ClockSampler:
         self.device = device
         self.proc = None
         self.lines = []
+        # 200 ms as in the profiling recipe; SPB_CLOCK_MS=0 turns sampling off (perturbation checks only).
+        self.ms = int(os.environ.get("SPB_CLOCK_MS", "200"))
 
     def start(self):
+        if self.ms <= 0:
+            return
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "50", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                          "-lms", str(self.ms), "-i", str(self.device)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -86,7 +90,8 @@ class ClockSampler:
 
     def stop(self):
         if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None,
+                    "reasons": ["sampling off (SPB_CLOCK_MS=0)" if self.ms <= 0 else "nvidia-smi unavailable"]}
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
