@@ -179,7 +179,7 @@ struct Engine {
   // separate update pass (measured: the fused epilogue costs the same as
   // wgrad + update at 1024 rows and saves ~20 us per layer at <= 512).
   int fused_mode = 2;
-  static constexpr int kFuseMaxRows = 512;
+  static constexpr int kFuseMaxRows = 512;  // 640 / 768 measured the same; 384 slower
   std::vector<char> fuse_layer;  // per layer, set by enqueue_step for enqueue_pass / on_layer
   // Multi-GPU aggregation mode: 0 = NCCL buckets, 1 = NVLS multicast,
   // 2 = peer-to-peer copy-engine pulls (p2p.cu), 3 = NCCL reduce-scatter +
