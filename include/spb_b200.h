@@ -115,6 +115,24 @@ SPB_API spb_status spb_get_params(spb_ctx* ctx, float* const* blocks);
  * spb_get_grads after a step is complete only in mode 0. Multi-GPU steps and
  * the ConvNet always use per-layer updates. */
 SPB_API spb_status spb_set_fused_update(spb_ctx* ctx, int fused);
+/* Cross-step pipelining for spb_train_steps / spb_time_train_steps: up to
+ * `steps` (1..16, default 8, env SPB_CHAIN) consecutive SPB iterations are
+ * captured into ONE CUDA graph in which iteration t+1's forward of layer l
+ * waits only for W_l of iteration t (its update and, multi-GPU, its exchange)
+ * instead of for the whole iteration, so the exchange / update tail of one
+ * iteration overlaps the next forward. Results are identical for every value
+ * (the same kernels in the same data order); 1 = one graph per iteration. */
+SPB_API spb_status spb_set_chain(spb_ctx* ctx, int steps);
+/* Timeline of `steps` (1..16) chained SPB iterations, as replayed from ONE
+ * graph (diagnostic; no reference counterpart): a %globaltimer stamp kernel
+ * on the op's stream before and after every op (GEMMs, reductions, updates,
+ * exchanges, p2p flag waits). Per op (up to cap): begin / end ns, class
+ * (0 fwd, 1 wgrad, 2 dgrad, 3 head, 4 colreduce, 5 update, 6 gather, 7 comm,
+ * 100 wait), stream (0 main, 1 wgrad, 2 update, 3 split, 4 collectives,
+ * 10+p / 20+p gradient / weight pulls from peer p), step index in the chain.
+ * Parameters advance by `steps` iterations twice (warm-up replay + traced). */
+SPB_API spb_status spb_trace_steps(spb_ctx* ctx, uint64_t seed, int step0, int steps, int full_backprop, int cap,
+                                   long long* t_begin, long long* t_end, int* cls, int* stream, int* sub, int* n_out);
 /* Optimizer: x -= lr * g (spb.cpp:196) when momentum = weight_decay = 0;
  * otherwise momentum SGD + weight decay (PyTorch semantics). */
 SPB_API spb_status spb_set_optimizer(spb_ctx* ctx, float lr, float momentum, float weight_decay);
@@ -181,12 +199,17 @@ SPB_API void* spb_stream(spb_ctx* ctx);
  *  - "rs": NCCL reduce-scatter of each layer's gradient, the optimizer on
  *    this rank's shard, NCCL all-gather of the fp32 weights (a layer with one
  *    contributing rank: that rank updates it and broadcasts the weights);
+ *  - "push": the wgrad GEMM epilogue stores each gradient row straight into
+ *    the owning rank's staging slot (NVLink stores through CUDA IPC); the
+ *    owner sums its rows, applies the optimizer and stores the new fp32 rows
+ *    into every peer; peers split them into (hi, lo). No copy engines, no
+ *    NCCL in the step;
  *  - "nccl" (default for more than 2 ranks): per-layer NCCL buckets
  *    (broadcast / all-reduce), then the local optimizer update on every rank.
  * Ranks of one node only. */
 SPB_API spb_status spb_comm_unique_id(void* out128);
 SPB_API spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int nranks);
-/* Active aggregation mode: 0 nccl, 1 nvls, 2 p2p, 3 rs (-1 before spb_comm_init). */
+/* Active aggregation mode: 0 nccl, 1 nvls, 2 p2p, 3 rs, 4 push (-1 before spb_comm_init). */
 SPB_API spb_status spb_comm_mode(spb_ctx* ctx, int* mode);
 /* Collective diagnostic of the NVLS path: multicast reduce + broadcast of a
  * known pattern over all ranks; *mismatches = wrong elements seen here. */

@@ -22,11 +22,14 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <functional>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/spb_b200.h"
@@ -160,10 +163,25 @@ struct Engine {
   Ctl* ctl = nullptr;
   int* workers_dev = nullptr;
   std::vector<int> workers;  // hosted workers, ascending
-  // graphs: [full][host_rows]
-  cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-  int graph_launches[2][2] = {{0, 0}, {0, 0}};
+  // graphs, keyed by (full, host_rows, steps chained in the graph); value:
+  // (exec, kernel launches per step)
+  std::map<std::tuple<bool, bool, int>, std::pair<cudaGraphExec_t, int>> graphs;
   int last_launches = 0;
+  // Cross-step pipelining (a chain of `chain` steps captured in ONE graph):
+  // step t+1's forward of layer l waits only for W_l of step t (its update,
+  // and in multi-GPU modes its exchange), not for the whole of step t, so the
+  // exchange / update tail of step t runs beside the forward of step t+1.
+  // fwd_wait[l] = event index the forward of layer l (the head for l = L)
+  // must wait on, -1 = none; chain_sub = index of the step being enqueued.
+  static constexpr int kMaxChain = 16;
+  int chain = default_chain();
+  int chain_sub = 0;
+  static int default_chain() {
+    const char* c = std::getenv("SPB_CHAIN");
+    const int v = c ? std::atoi(c) : 8;
+    return v < 1 ? 1 : (v > kMaxChain ? kMaxChain : v);
+  }
+  std::vector<int> fwd_wait;
   std::string err;
   // multi-GPU
   ncclComm_t comm = nullptr;
@@ -194,6 +212,16 @@ struct Engine {
   long stage_shard = 0;
   PeerPtrs<int> peer_flags{};
   std::vector<float*> peer_grad, peer_w32;
+  // push mode (comm_mode 4, push.cu): layer l's rows are owned block-wise
+  // (rank o: rows [o * prpo[l], (o + 1) * prpo[l])); pstage holds, per layer
+  // and source rank, the source's gradient rows this rank owns (weight rows
+  // then bias rows, pslot[l] floats per source), written by the sources'
+  // wgrad epilogues over NVLink.
+  float* pstage = nullptr;
+  std::vector<int> prpo;
+  std::vector<long> pstage_off, pslot;
+  std::vector<float*> peer_pstage;
+  bool route_push = false;  // set while enqueue_step builds a push-mode step
   cudaStream_t s4 = nullptr;
   std::vector<cudaStream_t> gpull, wpull;  // per-peer copy streams (copy engines run concurrently)
   // NVLS path (multi-GPU, NVSwitch multicast): p_hi / p_lo / grad live in
@@ -217,12 +245,51 @@ struct Engine {
   };
   std::vector<ProfRec>* prof = nullptr;
   cudaEvent_t prof_a = nullptr;
+  // Timeline tracing (spb_trace_steps): a %globaltimer stamp kernel before
+  // and after every op of a captured graph, on the op's own stream, so the
+  // replayed graph's real per-stream schedule can be read back.
+  static constexpr int kTraceCap = 1 << 15;  // ops
+  static constexpr int kTraceWait = 100;     // class of the p2p flag waits (trace only)
+  struct TraceRec {
+    int cls, stream, sub;
+  };
+  bool tracing = false;
+  unsigned long long* trace_dev = nullptr;
+  std::vector<TraceRec> trace_meta;
+  int trace_open = -1;
+  int stream_id(cudaStream_t q) const {
+    if (q == st) return 0;
+    if (q == s2) return 1;
+    if (q == s3) return 2;
+    if (q == s4) return 3;
+    if (q == cst) return 4;
+    for (size_t p = 0; p < gpull.size(); ++p)
+      if (q == gpull[p]) return 10 + static_cast<int>(p);
+    for (size_t p = 0; p < wpull.size(); ++p)
+      if (q == wpull[p]) return 20 + static_cast<int>(p);
+    return 99;
+  }
+  void tbeg(cudaStream_t s) {
+    if (!tracing) return;
+    if (trace_meta.size() >= static_cast<size_t>(kTraceCap)) throw ConfigError("trace: too many ops");
+    trace_open = static_cast<int>(trace_meta.size());
+    trace_meta.push_back({-1, stream_id(s), chain_sub});
+    launch_stamp(trace_dev + 2 * trace_open, s);
+  }
+  void tend(int cls, cudaStream_t s) {
+    if (!tracing || trace_open < 0) return;
+    trace_meta[trace_open].cls = cls;
+    launch_stamp(trace_dev + 2 * trace_open + 1, s);
+    trace_open = -1;
+  }
   void pbeg(cudaStream_t s) {
+    tbeg(s);
     if (!prof) return;
     SPB_CUDA(cudaEventCreate(&prof_a));
     SPB_CUDA(cudaEventRecord(prof_a, s));
   }
   void pend(int cls, double work, cudaStream_t s) {
+    tend(cls, s);
     if (!prof) return;
     cudaEvent_t b;
     SPB_CUDA(cudaEventCreate(&b));
@@ -238,10 +305,8 @@ struct Engine {
     // (flushes outstanding work) before it is destroyed.
     if (st) cudaStreamSynchronize(st);
     if (cst) cudaStreamSynchronize(cst);
-    for (auto& row : graph)
-      for (auto& g : row)
-        if (g) cudaGraphExecDestroy(g), g = nullptr;
-    if (comm_mode == 2) {
+    invalidate_graphs();
+    if (comm_mode == 2 || comm_mode == 4) {
       // Peers may still read this rank's memory until they pass this point.
       if (s3) cudaStreamSynchronize(s3);
       if (s4) cudaStreamSynchronize(s4);
@@ -258,8 +323,9 @@ struct Engine {
         if (peer_grad[p]) cudaIpcCloseMemHandle(peer_grad[p]);
         if (peer_w32[p]) cudaIpcCloseMemHandle(peer_w32[p]);
         if (peer_flags.p[p]) cudaIpcCloseMemHandle(peer_flags.p[p]);
+        if (p < static_cast<int>(peer_pstage.size()) && peer_pstage[p]) cudaIpcCloseMemHandle(peer_pstage[p]);
       }
-      peer_grad.clear(), peer_w32.clear();
+      peer_grad.clear(), peer_w32.clear(), peer_pstage.clear();
       for (auto q : gpull)
         if (q) cudaStreamDestroy(q);
       for (auto q : wpull)
@@ -412,7 +478,7 @@ struct Engine {
     tmp = alloc<float>(tmp_n);
     splitk_ws = alloc<float>(kSplitkWsFloats);
     ctl = alloc<Ctl>(1);
-    loss_dev = alloc<float>(1);
+    loss_dev = alloc<float>(kMaxChain);
     workers_dev = alloc<int>(k);
     set_workers_all();
   }
@@ -429,9 +495,19 @@ struct Engine {
   }
 
   void invalidate_graphs() {
-    for (auto& row : graph)
-      for (auto& g : row)
-        if (g) cudaGraphExecDestroy(g), g = nullptr;
+    for (auto& kv : graphs)
+      if (kv.second.first) cudaGraphExecDestroy(kv.second.first);
+    graphs.clear();
+  }
+
+  // Event index "W_l of the current step final on this rank".
+  static int ev_ready(int l) { return kEvP2pLayer + 32 * l + 2; }
+
+  // Before the forward of layer l (the head for l = L): wait for W_l of the
+  // previous step of the chain.
+  void fwd_gate(int l, cudaStream_t s) {
+    if (l < static_cast<int>(fwd_wait.size()) && fwd_wait[l] >= 0)
+      SPB_CUDA(cudaStreamWaitEvent(s, ev(fwd_wait[l]), 0));
   }
 
   void ensure_rows(int rows) {
@@ -565,6 +641,7 @@ struct Engine {
     int n = 0;
     const int Lc = L - 1;
     for (int l = 1; l <= Lc; ++l) {
+      fwd_gate(l, s);
       const int M = static_cast<int>(samples * pix[l]);
       const bool tma = conv_tma(l);
       if (!tma) {
@@ -595,12 +672,13 @@ struct Engine {
       pend(kClsFwd, 2.0 * M * w[l] * fan[l], s);
     }
     const bool has_next = Lc >= 1 && row0[Lc] < samples;
+    fwd_gate(L, s);
     pbeg(s);
     launch_avgpool(Hh[Lc], Hl[Lc], ld[Lc], samples, static_cast<int>(pix[Lc]), w[Lc], Ph, Pl, ld[Lc], s);
     launch_head(Ph, Pl, ld[Lc], samples, w[Lc], nout, p_hi + w_off[L], p_lo + w_off[L], ldf[L], p_hi + b_off[L],
                 p_lo + b_off[L], ybatch, delta, row_loss, has_next ? Gh : nullptr, has_next ? Gl : nullptr, ld[Lc],
                 has_next ? row0[Lc] : samples, false, s, /*dn_act=*/false);
-    launch_sum_loss(row_loss, samples, 1.0f / static_cast<float>(samples), loss_dev, step_dev, s);
+    launch_sum_loss(row_loss, samples, 1.0f / static_cast<float>(samples), loss_dev + chain_sub, step_dev, s);
     pend(kClsHead, 0, s);
     n += 3;
     if (row0[L] < samples) {
@@ -720,6 +798,7 @@ struct Engine {
     int n = 0;
     // Forward, hidden layers (mlp_forward model.cpp:108-128 batched).
     for (int l = 1; l < L; ++l) {
+      fwd_gate(l, s);
       Operand A{Hh[l - 1], Hl[l - 1], ld[l - 1], rows, w[l - 1], false};
       Operand B{p_hi + w_off[l], p_lo + w_off[l], ld[l - 1], w[l], w[l - 1], false};
       GemmEpilogue ep{};
@@ -739,11 +818,12 @@ struct Engine {
     auto lf = [&](int l) { return fused && static_cast<int>(fuse_layer.size()) > l && fuse_layer[l]; };
     // Output head: out, delta_L = out - y (model.cpp:156), Delta_{L-1}.
     const bool has_next = L > 1 && row0[L - 1] < rows;
+    fwd_gate(L, s);
     pbeg(s);
     launch_head(Hh[L - 1], Hl[L - 1], ld[L - 1], rows, w[L - 1], nout, p_hi + w_off[L], p_lo + w_off[L], ld[L - 1],
                 p_hi + b_off[L], p_lo + b_off[L], ybatch, delta, row_loss, has_next ? Dh[(L - 1) % kDbuf] : nullptr,
                 has_next ? Dl[(L - 1) % kDbuf] : nullptr, ldd, has_next ? row0[L - 1] : rows, false, s);
-    launch_sum_loss(row_loss, rows, 1.0f / static_cast<float>(rows), loss_dev, step_dev, s);
+    launch_sum_loss(row_loss, rows, 1.0f / static_cast<float>(rows), loss_dev + chain_sub, step_dev, s);
     pend(kClsHead, 0, s);
     n += 2;
     auto col_upd = [&](long off) {
@@ -829,6 +909,7 @@ struct Engine {
           ep.wd = wd;
         } else {
           ep.out_hi = grad + w_off[l];
+          if (route_push) push_route(l, ep);  // rows stored straight to their owners
         }
         pbeg(sw);
         n += gemm_tf32x3(A, B, lf(l) ? kEpiWgradUpdate : kEpiStoreScaled, ep, sw);
@@ -935,7 +1016,7 @@ struct Engine {
     auto evl = [&](int k) { return ev(kEvP2pLayer + 32 * l + k); };
     int n = 0;
     // 1. gradient of l final here -> G[l] to every rank.
-    launch_p2p_signal(peer_flags, 2 * l, nranks, rank, epoch_dev, gs);
+    launch_p2p_signal(peer_flags, 2 * l, nranks, rank, epoch_dev, chain_sub, gs);
     SPB_CUDA(cudaEventRecord(evl(0), s));  // dgrad_l issued on s before this point
     ++n;
     // 2. copy engines, one stream per peer: wait for the peer's G[l] (every
@@ -951,8 +1032,15 @@ struct Engine {
         continue;
       }
       cudaStream_t cs = gpull[r];
-      if (l + 2 <= L) SPB_CUDA(cudaStreamWaitEvent(cs, ev(kEvP2pLayer + 32 * (l + 2) + 1), 0));
-      launch_p2p_wait(flags, 2 * l, nranks, 1u << r, epoch_dev, cs);
+      // Staging buffer l % 2 was last read by the shard update of layer l + 2,
+      // or (top layers, chained step) of layer 1 / 2 of the previous step.
+      if (l + 2 <= L)
+        SPB_CUDA(cudaStreamWaitEvent(cs, ev(kEvP2pLayer + 32 * (l + 2) + 1), 0));
+      else if (chain_sub > 0 && l + 2 - L >= 1 && l + 2 - L <= 2)
+        SPB_CUDA(cudaStreamWaitEvent(cs, ev(kEvP2pLayer + 32 * ((l % 2) == 1 ? 1 : 2) + 1), 0));
+      tbeg(cs);
+      launch_p2p_wait(flags, 2 * l, nranks, 1u << r, epoch_dev, chain_sub, cs);
+      tend(kTraceWait, cs);
       ++n;
       if (contrib >> r & 1u) {
         float* dst = st_buf + static_cast<long>(slot++) * stage_shard;
@@ -975,14 +1063,16 @@ struct Engine {
     launch_p2p_update(src, nsrc, p_hi + off + a, p_lo + off + a, mom ? mom + off + a : nullptr, w32 + off + a, sh, lr, mu,
                       wd, s3);
     pend(kClsUpdate, static_cast<double>(sh) * 4.0 * (nsrc + (mom ? 7 : 5)), s3);
-    launch_p2p_signal(peer_flags, 2 * l + 1, nranks, rank, epoch_dev, s3);
+    launch_p2p_signal(peer_flags, 2 * l + 1, nranks, rank, epoch_dev, chain_sub, s3);
     SPB_CUDA(cudaEventRecord(evl(1), s3));
     n += 2;
     // 4. copy engines, one stream per peer: pull its updated fp32 shard.
     for (int r = 0; r < nranks; ++r) {
       if (r == rank) continue;
       cudaStream_t cs = wpull[r];
-      launch_p2p_wait(flags, 2 * l + 1, nranks, 1u << r, epoch_dev, cs);
+      tbeg(cs);
+      launch_p2p_wait(flags, 2 * l + 1, nranks, 1u << r, epoch_dev, chain_sub, cs);
+      tend(kTraceWait, cs);
       ++n;
       const long ra = lo_of(r), rb = lo_of(r + 1);
       pbeg(cs);
@@ -998,6 +1088,10 @@ struct Engine {
     launch_p2p_split(w32 + off, p_hi + off, p_lo + off, cnt, a, b, s4);
     pend(kClsUpdate, static_cast<double>(cnt - sh) * 12.0, s4);
     ++n;
+    // W_l final here: the peers' shards split (s4) and this rank's own (s3).
+    SPB_CUDA(cudaStreamWaitEvent(s4, evl(1), 0));
+    SPB_CUDA(cudaEventRecord(ev(ev_ready(l)), s4));
+    fwd_wait[l] = ev_ready(l);
     return n;
   }
 
@@ -1121,6 +1215,157 @@ struct Engine {
     host_barrier();
   }
 
+  // push mode setup (collective over the ranks): staging slots, fp32 weight
+  // copies for the received rows, flags; every peer's pstage / w32 / flags
+  // mapped through CUDA IPC. MLP only (the conv wgrad has no row routing).
+  void setup_push() {
+    if (nranks > kMaxPeers) throw ConfigError("comm: push mode supports at most 8 ranks");
+    if (conv_model) throw ConfigError("comm: push mode is MLP-only");
+    if (!bar_dev) bar_dev = alloc<float>(1);
+    w32 = alloc<float>(nflat);
+    flags = alloc<int>(2L * (L + 1) * nranks);
+    epoch_dev = alloc<int>(1);
+    prpo.assign(L + 1, 0);
+    pstage_off.assign(L + 1, 0);
+    pslot.assign(L + 1, 0);
+    long tot = 0;
+    for (int l = 1; l <= L; ++l) {
+      prpo[l] = (w[l] + nranks - 1) / nranks;
+      pslot[l] = round_up(static_cast<long>(prpo[l]) * ld[l - 1] + prpo[l], 32);
+      pstage_off[l] = tot;
+      tot += pslot[l] * nranks;
+    }
+    pstage = alloc<float>(tot);
+    cudaIpcMemHandle_t mine[3];
+    SPB_CUDA(cudaIpcGetMemHandle(&mine[0], pstage));
+    SPB_CUDA(cudaIpcGetMemHandle(&mine[1], w32));
+    SPB_CUDA(cudaIpcGetMemHandle(&mine[2], flags));
+    const size_t hb = sizeof mine;
+    char* dbuf = nullptr;
+    SPB_CUDA(cudaMalloc(&dbuf, hb * (nranks + 1)));
+    SPB_CUDA(cudaMemcpy(dbuf, mine, hb, cudaMemcpyHostToDevice));
+    nccl_check(nccl().AllGather(dbuf, dbuf + hb, hb, ncclUint8, comm, cst));
+    SPB_CUDA(cudaStreamSynchronize(cst));
+    std::vector<cudaIpcMemHandle_t> all(3 * nranks);
+    SPB_CUDA(cudaMemcpy(all.data(), dbuf + hb, hb * nranks, cudaMemcpyDeviceToHost));
+    cudaFree(dbuf);
+    peer_grad.assign(nranks, nullptr);
+    peer_pstage.assign(nranks, nullptr);
+    peer_w32.assign(nranks, nullptr);
+    for (int p = 0; p < nranks; ++p) {
+      if (p == rank) {
+        peer_pstage[p] = pstage, peer_w32[p] = w32, peer_flags.p[p] = flags;
+        continue;
+      }
+      void* q = nullptr;
+      SPB_CUDA(cudaIpcOpenMemHandle(&q, all[3 * p + 0], cudaIpcMemLazyEnablePeerAccess));
+      peer_pstage[p] = static_cast<float*>(q);
+      SPB_CUDA(cudaIpcOpenMemHandle(&q, all[3 * p + 1], cudaIpcMemLazyEnablePeerAccess));
+      peer_w32[p] = static_cast<float*>(q);
+      SPB_CUDA(cudaIpcOpenMemHandle(&q, all[3 * p + 2], cudaIpcMemLazyEnablePeerAccess));
+      peer_flags.p[p] = static_cast<int*>(q);
+    }
+    SPB_CUDA(cudaStreamCreateWithFlags(&s4, cudaStreamNonBlocking));
+    comm_mode = 4;
+    invalidate_graphs();
+    host_barrier();
+  }
+
+  // push mode: where the wgrad epilogue of layer l stores gradient row r
+  // (GemmEpilogue::route): the owner's staging slot for this rank, or this
+  // rank's own gradient buffer for its own rows.
+  void push_route(int l, GemmEpilogue& ep) const {
+    ep.route_rows = prpo[l];
+    for (int o = 0; o < nranks; ++o)
+      ep.route[o] = o == rank ? grad + w_off[l] + static_cast<long>(o) * prpo[l] * ld[l - 1]
+                              : peer_pstage[o] + pstage_off[l] + static_cast<long>(rank) * pslot[l];
+  }
+
+  // push mode, layer l (protocol: push.cu). gs: the stream that produced this
+  // rank's gradient of l (its wgrad already stored the weight rows to their
+  // owners, except for the head layer); s: main stream (dgrad_l issued).
+  int enqueue_push_layer(int l, bool full, cudaStream_t gs, cudaStream_t s) {
+    const Bucket* bk = nullptr;
+    for (auto& b : buckets[full])
+      if (b.l_lo <= l && l <= b.l_hi) bk = &b;
+    if (!bk) throw ConfigError("comm: no bucket for layer");
+    unsigned contrib = 0;
+    for (int r : bk->ranks) contrib |= 1u << r;
+    const bool mine = contrib >> rank & 1u;
+    const unsigned peers = ((1u << nranks) - 1u) & ~(1u << rank);
+    const long ldw = ld[l - 1];
+    const int rpo = prpo[l];
+    const int r0 = std::min(w[l], rank * rpo), r1 = std::min(w[l], (rank + 1) * rpo);
+    auto evl = [&](int k) { return ev(kEvP2pLayer + 32 * l + k); };
+    // Layer L's weight gradient comes from a column reduction, not the routed
+    // wgrad GEMM: its rows travel with the signal.
+    const bool rows_in_signal = l == L || conv_model;
+    PeerPtrs<float> wdst{}, bdst{};
+    for (int o = 0; o < nranks; ++o) {
+      if (o == rank) continue;
+      wdst.p[o] = peer_pstage[o] + pstage_off[l] + static_cast<long>(rank) * pslot[l];
+      bdst.p[o] = wdst.p[o] + static_cast<long>(rpo) * ldw;
+    }
+    // 1. bias rows (+ head weight rows) to their owners, fence, G[l].
+    pbeg(gs);
+    launch_push_signal(peer_flags, 2 * l, nranks, rank, epoch_dev, chain_sub,
+                       mine && rows_in_signal ? grad + w_off[l] : nullptr, ldw, mine ? grad + b_off[l] : nullptr, rpo,
+                       w[l], wdst, bdst, gs);
+    pend(kClsComm, 0, gs);
+    SPB_CUDA(cudaEventRecord(evl(0), s));  // dgrad_l issued on s before this point
+    SPB_CUDA(cudaEventRecord(ev(kEvBucket + l), gs));
+    // 2. owner update on s3: every rank's G[l], own gradient final, dgrad_l
+    // done (the update rewrites W_l rows in place).
+    SPB_CUDA(cudaStreamWaitEvent(s3, ev(kEvBucket + l), 0));
+    SPB_CUDA(cudaStreamWaitEvent(s3, evl(0), 0));
+    tbeg(s3);
+    launch_p2p_wait(flags, 2 * l, nranks, peers, epoch_dev, chain_sub, s3);
+    tend(kTraceWait, s3);
+    const long nw = static_cast<long>(r1 - r0) * ldw, nb = r1 - r0;
+    PeerPtrs<const float> sw{}, sb{};
+    PeerPtrs<float> dw{}, db{};
+    int nsrc = 0, ndst = 0;
+    for (int r = 0; r < nranks; ++r) {
+      if (!(contrib >> r & 1u)) continue;
+      if (r == rank) {
+        sw.p[nsrc] = grad + w_off[l] + static_cast<long>(r0) * ldw;
+        sb.p[nsrc] = grad + b_off[l] + r0;
+      } else {
+        sw.p[nsrc] = pstage + pstage_off[l] + static_cast<long>(r) * pslot[l];
+        sb.p[nsrc] = sw.p[nsrc] + static_cast<long>(rpo) * ldw;
+      }
+      ++nsrc;
+    }
+    for (int o = 0; o < nranks; ++o) {
+      if (o == rank) continue;
+      dw.p[ndst] = peer_w32[o] + w_off[l] + static_cast<long>(r0) * ldw;
+      db.p[ndst] = peer_w32[o] + b_off[l] + r0;
+      ++ndst;
+    }
+    pbeg(s3);
+    launch_push_update(sw, nsrc, p_hi + w_off[l] + r0 * ldw, p_lo + w_off[l] + r0 * ldw,
+                       mom ? mom + w_off[l] + r0 * ldw : nullptr, dw, ndst, nw, lr, mu, wd, s3);
+    launch_push_update(sb, nsrc, p_hi + b_off[l] + r0, p_lo + b_off[l] + r0, mom ? mom + b_off[l] + r0 : nullptr, db,
+                       ndst, nb, lr, mu, wd, s3);
+    pend(kClsUpdate, static_cast<double>(nw + nb) * 4.0 * (nsrc + (mom ? 5 : 4)), s3);
+    launch_p2p_signal(peer_flags, 2 * l + 1, nranks, rank, epoch_dev, chain_sub, s3);
+    SPB_CUDA(cudaEventRecord(evl(1), s3));
+    // 3. the other owners' rows: wait for their U[l] and for dgrad_l, split.
+    tbeg(s4);
+    launch_p2p_wait(flags, 2 * l + 1, nranks, peers, epoch_dev, chain_sub, s4);
+    tend(kTraceWait, s4);
+    SPB_CUDA(cudaStreamWaitEvent(s4, evl(0), 0));
+    pbeg(s4);
+    launch_push_split(w32 + w_off[l], p_hi + w_off[l], p_lo + w_off[l], static_cast<long>(w[l]) * ldw, r0 * ldw,
+                      r1 * ldw, s4);
+    launch_push_split(w32 + b_off[l], p_hi + b_off[l], p_lo + b_off[l], w[l], r0, r1, s4);
+    pend(kClsUpdate, static_cast<double>(w[l] - (r1 - r0)) * (ldw + 1) * 12.0, s4);
+    SPB_CUDA(cudaStreamWaitEvent(s4, evl(1), 0));
+    SPB_CUDA(cudaEventRecord(ev(ev_ready(l)), s4));
+    fwd_wait[l] = ev_ready(l);
+    return 6;
+  }
+
   void host_barrier() {
     nccl_check(nccl().AllReduce(bar_dev, bar_dev, 1, ncclFloat32, ncclSum, comm, cst));
     SPB_CUDA(cudaStreamSynchronize(cst));
@@ -1186,9 +1431,19 @@ struct Engine {
     }
   }
 
-  int enqueue_step(bool full, bool host_rows, cudaStream_t s) {
+  // Step `sub` of a chain of `nsub` steps captured into one graph (sub = 0,
+  // nsub = 1: a plain step). Side streams are joined back into s only after
+  // the last step of the chain; before that, the next step's forward waits
+  // per layer (fwd_wait) for the weights this step finalises.
+  int enqueue_step(bool full, bool host_rows, cudaStream_t s, int sub = 0, int nsub = 1) {
     const int rows = static_cast<int>(workers.size()) * bw;
     int n = 0;
+    if (nsub < 1 || nsub > kMaxChain || sub < 0 || sub >= nsub) throw ArgumentError("enqueue_step: bad chain index");
+    chain_sub = sub;
+    if (sub == 0) fwd_wait.assign(L + 1, -1);
+    const bool last = sub == nsub - 1;
+    // The gather overwrites H_0, read by wgrad_1 of the previous step (s2,
+    // joined into s by enqueue_pass), so it needs no extra wait.
     pbeg(s);
     if (host_rows && conv_model) {
       // Host images already in xin (spb_step_host): identity index, and no
@@ -1232,8 +1487,9 @@ struct Engine {
       n += enqueue_pass(rows, row0, alpha, s,
                         [&](int l, cudaStream_t from) { return enqueue_rs_layer(l, full, from, s); }, false,
                         &ctl->step, nullptr);
-      join(cst, kEvStepJoin);
+      join(cst, kEvStepJoin);  // not pipelined across steps: joined every step
       join(s3, kEvUpdJoin);
+      fwd_wait.assign(L + 1, -1);
       return n;
     }
     if (comm && comm_mode == 2) {
@@ -1247,8 +1503,31 @@ struct Engine {
       n += enqueue_pass(rows, row0, alpha, s,
                         [&](int l, cudaStream_t from) { return enqueue_p2p_layer(l, full, from, s); }, false,
                         &ctl->step, nullptr);
+      if (!last) return n;  // enqueue_p2p_layer set fwd_wait for the next step
       for (size_t i = 0; i < side.size(); ++i) join(side[i], kEvP2pFork + 32 + static_cast<int>(i));
-      launch_p2p_epoch(epoch_dev, s);
+      launch_p2p_epoch(epoch_dev, nsub, s);
+      return n + 1;
+    }
+    if (comm && comm_mode == 4) {
+      // Per layer (top down): gradient rows stored to their owners by the
+      // wgrad epilogue, G signal on the gradient stream, owner update + weight
+      // stores on s3, split of the received rows on s4.
+      fork(s3, kEvP2pFork);
+      fork(s4, kEvP2pFork + 1);
+      route_push = true;
+      try {
+        n += enqueue_pass(rows, row0, alpha, s,
+                          [&](int l, cudaStream_t from) { return enqueue_push_layer(l, full, from, s); }, false,
+                          &ctl->step, nullptr);
+      } catch (...) {
+        route_push = false;
+        throw;
+      }
+      route_push = false;
+      if (!last) return n;
+      join(s3, kEvP2pFork + 32);
+      join(s4, kEvP2pFork + 33);
+      launch_p2p_epoch(epoch_dev, nsub, s);
       return n + 1;
     }
     if (comm && nvls) {
@@ -1263,7 +1542,8 @@ struct Engine {
                           epoch_dev, cst);
       launch_nvls_epoch(epoch_dev, cst);
       n += 2;
-      join(cst, kEvStepJoin);
+      join(cst, kEvStepJoin);  // not pipelined across steps: joined every step
+      fwd_wait.assign(L + 1, -1);
       return n;
     }
     if (comm) fork(cst, kEvStepFork);
@@ -1280,36 +1560,63 @@ struct Engine {
       launch_sgd_update(p_hi + off, p_lo + off, grad + off, mom ? mom + off : nullptr, cnt, lr, mu, wd, us);
       pend(kClsUpdate, static_cast<double>(cnt) * 4.0 * (mom ? 7 : 5), us);
       ++n;
+      if (us != s) {  // W_l final on us
+        SPB_CUDA(cudaEventRecord(ev(ev_ready(l)), us));
+        fwd_wait[l] = ev_ready(l);
+      }
     };
     if (comm) {
       n += enqueue_pass(rows, row0, alpha, s, [&](int l, cudaStream_t from) { return enqueue_bucket(l, full, from); },
                         false, &ctl->step, on_layer);
-      join(cst, kEvStepJoin);
+      if (last) join(cst, kEvStepJoin);
     } else {
       n += enqueue_pass(rows, row0, alpha, s, nullptr, fused_ok, &ctl->step,
                         per_layer ? std::function<void(int, cudaStream_t)>(on_layer) : nullptr);
     }
-    if (per_layer && concurrent) join(s3, kEvUpdJoin);
+    if (per_layer && concurrent && last) join(s3, kEvUpdJoin);
     return n;
   }
 
-  cudaGraphExec_t get_graph(bool full, bool host_rows) {
-    cudaGraphExec_t& g = graph[full][host_rows];
-    if (g) return g;
-    cudaGraph_t gr;
-    SPB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    int n = 0;
-    try {
-      n = enqueue_step(full, host_rows, st);
-    } catch (...) {
-      cudaStreamEndCapture(st, &gr);
-      throw;
+  // The graph of `nsub` chained steps (see enqueue_step); `launches` gets the
+  // kernel launches per step.
+  cudaGraphExec_t get_graph(bool full, bool host_rows, int nsub = 1, int* launches = nullptr) {
+    auto& slot = graphs[std::make_tuple(full, host_rows, nsub)];
+    if (!slot.first) {
+      cudaGraph_t gr;
+      SPB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      int n = 0;
+      try {
+        for (int t = 0; t < nsub; ++t) n += enqueue_step(full, host_rows, st, t, nsub);
+      } catch (...) {
+        cudaStreamEndCapture(st, &gr);
+        graphs.erase(std::make_tuple(full, host_rows, nsub));
+        throw;
+      }
+      SPB_CUDA(cudaStreamEndCapture(st, &gr));
+      cudaGraphExec_t g = nullptr;
+      cudaError_t e = cudaGraphInstantiate(&g, gr, 0);
+      cudaGraphDestroy(gr);
+      if (e != cudaSuccess) {
+        graphs.erase(std::make_tuple(full, host_rows, nsub));
+        SPB_CUDA(e);
+      }
+      slot = {g, n / nsub};
     }
-    SPB_CUDA(cudaStreamEndCapture(st, &gr));
-    SPB_CUDA(cudaGraphInstantiate(&g, gr, 0));
-    cudaGraphDestroy(gr);
-    graph_launches[full][host_rows] = n;
-    return g;
+    if (launches) *launches = slot.second;
+    return slot.first;
+  }
+
+  // Replay `steps` steps as chained graphs of up to `chain` steps each
+  // (losses: the per-step loss, copied back asynchronously; may be null).
+  void run_steps(bool full, int steps, float* losses) {
+    int done = 0;
+    while (done < steps) {
+      const int c = std::max(1, std::min({chain, kMaxChain, steps - done}));
+      cudaGraphExec_t g = get_graph(full, false, c, &last_launches);
+      SPB_CUDA(cudaGraphLaunch(g, st));
+      if (losses) SPB_CUDA(cudaMemcpyAsync(losses + done, loss_dev, c * sizeof(float), cudaMemcpyDeviceToHost, st));
+      done += c;
+    }
   }
 };
 
@@ -1499,6 +1806,13 @@ spb_status spb_set_fused_update(spb_ctx* ctx, int fused) {
   });
 }
 
+spb_status spb_set_chain(spb_ctx* ctx, int steps) {
+  return guard(ctx, [&] {
+    if (steps < 1 || steps > Engine::kMaxChain) throw spb::ArgumentError("set_chain: steps must be in [1, 16]");
+    ctx->e.chain = steps;
+  });
+}
+
 spb_status spb_set_optimizer(spb_ctx* ctx, float lr, float momentum, float weight_decay) {
   return guard(ctx, [&] {
     auto& e = ctx->e;
@@ -1598,14 +1912,9 @@ spb_status spb_train_steps(spb_ctx* ctx, uint64_t seed, int step0, int steps, in
     if (!e.X) throw spb::ConfigError("train_steps: no dataset");
     if (steps < 0) throw spb::ArgumentError("train_steps: steps must be >= 0");
     e.ensure_rows(static_cast<int>(e.workers.size()) * e.bw);
-    cudaGraphExec_t g = e.get_graph(full_backprop != 0, false);
     spb::Ctl c{seed, step0, 0};
     SPB_CUDA(cudaMemcpyAsync(e.ctl, &c, sizeof c, cudaMemcpyHostToDevice, e.st));
-    for (int i = 0; i < steps; ++i) {
-      SPB_CUDA(cudaGraphLaunch(g, e.st));
-      if (losses) SPB_CUDA(cudaMemcpyAsync(losses + i, e.loss_dev, 4, cudaMemcpyDeviceToHost, e.st));
-    }
-    e.last_launches = e.graph_launches[full_backprop != 0][0];
+    e.run_steps(full_backprop != 0, steps, losses);
     if (losses) SPB_CUDA(cudaStreamSynchronize(e.st));
   });
 }
@@ -1615,14 +1924,13 @@ spb_status spb_step_host(spb_ctx* ctx, const float* X_rows, const float* Y_rows,
     auto& e = ctx->e;
     const int rows = static_cast<int>(e.workers.size()) * e.bw;
     e.ensure_rows(rows);
-    cudaGraphExec_t g = e.get_graph(full_backprop != 0, true);
+    cudaGraphExec_t g = e.get_graph(full_backprop != 0, true, 1, &e.last_launches);
     const size_t per = e.conv_model ? static_cast<size_t>(e.ldx) : static_cast<size_t>(e.w[0]);
     SPB_CUDA(cudaMemcpyAsync(e.xin, X_rows, static_cast<size_t>(rows) * per * 4, cudaMemcpyHostToDevice, e.st));
     SPB_CUDA(cudaMemcpyAsync(e.ybatch, Y_rows, static_cast<size_t>(rows) * e.nout * 4, cudaMemcpyHostToDevice, e.st));
     SPB_CUDA(cudaGraphLaunch(g, e.st));
     SPB_CUDA(cudaMemcpyAsync(loss_out, e.loss_dev, 4, cudaMemcpyDeviceToHost, e.st));
     SPB_CUDA(cudaStreamSynchronize(e.st));
-    e.last_launches = e.graph_launches[full_backprop != 0][1];
   });
 }
 
@@ -1690,9 +1998,10 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     // pattern (~450 GB/s per GPU) no longer beats NCCL's rings.
     const char* cm = std::getenv("SPB_COMM");
     const std::string mode = cm ? cm : (nranks == 2 ? "p2p" : "nccl");
-    if (mode != "p2p" && mode != "nccl" && mode != "nvls" && mode != "rs")
-      throw spb::ArgumentError("comm: SPB_COMM must be p2p, nccl, rs or nvls");
+    if (mode != "p2p" && mode != "nccl" && mode != "nvls" && mode != "rs" && mode != "push")
+      throw spb::ArgumentError("comm: SPB_COMM must be push, p2p, nccl, rs or nvls");
     if (nranks > 1 && mode == "p2p") e.setup_p2p();
+    if (nranks > 1 && mode == "push") e.setup_push();
     if (nranks > 1 && mode == "rs") e.setup_rs();
     if (nranks > 1 && mode == "nvls") {
       // Socket names derive from the unique id, shared by all ranks.
@@ -1787,24 +2096,65 @@ spb_status spb_profile_step(spb_ctx* ctx, uint64_t seed, int step, int full_back
   });
 }
 
+spb_status spb_trace_steps(spb_ctx* ctx, uint64_t seed, int step0, int steps, int full_backprop, int cap,
+                           long long* t_begin, long long* t_end, int* cls, int* stream, int* sub, int* n_out) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    if (!e.X) throw spb::ConfigError("trace_steps: no dataset");
+    if (steps < 1 || steps > Engine::kMaxChain) throw spb::ArgumentError("trace_steps: steps must be in [1, 16]");
+    if (!e.trace_dev) e.trace_dev = e.alloc<unsigned long long>(2L * Engine::kTraceCap);
+    e.invalidate_graphs();  // the traced graph must not be reused untraced
+    e.trace_meta.clear();
+    e.tracing = true;
+    cudaGraphExec_t g = nullptr;
+    try {
+      g = e.get_graph(full_backprop != 0, false, steps);
+    } catch (...) {
+      e.tracing = false;
+      throw;
+    }
+    e.tracing = false;
+    spb::Ctl c{seed, step0, 0};
+    SPB_CUDA(cudaMemcpyAsync(e.ctl, &c, sizeof c, cudaMemcpyHostToDevice, e.st));
+    SPB_CUDA(cudaGraphLaunch(g, e.st));  // warm-up replay (graph upload)
+    SPB_CUDA(cudaGraphLaunch(g, e.st));
+    const int n = static_cast<int>(e.trace_meta.size());
+    std::vector<unsigned long long> ts(2L * n);
+    SPB_CUDA(cudaMemcpyAsync(ts.data(), e.trace_dev, ts.size() * 8, cudaMemcpyDeviceToHost, e.st));
+    SPB_CUDA(cudaStreamSynchronize(e.st));
+    e.invalidate_graphs();
+    *n_out = n;
+    for (int i = 0; i < n && i < cap; ++i) {
+      t_begin[i] = static_cast<long long>(ts[2 * i]);
+      t_end[i] = static_cast<long long>(ts[2 * i + 1]);
+      cls[i] = e.trace_meta[i].cls;
+      stream[i] = e.trace_meta[i].stream;
+      sub[i] = e.trace_meta[i].sub;
+    }
+  });
+}
+
 spb_status spb_time_train_steps(spb_ctx* ctx, uint64_t seed, int step0, int steps, int full_backprop, float* ms) {
   return guard(ctx, [&] {
     auto& e = ctx->e;
     if (!e.X) throw spb::ConfigError("train_steps: no dataset");
-    cudaGraphExec_t g = e.get_graph(full_backprop != 0, false);
+    for (int d = 0; d < steps;) {  // instantiate every graph of the run before timing
+      const int c = std::max(1, std::min({e.chain, Engine::kMaxChain, steps - d}));
+      e.get_graph(full_backprop != 0, false, c);
+      d += c;
+    }
     spb::Ctl c{seed, step0, 0};
     SPB_CUDA(cudaMemcpyAsync(e.ctl, &c, sizeof c, cudaMemcpyHostToDevice, e.st));
     cudaEvent_t a, b;
     SPB_CUDA(cudaEventCreate(&a));
     SPB_CUDA(cudaEventCreate(&b));
     SPB_CUDA(cudaEventRecord(a, e.st));
-    for (int i = 0; i < steps; ++i) SPB_CUDA(cudaGraphLaunch(g, e.st));
+    e.run_steps(full_backprop != 0, steps, nullptr);
     SPB_CUDA(cudaEventRecord(b, e.st));
     SPB_CUDA(cudaEventSynchronize(b));
     SPB_CUDA(cudaEventElapsedTime(ms, a, b));
     cudaEventDestroy(a);
     cudaEventDestroy(b);
-    e.last_launches = e.graph_launches[full_backprop != 0][0];
   });
 }
 

@@ -57,7 +57,22 @@ struct GemmEpilogue {
   // Workspace the host launcher may use for split-K partials (nullable).
   float* splitk_ws;
   long splitk_ws_floats;
+  // kEpiStoreScaled row routing (multi-GPU "push" exchange): when
+  // route_rows > 0, output row r belongs to owner o = r / route_rows and is
+  // stored at route[o] + (r - o * route_rows) * ld_out + col -- the owner's
+  // staging slot in peer memory (NVLink stores), or this rank's own buffer.
+  float* route[8];
+  int route_rows;
 };
+
+// Address of output element (row, col) of a kEpiStoreScaled epilogue.
+__device__ __forceinline__ float* store_addr(const GemmEpilogue& ep, int row, int col, long out_shift) {
+  if (ep.route_rows > 0) {
+    const int o = row / ep.route_rows;
+    return ep.route[o] + static_cast<long>(row - o * ep.route_rows) * ep.ld_out + col;
+  }
+  return ep.out_hi + out_shift + static_cast<long>(row) * ep.ld_out + col;
+}
 
 // The optimizer step on one weight (PyTorch SGD semantics, see kernels.cu
 // sgd_update_kernel): g' = g + wd*w; buf = mu*buf + g'; w -= lr*buf.
@@ -131,7 +146,7 @@ template <int EPI>
 __device__ __forceinline__ void epilogue_one(const GemmEpilogue& ep, float v, int row, int col) {
   const long at = row * ep.ld_out + col;
   if constexpr (EPI == kEpiStoreScaled) {
-    ep.out_hi[at] = ep.alpha * v;
+    *store_addr(ep, row, col, 0) = ep.alpha * v;
   } else if constexpr (EPI == kEpiFwdTanh || EPI == kEpiFwdLinear) {
     float z = v + (ep.bias_hi[col] + ep.bias_lo[col]);
     if (EPI == kEpiFwdTanh) z = tanhf(z);
@@ -163,7 +178,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
   if (row >= ep.M) return;
   const bool full = (col0 + 32 <= n_lim);
   if constexpr (EPI == kEpiStoreScaled) {
-    float* o = ep.out_hi + out_shift + row * ep.ld_out + col0;
+    float* o = store_addr(ep, row, col0, out_shift);
     if (full) {
 #pragma unroll
       for (int j = 0; j < 32; j += 4)

@@ -434,6 +434,17 @@ void launch_join(const float* hi, const float* lo, long n, float* out, cudaStrea
   SPB_CUDA(cudaGetLastError());
 }
 
+__global__ void stamp_kernel(unsigned long long* slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *slot = t;
+}
+
+void launch_stamp(unsigned long long* slot, cudaStream_t s) {
+  stamp_kernel<<<1, 1, 0, s>>>(slot);
+  SPB_CUDA(cudaGetLastError());
+}
+
 void launch_sum_loss(const float* row_loss, int rows, float scale, float* out, int* step_dev, cudaStream_t s) {
   sum_loss_kernel<<<1, 1024, 0, s>>>(row_loss, rows, scale, out, step_dev);
   SPB_CUDA(cudaGetLastError());

@@ -109,5 +109,7 @@ void launch_split(const float* in, long n, float* hi, float* lo, cudaStream_t s)
 void launch_join(const float* hi, const float* lo, long n, float* out, cudaStream_t s);
 // Also advances *step_dev (nullable): the next step's Rng stream.
 void launch_sum_loss(const float* row_loss, int rows, float scale, float* out, int* step_dev, cudaStream_t s);
+// One thread writes %globaltimer (ns) to *slot (timeline tracing).
+void launch_stamp(unsigned long long* slot, cudaStream_t s);
 
 }  // namespace spb

@@ -13,8 +13,10 @@
 //   4. wait for U[l] of every rank, PULL their w32 shards (copy engines);
 //   5. split kernel: w32 -> (hi, lo) for the pulled shards.
 // Signals are epoch-stamped flags written into the peers' flag arrays with
-// st.release.sys and polled with ld.acquire.sys; the epoch is the step count,
-// advanced at the end of every step, identically on all ranks.
+// st.release.sys and polled with ld.acquire.sys; step t of a replayed graph
+// uses the value epoch + t + 1, and the epoch advances by the graph's step
+// count after its last step, identically on all ranks (values only grow, so
+// a wait is a >= compare).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -42,22 +44,24 @@ __device__ __forceinline__ void spin_ge(const int* flag, int target) {
 }
 
 // flags layout (every rank): [slot][src rank] int.
-__global__ void p2p_signal_kernel(PeerPtrs<int> flags, int slot, int nranks, int rank, const int* epoch) {
+// Flag value of step `sub` of the graph being replayed: epoch + sub + 1 (the
+// epoch advances by the graph's step count after its last step).
+__global__ void p2p_signal_kernel(PeerPtrs<int> flags, int slot, int nranks, int rank, const int* epoch, int sub) {
   __threadfence_system();
-  const int v = *epoch + 1;
+  const int v = *epoch + sub + 1;
   for (int p = threadIdx.x; p < nranks; p += blockDim.x) {
     int* f = flags.p[p] + slot * nranks + rank;
     asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
   }
 }
 
-__global__ void p2p_wait_kernel(const int* flags, int slot, int nranks, unsigned mask, const int* epoch) {
-  const int target = *epoch + 1;
+__global__ void p2p_wait_kernel(const int* flags, int slot, int nranks, unsigned mask, const int* epoch, int sub) {
+  const int target = *epoch + sub + 1;
   for (int p = threadIdx.x; p < nranks; p += blockDim.x)
     if (mask >> p & 1u) spin_ge(flags + slot * nranks + p, target);
 }
 
-__global__ void p2p_epoch_kernel(int* epoch) { *epoch += 1; }
+__global__ void p2p_epoch_kernel(int* epoch, int add) { *epoch += add; }
 
 // Shard update: g = sum of the contributions (fixed rank order), then
 // g' = g + wd*w; buf = mu*buf + g'; w -= lr*buf; hi, lo = split(w); w32 = w.
@@ -126,18 +130,19 @@ int grid_for(long n4) { return static_cast<int>(std::max<long>(1, std::min<long>
 
 }  // namespace
 
-void launch_p2p_signal(const PeerPtrs<int>& flags, int slot, int nranks, int rank, const int* epoch, cudaStream_t s) {
-  p2p_signal_kernel<<<1, 32, 0, s>>>(flags, slot, nranks, rank, epoch);
+void launch_p2p_signal(const PeerPtrs<int>& flags, int slot, int nranks, int rank, const int* epoch, int sub,
+                       cudaStream_t s) {
+  p2p_signal_kernel<<<1, 32, 0, s>>>(flags, slot, nranks, rank, epoch, sub);
   SPB_CUDA(cudaGetLastError());
 }
 
-void launch_p2p_wait(const int* flags, int slot, int nranks, unsigned mask, const int* epoch, cudaStream_t s) {
-  p2p_wait_kernel<<<1, 32, 0, s>>>(flags, slot, nranks, mask, epoch);
+void launch_p2p_wait(const int* flags, int slot, int nranks, unsigned mask, const int* epoch, int sub, cudaStream_t s) {
+  p2p_wait_kernel<<<1, 32, 0, s>>>(flags, slot, nranks, mask, epoch, sub);
   SPB_CUDA(cudaGetLastError());
 }
 
-void launch_p2p_epoch(int* epoch, cudaStream_t s) {
-  p2p_epoch_kernel<<<1, 1, 0, s>>>(epoch);
+void launch_p2p_epoch(int* epoch, int add, cudaStream_t s) {
+  p2p_epoch_kernel<<<1, 1, 0, s>>>(epoch, add);
   SPB_CUDA(cudaGetLastError());
 }
 

@@ -104,6 +104,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "spb_time_train_steps": (i, [vp, u64, i, i, i, fp]),
         "spb_bucket_plan": (i, [i, i, i, i, ip, ip, ip]),
         "spb_set_fused_update": (i, [vp, i]),
+        "spb_set_chain": (i, [vp, i]),
+        "spb_trace_steps": (i, [vp, u64, i, i, i, i, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong), ip, ip, ip,
+                                ip]),
         "spb_comm_mode": (i, [vp, ip]),
         "spb_comm_selftest": (i, [vp, C.POINTER(C.c_longlong)]),
         "spb_comm_bench": (i, [vp, C.c_longlong, i]),
@@ -125,6 +128,7 @@ EXPORTED = [
     "spb_step_host", "spb_loss", "spb_synchronize", "spb_stream", "spb_comm_unique_id", "spb_comm_init",
     "spb_last_batch", "spb_launches_per_step", "spb_make_random_chain_mlp",
     "spb_get_grads", "spb_profile_step", "spb_time_train_steps", "spb_bucket_plan", "spb_set_fused_update",
+    "spb_set_chain", "spb_trace_steps",
     "spb_comm_mode", "spb_comm_selftest", "spb_comm_bench", "spb_profile_task",
     "spb_empirical_variance", "spb_create_conv",
 ]
@@ -359,6 +363,29 @@ class ChainMlp:
         epilogue, 2 (the default) inside the cheap (<= 512-row) wgrads only."""
         _check(load_library().spb_set_fused_update(self._ctx, int(fused)), self._ctx)
 
+    def set_chain(self, steps: int):
+        """Steps captured per CUDA graph by train_steps (1..16): step t+1's
+        forward of layer l waits only for W_l of step t, so the exchange /
+        update tail of a step overlaps the next forward. Same results."""
+        _check(load_library().spb_set_chain(self._ctx, int(steps)), self._ctx)
+
+    def trace_steps(self, seed: int, step0: int, steps: int, full_backprop: bool = False) -> dict:
+        """Per-op timeline of `steps` chained iterations replayed from one
+        graph (spb_trace_steps): arrays t0 / t1 (ns, relative), cls, stream,
+        sub. Advances the parameters by 2 * steps iterations."""
+        cap = 1 << 15
+        tb = np.zeros(cap, np.int64)
+        te = np.zeros(cap, np.int64)
+        cl, stv, sb = (np.zeros(cap, np.int32) for _ in range(3))
+        n = C.c_int(0)
+        lib = load_library()
+        lp = C.POINTER(C.c_longlong)
+        _check(lib.spb_trace_steps(self._ctx, seed, step0, steps, int(full_backprop), cap, tb.ctypes.data_as(lp),
+                                   te.ctypes.data_as(lp), _ip(cl), _ip(stv), _ip(sb), C.byref(n)), self._ctx)
+        k = min(n.value, cap)
+        t0 = tb[:k].min() if k else 0
+        return {"t0": tb[:k] - t0, "t1": te[:k] - t0, "cls": cl[:k], "stream": stv[:k], "sub": sb[:k]}
+
     def set_optimizer(self, lr: float, momentum: float = 0.0, weight_decay: float = 0.0):
         _check(load_library().spb_set_optimizer(self._ctx, lr, momentum, weight_decay), self._ctx)
 
@@ -415,10 +442,10 @@ class ChainMlp:
 
     @property
     def comm_mode(self):
-        """Multi-GPU aggregation mode: "p2p", "rs", "nvls", "nccl" (None before comm_init)."""
+        """Multi-GPU aggregation mode: "push", "p2p", "rs", "nvls", "nccl" (None before comm_init)."""
         v = C.c_int()
         _check(load_library().spb_comm_mode(self._ctx, C.byref(v)), self._ctx)
-        return {0: "nccl", 1: "nvls", 2: "p2p", 3: "rs"}.get(v.value)
+        return {0: "nccl", 1: "nvls", 2: "p2p", 3: "rs", 4: "push"}.get(v.value)
 
     def comm_selftest(self) -> int:
         """Collective NVLS diagnostic; returns the mismatching element count."""

@@ -39,7 +39,7 @@ def _free_port():
 WIDTHS, N, K, BW, LR, SEED, DSEED = [96, 80, 72, 64, 56, 48, 40, 32, 1], 512, 8, 16, 0.05, 11, 5
 
 
-def _rank(rank, world, port, out_dir, full, mode="p2p", mu=0.0, wd=0.0):
+def _rank(rank, world, port, out_dir, full, mode="p2p", mu=0.0, wd=0.0, chain=None, steps=2):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -57,16 +57,18 @@ def _rank(rank, world, port, out_dir, full, mode="p2p", mu=0.0, wd=0.0):
     m.comm_init_torch(dist, rank, world)
     assert m.comm_mode == mode
     m.set_optimizer(LR, mu, wd)
+    if chain is not None:
+        m.set_chain(chain)
     m.train_steps(SEED, 1, 1, full_backprop=full)
     idx = m.last_batch(len(spb.rank_workers(K, len(WIDTHS) - 1, rank, world)) * BW)
-    m.train_steps(SEED, 2, 2, full_backprop=full)
+    m.train_steps(SEED, 2, steps, full_backprop=full)
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), idx, *m.get_params())
     dist.barrier()
     m.close()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["p2p", "rs", "nvls", "nccl"])
+@pytest.mark.parametrize("mode", ["push", "p2p", "rs", "nvls", "nccl"])
 @pytest.mark.parametrize("full", [False, True])
 def test_multi_gpu_step_matches_oracle(tmp_path, orc, full, mode):
     world = min(_gpus(), 4)
@@ -110,19 +112,52 @@ def test_multi_gpu_momentum_sharded_matches_nccl(tmp_path):
     import torch.multiprocessing as mp
 
     res = {}
-    for mode in ("p2p", "rs", "nvls", "nccl"):
+    for mode in ("push", "p2p", "rs", "nvls", "nccl"):
         d = tmp_path / mode
         d.mkdir()
         mp.start_processes(_rank_momentum, args=(world, _free_port(), str(d), mode), nprocs=world,
                            start_method="spawn")
         res[mode] = [np.load(d / f"r{r}.npz") for r in range(world)]
     L = len(WIDTHS) - 1
-    for mode in ("p2p", "rs", "nvls"):
+    for l in range(L):  # push and p2p sum the same contributions in the same order
+        for r in range(world):
+            assert np.array_equal(res["push"][r][f"arr_{l + 1}"], res["p2p"][r][f"arr_{l + 1}"])
+    for mode in ("push", "p2p", "rs", "nvls"):
         for l in range(L):
             a, b = res[mode][0][f"arr_{l + 1}"], res["nccl"][0][f"arr_{l + 1}"]
             assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-5
             for r in range(world):
                 assert np.array_equal(res[mode][r][f"arr_{l + 1}"], a)
+
+
+def _rank_chain(rank, world, port, out_dir, mode, chain):
+    _rank(rank, world, port, out_dir, False, mode, 0.9, 1e-3, chain=chain, steps=7)
+
+
+@pytest.mark.parametrize("mode", ["push", "p2p", "nccl"])
+def test_multi_gpu_chained_graph_bitwise(tmp_path, mode):
+    """Cross-step pipelining (spb_set_chain): with 7 iterations captured in one
+    graph, iteration t+1's forward of layer l waits only for W_l of
+    iteration t (its exchange and update) while the rest of iteration t's
+    exchange still runs. Weights must be bit-identical to one graph per
+    iteration and across ranks."""
+    world = min(_gpus(), 4)
+    if world < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import torch.multiprocessing as mp
+
+    res = {}
+    for chain in (1, 8):
+        d = tmp_path / f"c{chain}"
+        d.mkdir()
+        mp.start_processes(_rank_chain, args=(world, _free_port(), str(d), mode, chain), nprocs=world,
+                           start_method="spawn")
+        res[chain] = [np.load(d / f"r{r}.npz") for r in range(world)]
+    for l in range(len(WIDTHS) - 1):
+        a = res[1][0][f"arr_{l + 1}"]
+        for r in range(world):
+            assert np.array_equal(res[8][r][f"arr_{l + 1}"], a)
+            assert np.array_equal(res[1][r][f"arr_{l + 1}"], a)
 
 
 def _rank_selftest(rank, world, port, out_dir):

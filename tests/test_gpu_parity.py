@@ -366,3 +366,48 @@ def test_aggregate_repeated_calls_are_exact():
                 assert np.allclose(got[l], want, rtol=1e-6, atol=1e-7)
     finally:
         m.close()
+
+
+@pytest.mark.parametrize("fused", [0, 2])
+@pytest.mark.parametrize("full", [False, True])
+def test_chained_graph_bitwise_equals_single_steps(fused, full):
+    """spb_set_chain: up to 16 iterations captured in one graph, iteration
+    t+1's forward of layer l gated only on W_l of iteration t. Same kernels,
+    same data order: weights and per-step losses must be bit-identical to one
+    graph per iteration, over 11 steps (chunks 8 + 3) with momentum + wd."""
+    widths, N, k, bw = [96, 128, 80, 64, 1], 512, 4, 16
+    ms = []
+    for chain in (1, 8):
+        m, *_ = make(widths, N, 4, k=k, bw=bw)
+        m.set_optimizer(0.05, 0.9, 1e-3)
+        m.set_fused_update(fused)
+        m.set_chain(chain)
+        ms.append((m, m.train_steps(13, 1, 11, full_backprop=full, losses=True)))
+    (a, la), (b, lb) = ms
+    assert np.array_equal(la, lb)
+    for x, y in zip(a.get_params(), b.get_params()):
+        assert np.array_equal(x, y)
+
+
+def test_set_chain_rejects_bad_values():
+    m, *_ = make([8, 8, 1], 16, 1, k=1, bw=4)
+    for bad in (0, 17, -1):
+        with pytest.raises(spb.ArgumentError):
+            m.set_chain(bad)
+
+
+def test_trace_steps_timeline_and_results():
+    """spb_trace_steps replays a traced chained graph twice: every op gets a
+    begin <= end stamp, and the parameters equal 2 * steps untraced steps."""
+    widths, N, k, bw = [64, 96, 48, 1], 256, 4, 8
+    a, *_ = make(widths, N, 6, k=k, bw=bw)
+    b, *_ = make(widths, N, 6, k=k, bw=bw)
+    for m in (a, b):
+        m.set_optimizer(0.05, 0.9, 1e-3)
+    tr = a.trace_steps(3, 1, 3)
+    b.train_steps(3, 1, 6)
+    assert len(tr["t0"]) > 10 and (tr["t1"] >= tr["t0"]).all()
+    assert set(np.unique(tr["sub"])) == {0, 1, 2}
+    assert (tr["cls"] == 0).sum() == 3 * (len(widths) - 2)  # forward GEMMs
+    for x, y in zip(a.get_params(), b.get_params()):
+        assert np.array_equal(x, y)
