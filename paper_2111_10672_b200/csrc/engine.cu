@@ -1588,10 +1588,12 @@ struct Engine {
       try {
         for (int t = 0; t < nsub; ++t) n += enqueue_step(full, host_rows, st, t, nsub);
       } catch (...) {
+        fwd_wait.clear();
         cudaStreamEndCapture(st, &gr);
         graphs.erase(std::make_tuple(full, host_rows, nsub));
         throw;
       }
+      fwd_wait.clear();  // its events belong to this capture
       SPB_CUDA(cudaStreamEndCapture(st, &gr));
       cudaGraphExec_t g = nullptr;
       cudaError_t e = cudaGraphInstantiate(&g, gr, 0);
@@ -2071,7 +2073,9 @@ spb_status spb_profile_step(spb_ctx* ctx, uint64_t seed, int step, int full_back
     SPB_CUDA(cudaEventRecord(a, e.st));
     try {
       e.enqueue_step(full_backprop != 0, false, e.st);
+      e.fwd_wait.clear();
     } catch (...) {
+      e.fwd_wait.clear();
       e.prof = nullptr;
       e.concurrent = true;
       throw;

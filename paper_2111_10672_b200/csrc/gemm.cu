@@ -129,7 +129,7 @@ void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cud
 }
 
 template <bool AM, bool BM_, int EPI, int PN>
-void launch_2sm_pn(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
+void launch_2sm_pn(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, int splits = 1) {
   using Cfg = Gemm2smCfg<PN>;
   auto kern = gemm_tf32x3_2sm_kernel<AM, BM_, EPI, PN>;
   static bool configured = false;
@@ -142,34 +142,50 @@ void launch_2sm_pn(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
   const int num_kb = (A.k + kBK - 1) / kBK;
   const int num_m = (A.mn + 255) / 256, num_n = (B.mn + Cfg::kPairN - 1) / Cfg::kPairN;
   const int tiles = num_m * num_n;
+  if (splits > 1 && EPI != kEpiStoreScaled) throw std::invalid_argument("gemm: pair split-K needs kEpiStoreScaled");
+  const int kbs = (num_kb + splits - 1) / splits;
+  const int units = tiles * ((num_kb + kbs - 1) / kbs);
   const int pairs = num_sms() / 2;
-  const int clusters = tiles < pairs ? tiles : pairs;
-  kern<<<2 * clusters, Cfg::kThreads, Cfg::kSmem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, ep);
+  const int clusters = units < pairs ? units : pairs;
+  kern<<<2 * clusters, Cfg::kThreads, Cfg::kSmem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, ep);
   SPB_CUDA(cudaGetLastError());
 }
 
-// Pair-tile N: 240 when it turns a partial last wave into a full one.
-int pair_n_for(int M, int N) {
-  const int pairs = num_sms() / 2;
-  auto waves = [&](int pn) {
-    const long t = static_cast<long>((M + 255) / 256) * ((N + pn - 1) / pn);
-    return static_cast<double>((t + pairs - 1) / pairs) * pn;  // ~ time: waves x per-tile width
-  };
-  return waves(240) < waves(256) ? 240 : 256;
+// Pair-tile widths with instantiated kernels. 240 / 256 for every operand
+// layout and epilogue; 192 for the MLP's three GEMM shapes (forward K x K,
+// dgrad K x MN, wgrad MN x MN) and split-K partials. (64 and 128 were
+// measured too: they never beat these on the SPB shapes.)
+constexpr int kPairNs[] = {192, 240, 256};
+
+template <bool AM, bool BM_, int EPI>
+constexpr bool narrow_ok() {
+  return (!AM && !BM_ && (EPI == kEpiFwdTanh || EPI == kEpiFwdLinear || EPI == kEpiStoreScaled)) ||
+         (!AM && BM_ && (EPI == kEpiDgradTanh || EPI == kEpiStoreScaled)) || (AM && BM_ && EPI == kEpiStoreScaled);
 }
 
 template <bool AM, bool BM_, int EPI>
-void launch_2sm(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
-  if (pair_n_for(A.mn, B.mn) == 240) launch_2sm_pn<AM, BM_, EPI, 240>(A, B, ep, s);
-  else launch_2sm_pn<AM, BM_, EPI, 256>(A, B, ep, s);
+void launch_2sm(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, int pn, int splits) {
+  if constexpr (narrow_ok<AM, BM_, EPI>()) {
+    if (pn == 192) return launch_2sm_pn<AM, BM_, EPI, 192>(A, B, ep, s, splits);
+  }
+  if (pn == 240) return launch_2sm_pn<AM, BM_, EPI, 240>(A, B, ep, s, splits);
+  if (pn == 256) return launch_2sm_pn<AM, BM_, EPI, 256>(A, B, ep, s, splits);
+  throw std::invalid_argument("gemm: no pair kernel for this tile width / layout");
 }
 
 template <int EPI>
-void dispatch_2sm(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
-  if (!A.mn_major && !B.mn_major) launch_2sm<false, false, EPI>(A, B, ep, s);
-  else if (!A.mn_major && B.mn_major) launch_2sm<false, true, EPI>(A, B, ep, s);
-  else if (A.mn_major && !B.mn_major) launch_2sm<true, false, EPI>(A, B, ep, s);
-  else launch_2sm<true, true, EPI>(A, B, ep, s);
+void dispatch_2sm(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, int pn, int splits = 1) {
+  if (!A.mn_major && !B.mn_major) launch_2sm<false, false, EPI>(A, B, ep, s, pn, splits);
+  else if (!A.mn_major && B.mn_major) launch_2sm<false, true, EPI>(A, B, ep, s, pn, splits);
+  else if (A.mn_major && !B.mn_major) launch_2sm<true, false, EPI>(A, B, ep, s, pn, splits);
+  else launch_2sm<true, true, EPI>(A, B, ep, s, pn, splits);
+}
+
+bool narrow_pair_ok(const Operand& A, const Operand& B, int epi) {
+  if (!A.mn_major && !B.mn_major) return epi == kEpiFwdTanh || epi == kEpiFwdLinear || epi == kEpiStoreScaled;
+  if (!A.mn_major && B.mn_major) return epi == kEpiDgradTanh || epi == kEpiStoreScaled;
+  if (A.mn_major && B.mn_major) return epi == kEpiStoreScaled;
+  return false;
 }
 
 // Split-K fixup: sum the per-split fp32 partials (in split order, so the
@@ -186,8 +202,16 @@ __global__ void splitk_fixup_kernel(const float* __restrict__ ws, int splits, lo
   }
 }
 
+// Launch plan: the 1-CTA 128x128 kernel or the CTA-pair 256 x pn kernel,
+// with `splits` K-splits (fp32 partials + deterministic fixup) when > 1.
+struct Plan {
+  bool two_sm;
+  int splits;
+  int pn;
+};
+
 template <int EPI>
-void launch_splitk(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, int splits) {
+void launch_splitk(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, const Plan& plan) {
   const long ldw = round_up(B.mn, 4), stride = static_cast<long>(A.mn) * ldw;
   GemmEpilogue part{};
   part.out_hi = ep.splitk_ws;
@@ -196,7 +220,11 @@ void launch_splitk(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
   part.M = A.mn;
   part.N = B.mn;
   part.split_stride = stride;
-  if (!A.mn_major && !B.mn_major) launch_inst<128, false, false, kEpiStoreScaled>(A, B, part, s, splits);
+  // Splits actually populated: ceil(kb / ceil(kb / splits)) can be < splits.
+  const int kb = (A.k + kBK - 1) / kBK, kbs = (kb + plan.splits - 1) / plan.splits;
+  const int splits = (kb + kbs - 1) / kbs;
+  if (plan.two_sm) dispatch_2sm<kEpiStoreScaled>(A, B, part, s, plan.pn, splits);
+  else if (!A.mn_major && !B.mn_major) launch_inst<128, false, false, kEpiStoreScaled>(A, B, part, s, splits);
   else if (!A.mn_major && B.mn_major) launch_inst<128, false, true, kEpiStoreScaled>(A, B, part, s, splits);
   else if (A.mn_major && !B.mn_major) launch_inst<128, true, false, kEpiStoreScaled>(A, B, part, s, splits);
   else launch_inst<128, true, true, kEpiStoreScaled>(A, B, part, s, splits);
@@ -206,46 +234,59 @@ void launch_splitk(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
   SPB_CUDA(cudaGetLastError());
 }
 
-int g_force_variant = -1;  // -1 auto, 0 = 1-CTA 128x128, 1 = CTA pair 256x256
+int g_force_variant = -1;  // -1 auto, 0 = 1-CTA 128x128, 1 = CTA pair
+Plan g_force_plan{false, 0, 0};  // splits == 0: not forced
 
-// Launch plan: the 1-CTA kernel with `splits` K-splits, or the CTA-pair
-// kernel. Wave-quantised cost model (microseconds) calibrated on B200 with
-// tests/native/gemm_bench.cu: a 1-CTA 128x128 work unit costs
-// 0.62 us per k-block + 2.8 us; a 256x256 pair tile 1.07 us per k-block +
-// 7 us on 2 SMs (recalibrated: the pair loses the SPB wgrad shapes with
-// K <= 512 to the 1-CTA kernel by 8-19 %); a split-K fixup streams
-// (splits + 2) M x N floats.
-struct Plan {
-  bool two_sm;
-  int splits;
-};
-
-int pair_n_for(int M, int N);
-
-Plan plan_gemm(int M, int N, int K, long ws_floats, bool can_split) {
+// Wave-quantised cost model (microseconds), fitted on B200 to the plan
+// sweep of tests/native/gemm_bench.cu (`gemm_bench 10 sweep`: every plan on
+// the SPB forward / dgrad / wgrad shapes at 1, 2 and 4 GPUs; 7.6 % rms; its
+// choice is within 1 % of the best measured plan summed over the shapes):
+//  - 1-CTA 128 x 128 unit: 0.638 us per 32-deep k-block + 1.41 us
+//    (0.31 us per k-block for N <= 64 tiles);
+//  - pair 256 x pn unit (2 SMs): 1.01 us x pe / 256 per k-block + 1.01 us +
+//    4.24 us x pn / 256, pe = the B rows actually loaded (MN-major B comes in
+//    32-row boxes: pn 240 loads 256 when A is MN-major too);
+//  - split-K: + 3.0 us + (splits + 2) M N fp32 streamed at 3.17 TB/s (fixup;
+//    the constant is the old small-shape calibration, the slope the new fit).
+Plan plan_gemm(int M, int N, int K, long ws_floats, bool can_split, bool narrow_ok, bool allow_pair = true,
+               bool both_mn = false) {
   const int sms = num_sms();
   const int kb = (K + kBK - 1) / kBK;
   const long t1 = static_cast<long>((M + 127) / 128) * ((N + 127) / 128);
-  const long t2 = static_cast<long>((M + 255) / 256) * ((N + 255) / 256);
-  if (g_force_variant >= 0) return {g_force_variant == 1, 1};
-  Plan best{false, 1};
+  if (allow_pair && g_force_plan.splits > 0) return g_force_plan;
+  if (g_force_variant >= 0) return {allow_pair && g_force_variant == 1, 1, 256};
+  Plan best{false, 1, 256};
   double best_t = 1e30;
+  auto fixup = [&](int sp) { return sp > 1 ? 3.0 + (sp + 2.0) * M * static_cast<double>(N) * 4.0 / 3.17e6 : 0.0; };
+  auto split_ok = [&](int sp) {
+    return sp == 1 || (can_split && static_cast<long>(sp) * M * round_up(N, 4) <= ws_floats && kb >= 8 * sp);
+  };
   // Split counts: up to 8 for the MLP shapes; far more for the few-tile,
   // huge-K wgrad GEMMs of the conv model (K = pixel rows, up to ~1M).
   static const int kSplits[] = {1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 32, 48, 64, 96, 128, 148, 192, 256, 296};
   for (int sp : kSplits) {
-    if (sp > 1 && (!can_split || static_cast<long>(sp) * M * round_up(N, 4) > ws_floats || kb < 8 * sp)) break;
-    const int kbs = (kb + sp - 1) / sp;
-    const long units = t1 * ((kb + kbs - 1) / kbs);
-    double t = static_cast<double>((units + sms - 1) / sms) * ((N <= 64 && sp == 1 ? 0.31 : 0.62) * kbs + 2.8);
-    if (sp > 1) t += 3.0 + (sp + 2.0) * M * static_cast<double>(N) * 4.0 / 4.0e6;
-    if (t < best_t) best_t = t, best = {false, sp};
+    if (!split_ok(sp)) break;
+    const int kbs = (kb + sp - 1) / sp, eff = (kb + kbs - 1) / kbs;
+    const long units = t1 * eff;
+    const double t =
+        static_cast<double>((units + sms - 1) / sms) * ((N <= 64 && sp == 1 ? 0.31 : 0.638) * kbs + 1.41) + fixup(eff);
+    if (t < best_t) best_t = t, best = {false, sp, 256};
   }
-  const int pn = pair_n_for(M, N);
-  const long t2n = static_cast<long>((M + 255) / 256) * ((N + pn - 1) / pn);
-  (void)t2;
-  const double t_two = static_cast<double>((t2n + sms / 2 - 1) / (sms / 2)) * (1.07 * kb + 7.0) * pn / 256.0;
-  if (t_two < best_t) best = {true, 1};
+  const int pairs = sms / 2;
+  for (int pn : kPairNs) {
+    if (!allow_pair) break;
+    if (pn < 240 && !narrow_ok) continue;
+    const int pe = both_mn ? 64 * ((pn + 63) / 64) : pn;
+    for (int sp : {1, 2, 3, 4, 6, 8}) {
+      if (!split_ok(sp)) break;
+      const int kbs = (kb + sp - 1) / sp, eff = (kb + kbs - 1) / kbs;
+      const long units = static_cast<long>((M + 255) / 256) * ((N + pn - 1) / pn) * eff;
+      const double t = static_cast<double>((units + pairs - 1) / pairs) *
+                           (1.01 * pe / 256.0 * kbs + 1.01 + 4.24 * pn / 256.0) +
+                       fixup(eff);
+      if (t < best_t) best_t = t, best = {true, sp, pn};
+    }
+  }
   return best;
 }
 
@@ -260,6 +301,8 @@ void dispatch_major(const Operand& A, const Operand& B, const GemmEpilogue& ep, 
 }  // namespace
 
 void gemm_force_variant(int v) { g_force_variant = v; }
+
+void gemm_force_plan(int two_sm, int pn, int splits) { g_force_plan = {two_sm != 0, splits, pn}; }
 
 int gemm_conv_fwd(const ConvSrc& src, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
   const ConvGeom& g = src.g;
@@ -303,7 +346,8 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
                       im2col_map(src.lo, src, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)};
   const ConvTmaArgs ic{g.out_h * g.out_w, g.out_w, g.stride, g.c_in, pixel0, 0};
   Operand B{nullptr, nullptr, 4, N, A.k, true};  // shape only
-  const Plan plan = plan_gemm(A.mn, N, A.k, ep.splitk_ws ? ep.splitk_ws_floats : 0, ep.splitk_ws != nullptr);
+  const Plan plan = plan_gemm(A.mn, N, A.k, ep.splitk_ws ? ep.splitk_ws_floats : 0, ep.splitk_ws != nullptr, false,
+                              false);  // the im2col-B wgrad has a 1-CTA kernel only
   if (plan.splits > 1) {
     const long ldw = round_up(N, 4), stride = static_cast<long>(A.mn) * ldw;
     GemmEpilogue part{};
@@ -316,7 +360,8 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
     launch_inst<128, true, true, kEpiStoreScaled, false, 2>(A, B, part, s, plan.splits, nullptr, b, ic);
     const long n = static_cast<long>(A.mn) * N;
     const int grid = static_cast<int>(std::min<long>((n + 255) / 256, 148L * 16));
-    splitk_fixup_kernel<kEpiStoreScaled><<<grid, 256, 0, s>>>(ep.splitk_ws, plan.splits, stride, ldw, ep);
+    const int kb = (A.k + kBK - 1) / kBK, kbs = (kb + plan.splits - 1) / plan.splits;
+    splitk_fixup_kernel<kEpiStoreScaled><<<grid, 256, 0, s>>>(ep.splitk_ws, (kb + kbs - 1) / kbs, stride, ldw, ep);
     SPB_CUDA(cudaGetLastError());
     return 2;
   }
@@ -333,15 +378,16 @@ int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue&
   if ((A.ld % 4) || (B.ld % 4)) throw std::invalid_argument("gemm: ld must be a multiple of 4");
   constexpr int BN = 128;
   static const bool no_split = std::getenv("SPB_NO_SPLITK") != nullptr;  // tuning experiments
-  const Plan plan = plan_gemm(A.mn, B.mn, A.k, ep.splitk_ws && !no_split ? ep.splitk_ws_floats : 0,
-                              ep.splitk_ws != nullptr && (epi == kEpiFwdTanh || epi == kEpiDgradTanh ||
-                                                          epi == kEpiFwdLinear || epi == kEpiStoreScaled));
+  const bool can_split = ep.splitk_ws != nullptr && (epi == kEpiFwdTanh || epi == kEpiDgradTanh ||
+                                                     epi == kEpiFwdLinear || epi == kEpiStoreScaled);
+  const Plan plan = plan_gemm(A.mn, B.mn, A.k, ep.splitk_ws && !no_split ? ep.splitk_ws_floats : 0, can_split,
+                              narrow_pair_ok(A, B, epi), true, A.mn_major && B.mn_major);
   if (plan.splits > 1) {
     switch (epi) {
-      case kEpiFwdTanh: launch_splitk<kEpiFwdTanh>(A, B, ep, s, plan.splits); break;
-      case kEpiDgradTanh: launch_splitk<kEpiDgradTanh>(A, B, ep, s, plan.splits); break;
-      case kEpiFwdLinear: launch_splitk<kEpiFwdLinear>(A, B, ep, s, plan.splits); break;
-      case kEpiStoreScaled: launch_splitk<kEpiStoreScaled>(A, B, ep, s, plan.splits); break;
+      case kEpiFwdTanh: launch_splitk<kEpiFwdTanh>(A, B, ep, s, plan); break;
+      case kEpiDgradTanh: launch_splitk<kEpiDgradTanh>(A, B, ep, s, plan); break;
+      case kEpiFwdLinear: launch_splitk<kEpiFwdLinear>(A, B, ep, s, plan); break;
+      case kEpiStoreScaled: launch_splitk<kEpiStoreScaled>(A, B, ep, s, plan); break;
       default: throw std::invalid_argument("gemm: split-K not supported for this epilogue");
     }
     return 2;
@@ -353,12 +399,13 @@ int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue&
     return 1;
   }
   if (plan.two_sm) {
+    const int pn = epi == kEpiWgradUpdate && plan.pn < 240 ? 256 : plan.pn;
     switch (epi) {
-      case kEpiFwdTanh: dispatch_2sm<kEpiFwdTanh>(A, B, ep, s); break;
-      case kEpiStoreScaled: dispatch_2sm<kEpiStoreScaled>(A, B, ep, s); break;
-      case kEpiDgradTanh: dispatch_2sm<kEpiDgradTanh>(A, B, ep, s); break;
-      case kEpiFwdLinear: dispatch_2sm<kEpiFwdLinear>(A, B, ep, s); break;
-      case kEpiWgradUpdate: launch_2sm<true, true, kEpiWgradUpdate>(A, B, ep, s); break;
+      case kEpiFwdTanh: dispatch_2sm<kEpiFwdTanh>(A, B, ep, s, pn); break;
+      case kEpiStoreScaled: dispatch_2sm<kEpiStoreScaled>(A, B, ep, s, pn); break;
+      case kEpiDgradTanh: dispatch_2sm<kEpiDgradTanh>(A, B, ep, s, pn); break;
+      case kEpiFwdLinear: dispatch_2sm<kEpiFwdLinear>(A, B, ep, s, pn); break;
+      case kEpiWgradUpdate: launch_2sm<true, true, kEpiWgradUpdate>(A, B, ep, s, pn, 1); break;
       default: throw std::invalid_argument("gemm: bad epilogue");
     }
     return 1;

@@ -21,8 +21,11 @@
 
 namespace spb {
 
-// PN: the pair tile's N (256, or 240 so that e.g. 4096 columns make 18 tiles
-// and a 1024-row forward fills 72 of the 74 SM pairs in one wave).
+// PN: the pair tile's N (a multiple of 16 in [64, 256]): 256 for large
+// outputs, 240 so that e.g. 4096 columns make 18 tiles and a 1024-row forward
+// fills 72 of the 74 SM pairs in one wave, and 64 / 128 / 192 so that the
+// few-row GEMMs (the multi-GPU forward, the SPB dgrads) fill a wave instead of
+// leaving half the SM pairs idle (the host planner picks by wave-quantised cost).
 template <int PN = 256>
 struct Gemm2smCfg {
   static constexpr int kRowsA = 128;      // per CTA
@@ -53,7 +56,8 @@ template <bool A_MN, bool B_MN, int EPI, int PN = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
     gemm_tf32x3_2sm_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                            const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
-                           int num_kb, int num_m_pairs, int num_tiles, const __grid_constant__ GemmEpilogue ep) {
+                           int num_kb, int num_m_pairs, int num_tiles, int kb_per_split, int num_units,
+                           const __grid_constant__ GemmEpilogue ep) {
   using Cfg = Gemm2smCfg<PN>;
   // TMA bytes one CTA brings per k-block (A hi/lo + B hi/lo).
   constexpr uint32_t kBLoaded = B_MN ? ((Cfg::kRowsB + 31) / 32) * 4096 : Cfg::kRowsB * 128;
@@ -71,7 +75,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
   const uint32_t cta = cluster_ctarank();
   const bool leader = cta == 0;
   const int cluster_id = static_cast<int>(blockIdx.x >> 1), nclusters = static_cast<int>(gridDim.x >> 1);
-  const int num_chunks = (num_kb + kChunkKb - 1) / kChunkKb;
+  // Work unit u -> pair tile u % num_tiles, K-split u / num_tiles (split-K:
+  // kEpiStoreScaled partials at out_hi + split * split_stride, summed by the
+  // host launcher's fixup kernel).
+  // Only kEpiStoreScaled instantiations take K-splits (the partials); the
+  // others compile to the plain tile loop (registers are tight at 96/thread).
+  constexpr bool kSplit = EPI == kEpiStoreScaled;
+  auto unit = [&](int u, int& t, int& kb0, int& kb1, int& split) {
+    if constexpr (kSplit) {
+      t = u % num_tiles;
+      split = u / num_tiles;
+      kb0 = split * kb_per_split;
+      kb1 = min(num_kb, kb0 + kb_per_split);
+    } else {
+      t = u, split = 0, kb0 = 0, kb1 = num_kb;
+    }
+  };
 
   if (warp == 0 && elect_one()) {
     tma_prefetch(&ta_hi);
@@ -100,10 +119,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
     if (warp == 0) {
       if (elect_one()) {
         int it = 0;
-        for (int t = cluster_id; t < num_tiles; t += nclusters) {
+        for (int u = cluster_id; u < num_units; u += nclusters) {
+          int t, kb0, kb1, split;
+          unit(u, t, kb0, kb1, split);
           const int m0 = (t % num_m_pairs) * 256 + static_cast<int>(cta) * Cfg::kRowsA;
           const int n0 = (t / num_m_pairs) * Cfg::kPairN + static_cast<int>(cta) * Cfg::kRowsB;
-          for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          for (int kb = kb0; kb < kb1; ++kb, ++it) {
             const int s = it % Cfg::kStages;
             const uint32_t ph = (it / Cfg::kStages) & 1u;
             mbar_wait(&empty_bar[s], ph ^ 1u);
@@ -121,14 +142,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       if (elect_one()) {
         constexpr uint32_t idesc = idesc_tf32(256, Cfg::kPairN, A_MN, B_MN);
         int it = 0, g = 0;
-        for (int t = cluster_id; t < num_tiles; t += nclusters) {
+        for (int u = cluster_id; u < num_units; u += nclusters) {
+          int t, kb0, kb1, split;
+          unit(u, t, kb0, kb1, split);
+          const int num_chunks = (kb1 - kb0 + kChunkKb - 1) / kChunkKb;
           for (int c = 0; c < num_chunks; ++c, ++g) {
             const uint32_t b = g & 1, tph = (g >> 1) & 1;
             mbar_wait(&tempty_bar[b], tph ^ 1u);  // both CTAs' epilogues drained buffer b
             tc_fence_after();
             const uint32_t acc_addr = tmem + b * Cfg::kPairN;
-            const int kb_end = min(num_kb, (c + 1) * kChunkKb);
-            for (int kb = c * kChunkKb; kb < kb_end; ++kb, ++it) {
+            const int kb_beg = kb0 + c * kChunkKb, kb_end = min(kb1, kb_beg + kChunkKb);
+            for (int kb = kb_beg; kb < kb_end; ++kb, ++it) {
               const int s = it % Cfg::kStages;
               const uint32_t ph = (it / Cfg::kStages) & 1u;
               mbar_wait(&full_bar[s], ph);
@@ -138,7 +162,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
               const uint32_t b_hi = base + 2 * Cfg::kABytes, b_lo = b_hi + Cfg::kBBytes;
 #pragma unroll
               for (int kk = 0; kk < kBK / 8; ++kk) {
-                const uint32_t acc = (kb != c * kChunkKb) || kk != 0;
+                const uint32_t acc = (kb != kb_beg) || kk != 0;
                 umma_tf32_2sm(acc_addr, operand_desc<A_MN>(a_lo, kk), operand_desc<B_MN>(b_hi, kk), idesc, acc);
                 umma_tf32_2sm(acc_addr, operand_desc<A_MN>(a_hi, kk), operand_desc<B_MN>(b_lo, kk), idesc, 1u);
                 umma_tf32_2sm(acc_addr, operand_desc<A_MN>(a_hi, kk), operand_desc<B_MN>(b_hi, kk), idesc, 1u);
@@ -158,7 +182,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
     const uint32_t lane_addr = (q * 32u) << 16;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     int g = 0;
-    for (int t = cluster_id; t < num_tiles; t += nclusters) {
+    for (int u = cluster_id; u < num_units; u += nclusters) {
+      int t, kb0, kb1, split;
+      unit(u, t, kb0, kb1, split);
+      const int num_chunks = (kb1 - kb0 + kChunkKb - 1) / kChunkKb;
+      const long out_shift = EPI == kEpiStoreScaled ? split * ep.split_stride : 0;
       const int m0 = (t % num_m_pairs) * 256 + static_cast<int>(cta) * Cfg::kRowsA;
       const int n_pair0 = (t / num_m_pairs) * Cfg::kPairN;
       const int n0 = n_pair0 + colbase;
@@ -185,7 +213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       const int row = m0 + static_cast<int>(q * 32 + lane);
 #pragma unroll
       for (int c0 = 0; c0 < Cfg::kEpiCols; c0 += 32)
-        if (n0 + c0 < n_lim) epilogue_chunk<EPI>(ep, acc + c0, row, n0 + c0, 0, n_lim);
+        if (n0 + c0 < n_lim) epilogue_chunk<EPI>(ep, acc + c0, row, n0 + c0, out_shift, n_lim);
     }
   }
   tc_fence_before();

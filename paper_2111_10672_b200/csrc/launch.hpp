@@ -61,6 +61,9 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
 int gemm_conv_dgrad(const ConvSrc& src, long pixel0, int rows, const Operand& B, const GemmEpilogue& ep, cudaStream_t s);
 // Test hook: -1 automatic choice, 0 force 1-CTA, 1 force CTA pair.
 void gemm_force_variant(int v);
+// Tuning aid: force every GEMM onto one plan (two_sm: CTA-pair kernel of
+// width pn; splits K-splits); splits = 0 restores the planner.
+void gemm_force_plan(int two_sm, int pn, int splits);
 // Persistent GEMM grids leave n SMs free (for NCCL kernels running beside them).
 void gemm_reserve_sms(int n);
 

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <string>
 #include <vector>
 
 #include "../../paper_2111_10672_b200/csrc/gemm_tf32x3.cuh"
@@ -23,10 +24,27 @@ int main(int argc, char** argv) {
     int epi;
   };
   std::vector<Shape> shapes;
-  shapes.push_back({"fwd", 1024, 4096, 4096, false, false, kEpiFwdTanh});
-  for (int q : {1, 2, 3, 4, 7}) shapes.push_back({"dgrad", 128 * q, 4096, 4096, false, true, kEpiDgradTanh});
-  for (int m : {1, 2, 4, 8}) shapes.push_back({"wgrad", 4096, 4096, 128 * m, true, true, kEpiStoreScaled});
-  for (int m : {1, 4, 8}) shapes.push_back({"wgupd", 4096, 4096, 128 * m, true, true, kEpiWgradUpdate});
+  const bool sweep = argc > 2 && std::string(argv[2]) == "sweep";
+  if (sweep) {  // plan sweep over the SPB shapes at 1 / 2 / 4 GPUs (planner calibration)
+    for (int m : {256, 512, 1024}) shapes.push_back({"fwd", m, 4096, 4096, false, false, kEpiFwdTanh});
+    for (int q : {1, 2, 3, 4, 5, 6, 7}) shapes.push_back({"dgrad", 128 * q, 4096, 4096, false, true, kEpiDgradTanh});
+    for (int q : {1, 2, 3, 4, 5, 6, 8}) shapes.push_back({"wgrad", 4096, 4096, 128 * q, true, true, kEpiStoreScaled});
+  } else {
+    shapes.push_back({"fwd", 1024, 4096, 4096, false, false, kEpiFwdTanh});
+    for (int q : {1, 2, 3, 4, 7}) shapes.push_back({"dgrad", 128 * q, 4096, 4096, false, true, kEpiDgradTanh});
+    for (int m : {1, 2, 4, 8}) shapes.push_back({"wgrad", 4096, 4096, 128 * m, true, true, kEpiStoreScaled});
+    for (int m : {1, 4, 8}) shapes.push_back({"wgupd", 4096, 4096, 128 * m, true, true, kEpiWgradUpdate});
+  }
+  struct P {
+    int two, pn, sp;
+  };
+  std::vector<P> plans = {{-1, 0, 0}, {0, 0, 1}, {1, 256, 1}};
+  if (sweep) {
+    plans = {{-1, 0, 0}};
+    for (int sp : {1, 2, 4}) plans.push_back({0, 128, sp});
+    for (int pn : {192, 240, 256})
+      for (int sp : {1, 2, 4}) plans.push_back({1, pn, sp});
+  }
   const long big = 4096L * 4096;
   float *ah, *al, *bh, *bl, *out, *oh, *ol;
   cudaMalloc(&ah, big * 4), cudaMalloc(&al, big * 4), cudaMalloc(&bh, big * 4), cudaMalloc(&bl, big * 4);
@@ -39,8 +57,10 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0), cudaEventCreate(&e1);
   for (auto& sh : shapes) {
-    for (int variant = -1; variant < 2; ++variant) {
-      gemm_force_variant(variant);
+    for (const P& pl : plans) {
+      if (pl.two < 0) gemm_force_plan(0, 0, 0);
+      else gemm_force_plan(pl.two, pl.pn, pl.sp);
+      if (pl.sp > 1 && sh.epi == kEpiWgradUpdate) continue;
       Operand A{ah, al, sh.am ? sh.M : sh.K, sh.M, sh.K, sh.am};
       Operand B{bh, bl, sh.bm ? sh.N : sh.K, sh.N, sh.K, sh.bm};
       GemmEpilogue ep{};
@@ -73,8 +93,11 @@ int main(int argc, char** argv) {
       cudaEventElapsedTime(&ms, e0, e1);
       const double us = 1e3 * ms / reps;
       const double tf = 2.0 * sh.M * sh.N * sh.K / (us * 1e-6) / 1e12;
-      std::printf("%-6s %s M=%5d N=%5d K=%5d  %8.1f us  alg %6.1f TF/s  pipe %7.1f TF/s  %s\n", sh.name,
-                  variant < 0 ? "auto" : variant ? "2sm " : "1sm ", sh.M, sh.N, sh.K, us, tf, 6 * tf, cudaGetErrorString(cudaGetLastError()));
+      char tag[32];
+      if (pl.two < 0) std::snprintf(tag, sizeof tag, "auto");
+      else std::snprintf(tag, sizeof tag, "%s pn=%d sp=%d", pl.two ? "2sm" : "1sm", pl.two ? pl.pn : 128, pl.sp);
+      std::printf("%-6s %-18s M=%5d N=%5d K=%5d  %8.1f us  alg %6.1f TF/s  pipe %7.1f TF/s  %s\n", sh.name, tag, sh.M,
+                  sh.N, sh.K, us, tf, 6 * tf, cudaGetErrorString(cudaGetLastError()));
     }
   }
   return 0;

@@ -77,10 +77,19 @@ int main() {
         for (int q = 0; q < c.K; ++q) s += static_cast<double>(A[static_cast<long>(i) * c.K + q]) * B[static_cast<long>(j) * c.K + q];
         R[static_cast<long>(i) * c.N + j] = s;
       }
-    for (int variant = -1; variant < 2; ++variant)
+    // variant -1 auto, 0 1-CTA, 1 pair 256; >= 2: forced plans (pair tile
+    // widths 192 / 240 / 256, K-splits on both kernels).
+    struct Forced {
+      int two, pn, sp;
+    };
+    const Forced forced[] = {{1, 192, 1}, {1, 192, 3}, {1, 240, 2}, {1, 256, 4}, {0, 128, 3}};
+    for (int variant = -1; variant < 2 + 5; ++variant)
     for (int am = 0; am < 2; ++am)
       for (int bm = 0; bm < 2; ++bm) {
-        gemm_force_variant(variant);
+        if (variant >= 2 && forced[variant - 2].two && forced[variant - 2].pn < 240 && am && !bm) continue;
+        gemm_force_variant(variant < 2 ? variant : -1);
+        if (variant >= 2) gemm_force_plan(forced[variant - 2].two, forced[variant - 2].pn, forced[variant - 2].sp);
+        else gemm_force_plan(0, 0, 0);
         long lda, ldb;
         Dev a = upload(A, c.M, c.K, am, lda), b = upload(B, c.N, c.K, bm, ldb);
         float* out;
@@ -121,13 +130,18 @@ int main() {
             mx = std::max(mx, std::fabs(d));
           }
         const double rel = std::sqrt(num / (den > 0 ? den : 1));
-        std::printf("case %s am=%d bm=%d M=%d N=%d K=%d rel_err=%.3e max_abs=%.3e %s\n", variant < 0 ? "auto" : variant ? "2sm" : "1sm", am, bm,
+        char tag[40];
+        if (variant < 2) std::snprintf(tag, sizeof tag, "%s", variant < 0 ? "auto" : variant ? "2sm" : "1sm");
+        else std::snprintf(tag, sizeof tag, "%s/pn%d/sp%d", forced[variant - 2].two ? "2sm" : "1sm", forced[variant - 2].pn,
+                           forced[variant - 2].sp);
+        std::printf("case %s am=%d bm=%d M=%d N=%d K=%d rel_err=%.3e max_abs=%.3e %s\n", tag, am, bm,
                     c.M, c.N, c.K, rel, mx,
                     e == cudaSuccess ? "" : cudaGetErrorString(e));
         if (!(rel <= 2e-6) || e != cudaSuccess) ++bad;
         cudaFree(a.hi), cudaFree(a.lo), cudaFree(b.hi), cudaFree(b.lo), cudaFree(out);
       }
   }
+  gemm_force_plan(0, 0, 0);
   std::printf("%s\n", bad ? "GEMM PROBE FAILED" : "GEMM PROBE OK");
   return bad ? 1 : 0;
 }
