@@ -174,13 +174,19 @@ struct Engine {
   // fwd_wait[l] = event index the forward of layer l (the head for l = L)
   // must wait on, -1 = none; chain_sub = index of the step being enqueued.
   static constexpr int kMaxChain = 16;
+  // chain = 0: automatic -- 8 on one GPU (measured +1.7 % on cfg3), 1 with a
+  // multi-GPU exchange (the exchange tail running beside the next forward
+  // slowed both: -2 to -7 % at 2 and 4 ranks). SPB_CHAIN / spb_set_chain
+  // override.
   int chain = default_chain();
   int chain_sub = 0;
   static int default_chain() {
     const char* c = std::getenv("SPB_CHAIN");
-    const int v = c ? std::atoi(c) : 8;
+    if (!c) return 0;
+    const int v = std::atoi(c);
     return v < 1 ? 1 : (v > kMaxChain ? kMaxChain : v);
   }
+  int chain_len() const { return chain > 0 ? chain : (comm ? 1 : 8); }
   std::vector<int> fwd_wait;
   std::string err;
   // multi-GPU
@@ -1613,7 +1619,7 @@ struct Engine {
   void run_steps(bool full, int steps, float* losses) {
     int done = 0;
     while (done < steps) {
-      const int c = std::max(1, std::min({chain, kMaxChain, steps - done}));
+      const int c = std::max(1, std::min({chain_len(), kMaxChain, steps - done}));
       cudaGraphExec_t g = get_graph(full, false, c, &last_launches);
       SPB_CUDA(cudaGraphLaunch(g, st));
       if (losses) SPB_CUDA(cudaMemcpyAsync(losses + done, loss_dev, c * sizeof(float), cudaMemcpyDeviceToHost, st));
@@ -2143,7 +2149,7 @@ spb_status spb_time_train_steps(spb_ctx* ctx, uint64_t seed, int step0, int step
     auto& e = ctx->e;
     if (!e.X) throw spb::ConfigError("train_steps: no dataset");
     for (int d = 0; d < steps;) {  // instantiate every graph of the run before timing
-      const int c = std::max(1, std::min({e.chain, Engine::kMaxChain, steps - d}));
+      const int c = std::max(1, std::min({e.chain_len(), Engine::kMaxChain, steps - d}));
       e.get_graph(full_backprop != 0, false, c);
       d += c;
     }
