@@ -200,17 +200,22 @@ SPB_API void* spb_stream(spb_ctx* ctx);
  *  - "rs": NCCL reduce-scatter of each layer's gradient, the optimizer on
  *    this rank's shard, NCCL all-gather of the fp32 weights (a layer with one
  *    contributing rank: that rank updates it and broadcasts the weights);
+ *  - "rh" (power-of-two rank counts; default for 4 and 8): the p2p protocol's buffers with
+ *    Rabenseifner's schedule -- recursive-halving reduce-scatter, the owner's
+ *    update, recursive-doubling all-gather of the fp32 weights -- so every
+ *    copy-engine pull is from ONE peer (single-peer NVLink copies run at
+ *    ~760 GB/s, all-to-all pulls at ~450 GB/s);
  *  - "push": the wgrad GEMM epilogue stores each gradient row straight into
  *    the owning rank's staging slot (NVLink stores through CUDA IPC); the
  *    owner sums its rows, applies the optimizer and stores the new fp32 rows
  *    into every peer; peers split them into (hi, lo). No copy engines, no
  *    NCCL in the step;
- *  - "nccl" (default for more than 2 ranks): per-layer NCCL buckets
+ *  - "nccl" (default for other rank counts): per-layer NCCL buckets
  *    (broadcast / all-reduce), then the local optimizer update on every rank.
  * Ranks of one node only. */
 SPB_API spb_status spb_comm_unique_id(void* out128);
 SPB_API spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int nranks);
-/* Active aggregation mode: 0 nccl, 1 nvls, 2 p2p, 3 rs, 4 push (-1 before spb_comm_init). */
+/* Active aggregation mode: 0 nccl, 1 nvls, 2 p2p, 3 rs, 4 push, 5 rh (-1 before spb_comm_init). */
 SPB_API spb_status spb_comm_mode(spb_ctx* ctx, int* mode);
 /* Collective diagnostic of the NVLS path: multicast reduce + broadcast of a
  * known pattern over all ranks; *mismatches = wrong elements seen here. */

@@ -227,6 +227,7 @@ struct Engine {
   std::vector<int> prpo;
   std::vector<long> pstage_off, pslot;
   std::vector<float*> peer_pstage;
+  int flag_slots = 2;  // flags per layer (p2p / push: 2; rh: 2 log2 N)
   bool route_push = false;  // set while enqueue_step builds a push-mode step
   cudaStream_t s4 = nullptr;
   std::vector<cudaStream_t> gpull, wpull;  // per-peer copy streams (copy engines run concurrently)
@@ -312,7 +313,7 @@ struct Engine {
     if (st) cudaStreamSynchronize(st);
     if (cst) cudaStreamSynchronize(cst);
     invalidate_graphs();
-    if (comm_mode == 2 || comm_mode == 4) {
+    if (comm_mode == 2 || comm_mode == 4 || comm_mode == 5) {
       // Peers may still read this rank's memory until they pass this point.
       if (s3) cudaStreamSynchronize(s3);
       if (s4) cudaStreamSynchronize(s4);
@@ -857,7 +858,9 @@ struct Engine {
     // Fused: wgrad_l updates W_l in place, so it also waits for dgrad_l (the
     // last reader of W_l). Collectives and per-layer updates hang off the
     // events recorded here.
-    const bool two = concurrent;
+    // SPB_SERIAL_BWD=1 (experiment): wgrad on the dgrad stream.
+    static const bool serial_bwd = std::getenv("SPB_SERIAL_BWD") != nullptr;
+    const bool two = concurrent && !serial_bwd;
     if (two) {
       SPB_CUDA(cudaEventRecord(ev(kEvFork), s));
       SPB_CUDA(cudaStreamWaitEvent(s2, ev(kEvFork), 0));
@@ -1101,6 +1104,141 @@ struct Engine {
     return n;
   }
 
+  // "rh" mode (N = 2^d ranks), layer l: Rabenseifner's all-reduce on the
+  // copy engines -- recursive-halving reduce-scatter, the owner's update,
+  // recursive-doubling all-gather of the fp32 weights -- so that every
+  // transfer is a single-peer pull (measured ~760 GB/s per direction over
+  // NVLink, against ~450 GB/s when a GPU pulls from 3 peers at once, the p2p
+  // mode's pattern). Rank r owns shard r of the layer segment (the p2p
+  // sharding). Reduce round k = 0..d-1 (bit b = d-1-k, partner r ^ 2^b): r
+  // keeps the half of its current shard block whose bit b matches its own,
+  // pulls the partner's partial sums of that half and adds them into its own
+  // gradient buffer in place (the partner pulls the other half of r's buffer
+  // meanwhile); the last round feeds the update kernel directly. Partial sums
+  // that cover no contributor of the layer (SPB) are skipped. All-gather
+  // round b = 0..d-1: pull the partner's weight block of 2^b shards. Flags
+  // per layer (slot base 2d*l): +0 gradient final, +1+k reduce round k done
+  // (k < d-1), +d+b weight block of 2^b shards final (b = 0: the update).
+  int enqueue_rh_layer(int l, bool full, cudaStream_t gs, cudaStream_t s) {
+    const Bucket* bk = nullptr;
+    for (auto& b : buckets[full])
+      if (b.l_lo <= l && l <= b.l_hi) bk = &b;
+    if (!bk) throw ConfigError("comm: no bucket for layer");
+    unsigned contrib = 0;
+    for (int r : bk->ranks) contrib |= 1u << r;
+    const int d = flag_slots / 2;
+    const long off = w_off[l], cnt = b_off[l] + round_up(w[l], 32) - w_off[l], n4 = cnt / 4;
+    auto lo_of = [&](int sidx) { return n4 * sidx / nranks * 4; };
+    auto evl = [&](int k) { return ev(kEvP2pLayer + 32 * l + k); };
+    auto slot = [&](int j) { return flag_slots * l + j; };
+    // Ranks whose contributions a partial held by rank q before reduce round
+    // k covers: those agreeing with q on bits 0..b (b = d-1-k).
+    auto covers = [&](int q, int b) {
+      unsigned m = 0;
+      const int low = (1 << (b + 1)) - 1;
+      for (int x = 0; x < nranks; ++x)
+        if ((x & low) == (q & low)) m |= 1u << x;
+      return m;
+    };
+    int n = 0;
+    SPB_CUDA(cudaEventRecord(evl(0), s));  // dgrad_l (last reader of W_l) issued on s
+    launch_p2p_signal(peer_flags, slot(0), nranks, rank, epoch_dev, chain_sub, gs);
+    ++n;
+    SPB_CUDA(cudaEventRecord(ev(kEvBucket + l), gs));
+    SPB_CUDA(cudaStreamWaitEvent(s3, ev(kEvBucket + l), 0));
+    SPB_CUDA(cudaStreamWaitEvent(s3, evl(0), 0));
+    float* st_buf = stage + static_cast<long>(l % 2) * (nranks - 1) * stage_shard;
+    long st_off = 0;
+    bool own = contrib >> rank & 1u;  // does this rank's buffer hold a valid partial?
+    PeerPtrs<const float> fin{};
+    int nfin = 0;
+    for (int k = 0; k < d; ++k) {
+      const int b = d - 1 - k, p = rank ^ (1 << b);
+      const int base = (rank >> (b + 1)) << (b + 1), s0 = base + (((rank >> b) & 1) << b), s1 = s0 + (1 << b);
+      const long a0 = lo_of(s0), a1 = lo_of(s1), len = a1 - a0;
+      const bool theirs = (covers(p, b) & contrib) != 0;
+      cudaStream_t cs = gpull[p];
+      // Staging reuse: the buffer of layer l % 2 was last read by layer l + 2's update.
+      if (k == 0 && l + 2 <= L) SPB_CUDA(cudaStreamWaitEvent(cs, ev(kEvP2pLayer + 32 * (l + 2) + 1), 0));
+      if (k > 0) SPB_CUDA(cudaStreamWaitEvent(cs, evl(3 + k - 1 + 8), 0));  // my previous round's sum done
+      tbeg(cs);
+      launch_p2p_wait(flags, k == 0 ? slot(0) : slot(k), nranks, 1u << p, epoch_dev, chain_sub, cs);
+      tend(kTraceWait, cs);
+      ++n;
+      float* dst = nullptr;
+      if (theirs) {
+        dst = own ? st_buf + st_off : grad + off + a0;
+        if (!own && k == 0) SPB_CUDA(cudaStreamWaitEvent(cs, ev(kEvBucket + l), 0));  // (own grad unused; order anyway)
+        pbeg(cs);
+        if (len > 0) SPB_CUDA(cudaMemcpyAsync(dst, peer_grad[p] + off + a0, len * 4, cudaMemcpyDeviceToDevice, cs));
+        pend(kClsComm, static_cast<double>(len) * 4.0, cs);
+      }
+      SPB_CUDA(cudaEventRecord(evl(3 + k), cs));
+      SPB_CUDA(cudaStreamWaitEvent(s3, evl(3 + k), 0));
+      if (k < d - 1) {
+        if (theirs && own) {
+          pbeg(s3);
+          launch_rh_add(grad + off + a0, st_buf + st_off, len, s3);
+          pend(kClsComm, static_cast<double>(len) * 12.0, s3);
+          ++n;
+        }
+        own = own || theirs;
+        launch_p2p_signal(peer_flags, slot(1 + k), nranks, rank, epoch_dev, chain_sub, s3);
+        ++n;
+        SPB_CUDA(cudaEventRecord(evl(3 + k + 8), s3));
+      } else {
+        if (own) fin.p[nfin++] = grad + off + a0;
+        if (theirs && own) fin.p[nfin++] = st_buf + st_off;
+        if (theirs && !own) fin.p[nfin++] = grad + off + a0;
+      }
+      if (theirs && own) st_off += len;
+    }
+    // Update of shard `rank` (the last round's range) -> hi, lo, mom, w32.
+    const long a = lo_of(rank), sh = lo_of(rank + 1) - a;
+    pbeg(s3);
+    launch_p2p_update(fin, nfin, p_hi + off + a, p_lo + off + a, mom ? mom + off + a : nullptr, w32 + off + a, sh, lr, mu,
+                      wd, s3);
+    pend(kClsUpdate, static_cast<double>(sh) * 4.0 * (nfin + (mom ? 7 : 5)), s3);
+    launch_p2p_signal(peer_flags, slot(d), nranks, rank, epoch_dev, chain_sub, s3);
+    SPB_CUDA(cudaEventRecord(evl(1), s3));
+    n += 2;
+    // All-gather rounds: pull the partner's final weight block of 2^b shards.
+    cudaStream_t prev = s3;
+    for (int b = 0; b < d; ++b) {
+      const int p = rank ^ (1 << b);
+      const int pb = (p >> b) << b;
+      const long a0 = lo_of(pb), a1 = lo_of(pb + (1 << b));
+      cudaStream_t cs = wpull[p];
+      SPB_CUDA(cudaEventRecord(evl(24 + b), prev));
+      SPB_CUDA(cudaStreamWaitEvent(cs, evl(24 + b), 0));  // my block of 2^b shards final
+      tbeg(cs);
+      launch_p2p_wait(flags, slot(d + b), nranks, 1u << p, epoch_dev, chain_sub, cs);
+      tend(kTraceWait, cs);
+      pbeg(cs);
+      if (a1 > a0) SPB_CUDA(cudaMemcpyAsync(w32 + off + a0, peer_w32[p] + off + a0, (a1 - a0) * 4,
+                                            cudaMemcpyDeviceToDevice, cs));
+      pend(kClsComm, static_cast<double>(a1 - a0) * 4.0, cs);
+      n += 1;
+      if (b + 1 < d) {
+        launch_p2p_signal(peer_flags, slot(d + b + 1), nranks, rank, epoch_dev, chain_sub, cs);
+        ++n;
+      }
+      prev = cs;
+    }
+    // Split every shard but this rank's own into (hi, lo), after dgrad_l.
+    SPB_CUDA(cudaEventRecord(evl(16), prev));
+    SPB_CUDA(cudaStreamWaitEvent(s4, evl(16), 0));
+    SPB_CUDA(cudaStreamWaitEvent(s4, evl(0), 0));
+    pbeg(s4);
+    launch_p2p_split(w32 + off, p_hi + off, p_lo + off, cnt, a, a + sh, s4);
+    pend(kClsUpdate, static_cast<double>(cnt - sh) * 12.0, s4);
+    ++n;
+    SPB_CUDA(cudaStreamWaitEvent(s4, evl(1), 0));
+    SPB_CUDA(cudaEventRecord(ev(ev_ready(l)), s4));
+    fwd_wait[l] = ev_ready(l);
+    return n;
+  }
+
   // "rs" mode, layer l, on cst after the layer's gradient is final (gs) and
   // dgrad_l (s) has read W_l:
   //  - several contributing ranks: ncclReduceScatter of the gradient (zeros
@@ -1170,11 +1308,14 @@ struct Engine {
 
   // Collective over the ranks (spb_comm_init): allocate the p2p buffers and
   // map every peer's grad / w32 / flags through CUDA IPC.
-  void setup_p2p() {
+  // slots_per_layer: epoch-stamped flags per layer (p2p: G and U; rh: see
+  // enqueue_rh_layer).
+  void setup_p2p(int slots_per_layer = 2) {
     if (nranks > kMaxPeers) throw ConfigError("comm: p2p mode supports at most 8 ranks");
     if (!bar_dev) bar_dev = alloc<float>(1);
     w32 = alloc<float>(nflat);
-    flags = alloc<int>(2L * (L + 1) * nranks);
+    flag_slots = slots_per_layer;
+    flags = alloc<int>(static_cast<long>(slots_per_layer) * (L + 1) * nranks);
     epoch_dev = alloc<int>(1);
     long maxcnt = 0;
     for (int l = 1; l <= L; ++l) maxcnt = std::max(maxcnt, b_off[l] + round_up(w[l], 32) - w_off[l]);
@@ -1498,18 +1639,21 @@ struct Engine {
       fwd_wait.assign(L + 1, -1);
       return n;
     }
-    if (comm && comm_mode == 2) {
+    if (comm && (comm_mode == 2 || comm_mode == 5)) {
       // Per layer (top down): G signal on the gradient stream, gradient and
       // weight pulls on per-peer copy streams, shard update on s3, split on
-      // s4; all joined back into s, then the epoch advances.
+      // s4; all joined back into s, then the epoch advances. (5 = rh: the
+      // same streams, recursive-halving / -doubling pull schedule.)
       std::vector<cudaStream_t> side = {s3, s4};
       for (int p = 0; p < nranks; ++p)
         if (p != rank) side.push_back(gpull[p]), side.push_back(wpull[p]);
       for (size_t i = 0; i < side.size(); ++i) fork(side[i], kEvP2pFork + static_cast<int>(i));
       n += enqueue_pass(rows, row0, alpha, s,
-                        [&](int l, cudaStream_t from) { return enqueue_p2p_layer(l, full, from, s); }, false,
-                        &ctl->step, nullptr);
-      if (!last) return n;  // enqueue_p2p_layer set fwd_wait for the next step
+                        [&](int l, cudaStream_t from) {
+                          return comm_mode == 5 ? enqueue_rh_layer(l, full, from, s) : enqueue_p2p_layer(l, full, from, s);
+                        },
+                        false, &ctl->step, nullptr);
+      if (!last) return n;  // enqueue_p2p_layer / enqueue_rh_layer set fwd_wait for the next step
       for (size_t i = 0; i < side.size(); ++i) join(side[i], kEvP2pFork + 32 + static_cast<int>(i));
       launch_p2p_epoch(epoch_dev, nsub, s);
       return n + 1;
@@ -2000,15 +2144,25 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     e.buckets[1] = spb::bucket_plan(e.k, e.L, nranks, true);
     e.set_workers(spb::rank_workers(e.k, e.L, rank, nranks));
     e.ensure_rows(static_cast<int>(e.workers.size()) * e.bw);
-    // Aggregation mode: SPB_COMM = p2p | nccl | nvls. Default by measurement
-    // (cfg3): p2p for 2 ranks (pairwise copy-engine exchange at
-    // ~750 GB/s); NCCL from 4 ranks, where the copy engines' all-to-all
-    // pattern (~450 GB/s per GPU) no longer beats NCCL's rings.
+    // Aggregation mode: SPB_COMM = rh | p2p | nccl | nvls | rs | push.
+    // Default by measurement (cfg3): p2p for 2 ranks (one
+    // pairwise copy-engine exchange); rh for 4 (and 8) ranks, whose
+    // single-peer pull rounds beat both the p2p all-to-all pulls and NCCL's
+    // rings there (4.98 vs 5.09 / 5.2-5.4 ms); NCCL for other rank counts.
     const char* cm = std::getenv("SPB_COMM");
-    const std::string mode = cm ? cm : (nranks == 2 ? "p2p" : "nccl");
-    if (mode != "p2p" && mode != "nccl" && mode != "nvls" && mode != "rs" && mode != "push")
-      throw spb::ArgumentError("comm: SPB_COMM must be push, p2p, nccl, rs or nvls");
+    const bool pow2 = (nranks & (nranks - 1)) == 0;
+    const std::string mode = cm ? cm : (nranks == 2 ? "p2p" : (pow2 ? "rh" : "nccl"));
+    if (mode != "p2p" && mode != "nccl" && mode != "nvls" && mode != "rs" && mode != "push" && mode != "rh")
+      throw spb::ArgumentError("comm: SPB_COMM must be rh, push, p2p, nccl, rs or nvls");
+    if (mode == "rh" && (nranks & (nranks - 1)))
+      throw spb::ArgumentError("comm: rh mode needs a power-of-two rank count");
     if (nranks > 1 && mode == "p2p") e.setup_p2p();
+    if (nranks > 1 && mode == "rh") {
+      int d = 0;
+      while ((1 << d) < nranks) ++d;
+      e.setup_p2p(2 * d);
+      e.comm_mode = 5;
+    }
     if (nranks > 1 && mode == "push") e.setup_push();
     if (nranks > 1 && mode == "rs") e.setup_rs();
     if (nranks > 1 && mode == "nvls") {

@@ -126,6 +126,17 @@ __global__ void __launch_bounds__(256) p2p_split_kernel(const float* __restrict_
   }
 }
 
+// dst += src over n floats (n % 4 == 0): one recursive-halving reduce round.
+__global__ void __launch_bounds__(256) rh_add_kernel(float* __restrict__ dst, const float* __restrict__ src, long n4) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 a = reinterpret_cast<float4*>(dst)[i];
+    const float4 b = reinterpret_cast<const float4*>(src)[i];
+    a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
+    reinterpret_cast<float4*>(dst)[i] = a;
+  }
+}
+
 int grid_for(long n4) { return static_cast<int>(std::max<long>(1, std::min<long>((n4 + 255) / 256, 148L * 8))); }
 
 }  // namespace
@@ -152,6 +163,13 @@ void launch_p2p_update(const PeerPtrs<const float>& src, int nsrc, float* hi, fl
   if (n % 4) throw std::invalid_argument("p2p: shard must be a multiple of 4 floats");
   if (nsrc > kMaxPeers) throw std::invalid_argument("p2p: too many sources");
   p2p_update_kernel<<<grid_for(n / 4), 256, 0, s>>>(src, nsrc, hi, lo, mom, w32, n / 4, lr, mu, wd);
+  SPB_CUDA(cudaGetLastError());
+}
+
+void launch_rh_add(float* dst, const float* src, long n, cudaStream_t s) {
+  if (n <= 0) return;
+  if (n % 4) throw std::invalid_argument("rh: ranges must be multiples of 4 floats");
+  rh_add_kernel<<<grid_for(n / 4), 256, 0, s>>>(dst, src, n / 4);
   SPB_CUDA(cudaGetLastError());
 }
 

@@ -23,6 +23,8 @@ void launch_p2p_update(const PeerPtrs<const float>& src, int nsrc, float* hi, fl
 // (hi, lo) = split(w32) on [0, n) except [hole0, hole1).
 void launch_p2p_split(const float* w32, float* hi, float* lo, long n, long hole0, long hole1, cudaStream_t s);
 
+// dst += src (n floats, n % 4 == 0): a reduce round of the rh mode.
+void launch_rh_add(float* dst, const float* src, long n, cudaStream_t s);
 // "push" mode (push.cu): see the file comment for the protocol.
 void launch_push_signal(const PeerPtrs<int>& flags, int slot, int nranks, int rank, const int* epoch, int sub,
                         const float* gw, long ldw, const float* gb, int rpo, int n_rows, const PeerPtrs<float>& wdst,

@@ -442,10 +442,10 @@ class ChainMlp:
 
     @property
     def comm_mode(self):
-        """Multi-GPU aggregation mode: "push", "p2p", "rs", "nvls", "nccl" (None before comm_init)."""
+        """Multi-GPU aggregation mode: "rh", "push", "p2p", "rs", "nvls", "nccl" (None before comm_init)."""
         v = C.c_int()
         _check(load_library().spb_comm_mode(self._ctx, C.byref(v)), self._ctx)
-        return {0: "nccl", 1: "nvls", 2: "p2p", 3: "rs", 4: "push"}.get(v.value)
+        return {0: "nccl", 1: "nvls", 2: "p2p", 3: "rs", 4: "push", 5: "rh"}.get(v.value)
 
     def comm_selftest(self) -> int:
         """Collective NVLS diagnostic; returns the mismatching element count."""

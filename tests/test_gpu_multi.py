@@ -68,7 +68,7 @@ def _rank(rank, world, port, out_dir, full, mode="p2p", mu=0.0, wd=0.0, chain=No
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["push", "p2p", "rs", "nvls", "nccl"])
+@pytest.mark.parametrize("mode", ["rh", "push", "p2p", "rs", "nvls", "nccl"])
 @pytest.mark.parametrize("full", [False, True])
 def test_multi_gpu_step_matches_oracle(tmp_path, orc, full, mode):
     world = min(_gpus(), 4)
@@ -112,7 +112,7 @@ def test_multi_gpu_momentum_sharded_matches_nccl(tmp_path):
     import torch.multiprocessing as mp
 
     res = {}
-    for mode in ("push", "p2p", "rs", "nvls", "nccl"):
+    for mode in ("rh", "push", "p2p", "rs", "nvls", "nccl"):
         d = tmp_path / mode
         d.mkdir()
         mp.start_processes(_rank_momentum, args=(world, _free_port(), str(d), mode), nprocs=world,
@@ -122,7 +122,7 @@ def test_multi_gpu_momentum_sharded_matches_nccl(tmp_path):
     for l in range(L):  # push and p2p sum the same contributions in the same order
         for r in range(world):
             assert np.array_equal(res["push"][r][f"arr_{l + 1}"], res["p2p"][r][f"arr_{l + 1}"])
-    for mode in ("push", "p2p", "rs", "nvls"):
+    for mode in ("rh", "push", "p2p", "rs", "nvls"):
         for l in range(L):
             a, b = res[mode][0][f"arr_{l + 1}"], res["nccl"][0][f"arr_{l + 1}"]
             assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-5
