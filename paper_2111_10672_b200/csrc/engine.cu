@@ -229,6 +229,12 @@ struct Engine {
   std::vector<float*> peer_pstage;
   int flag_slots = 2;  // flags per layer (p2p / push: 2; rh: 2 log2 N)
   bool route_push = false;  // set while enqueue_step builds a push-mode step
+  // spb_step_host_async: double-buffered device staging of host batches,
+  // filled on their own copy stream while the previous step runs.
+  float *hx[2] = {nullptr, nullptr}, *hy[2] = {nullptr, nullptr};
+  long hx_n = 0, hy_n = 0;
+  cudaStream_t hst = nullptr;
+  unsigned host_calls = 0;
   cudaStream_t s4 = nullptr;
   std::vector<cudaStream_t> gpull, wpull;  // per-peer copy streams (copy engines run concurrently)
   // NVLS path (multi-GPU, NVSwitch multicast): p_hi / p_lo / grad live in
@@ -366,7 +372,9 @@ struct Engine {
     f(splitk_ws);
     f(p_hi), f(p_lo), f(grad), f(mom), f(X), f(Y), f(delta), f(row_loss), f(ybatch), f(scratch), f(scratch2), f(xin), f(idx),
         f(idx_in), f(loss_dev), f(tmp), f(ctl), f(workers_dev), f(epoch_dev), f(bar_dev), f(w32), f(flags),
-        f(stage);
+        f(stage), f(pstage), f(trace_dev);
+    for (int i = 0; i < 2; ++i) f(hx[i]), f(hy[i]);
+    if (hst) cudaStreamDestroy(hst), hst = nullptr;
     for (auto p : Hh) f(p);
     for (auto p : Hl) f(p);
     for (auto p : Ch) f(p);
@@ -2083,6 +2091,45 @@ spb_status spb_step_host(spb_ctx* ctx, const float* X_rows, const float* Y_rows,
     SPB_CUDA(cudaGraphLaunch(g, e.st));
     SPB_CUDA(cudaMemcpyAsync(loss_out, e.loss_dev, 4, cudaMemcpyDeviceToHost, e.st));
     SPB_CUDA(cudaStreamSynchronize(e.st));
+  });
+}
+
+spb_status spb_step_host_async(spb_ctx* ctx, const float* X_rows, const float* Y_rows, int full_backprop,
+                               float* loss_out) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    const int rows = static_cast<int>(e.workers.size()) * e.bw;
+    e.ensure_rows(rows);
+    const long per = e.conv_model ? static_cast<long>(e.ldx) : static_cast<long>(e.w[0]);
+    const long nx = rows * per, ny = static_cast<long>(rows) * e.nout;
+    if (!e.hst) SPB_CUDA(cudaStreamCreateWithFlags(&e.hst, cudaStreamNonBlocking));
+    if (nx > e.hx_n || ny > e.hy_n) {
+      SPB_CUDA(cudaStreamSynchronize(e.st));
+      SPB_CUDA(cudaStreamSynchronize(e.hst));
+      for (int i = 0; i < 2; ++i) {
+        if (e.hx[i]) cudaFree(e.hx[i]);
+        if (e.hy[i]) cudaFree(e.hy[i]);
+        e.hx[i] = Engine::alloc<float>(nx);
+        e.hy[i] = Engine::alloc<float>(ny);
+      }
+      e.hx_n = nx, e.hy_n = ny;
+    }
+    int launches = 0;
+    cudaGraphExec_t g = e.get_graph(full_backprop != 0, true, 1, &launches);
+    const int b = static_cast<int>(e.host_calls++ & 1u);
+    const int ev_done = spb::kEvP2pFork + 56 + b, ev_in = spb::kEvP2pFork + 58 + b;  // past the p2p joins (<= +47)
+    // Staging slot b was last read by the step two calls ago (its D2D copy on st).
+    if (e.host_calls > 2) SPB_CUDA(cudaStreamWaitEvent(e.hst, e.ev(ev_done), 0));
+    SPB_CUDA(cudaMemcpyAsync(e.hx[b], X_rows, nx * 4, cudaMemcpyHostToDevice, e.hst));
+    SPB_CUDA(cudaMemcpyAsync(e.hy[b], Y_rows, ny * 4, cudaMemcpyHostToDevice, e.hst));
+    SPB_CUDA(cudaEventRecord(e.ev(ev_in), e.hst));
+    SPB_CUDA(cudaStreamWaitEvent(e.st, e.ev(ev_in), 0));
+    SPB_CUDA(cudaMemcpyAsync(e.xin, e.hx[b], nx * 4, cudaMemcpyDeviceToDevice, e.st));
+    SPB_CUDA(cudaMemcpyAsync(e.ybatch, e.hy[b], ny * 4, cudaMemcpyDeviceToDevice, e.st));
+    SPB_CUDA(cudaEventRecord(e.ev(ev_done), e.st));
+    SPB_CUDA(cudaGraphLaunch(g, e.st));
+    SPB_CUDA(cudaMemcpyAsync(loss_out, e.loss_dev, 4, cudaMemcpyDeviceToHost, e.st));
+    e.last_launches = launches;
   });
 }
 

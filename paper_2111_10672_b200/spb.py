@@ -105,6 +105,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "spb_bucket_plan": (i, [i, i, i, i, ip, ip, ip]),
         "spb_set_fused_update": (i, [vp, i]),
         "spb_set_chain": (i, [vp, i]),
+        "spb_step_host_async": (i, [vp, fp, fp, i, fp]),
         "spb_trace_steps": (i, [vp, u64, i, i, i, i, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong), ip, ip, ip,
                                 ip]),
         "spb_comm_mode": (i, [vp, ip]),
@@ -128,7 +129,7 @@ EXPORTED = [
     "spb_step_host", "spb_loss", "spb_synchronize", "spb_stream", "spb_comm_unique_id", "spb_comm_init",
     "spb_last_batch", "spb_launches_per_step", "spb_make_random_chain_mlp",
     "spb_get_grads", "spb_profile_step", "spb_time_train_steps", "spb_bucket_plan", "spb_set_fused_update",
-    "spb_set_chain", "spb_trace_steps",
+    "spb_set_chain", "spb_trace_steps", "spb_step_host_async",
     "spb_comm_mode", "spb_comm_selftest", "spb_comm_bench", "spb_profile_task",
     "spb_empirical_variance", "spb_create_conv",
 ]
@@ -408,6 +409,14 @@ class ChainMlp:
         _check(load_library().spb_step_host(self._ctx, _fp(X_rows), _fp(Y_rows), int(full_backprop), _fp(loss)),
                self._ctx)
         return float(loss[0])
+
+    def step_host_async(self, X_rows: np.ndarray, Y_rows: np.ndarray, loss_out: np.ndarray, full_backprop: bool = False):
+        """spb_step_host_async: enqueue one step on host rows (pinned for an
+        asynchronous copy); loss_out (float32, >= 1 element) receives the
+        loss. The arrays must stay alive and unchanged until synchronize()."""
+        assert loss_out.dtype == np.float32 and X_rows.dtype == np.float32 and Y_rows.dtype == np.float32
+        _check(load_library().spb_step_host_async(self._ctx, _fp(X_rows), _fp(Y_rows), int(full_backprop),
+                                                  _fp(loss_out)), self._ctx)
 
     def profile_step(self, seed: int, step: int, full_backprop: bool = False):
         """One eager step with per-class CUDA-event timings (see spb_profile_step)."""

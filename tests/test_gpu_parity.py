@@ -411,3 +411,25 @@ def test_trace_steps_timeline_and_results():
     assert (tr["cls"] == 0).sum() == 3 * (len(widths) - 2)  # forward GEMMs
     for x, y in zip(a.get_params(), b.get_params()):
         assert np.array_equal(x, y)
+
+
+def test_step_host_async_equals_step_host():
+    """spb_step_host_async (double-buffered staging, copy stream, no host
+    sync) must produce the same losses and weights as spb_step_host."""
+    widths, N, k, bw = [64, 48, 32, 1], 256, 4, 8
+    a, X, Y, W = make(widths, N, 8, k=k, bw=bw)
+    b, *_ = make(widths, N, 8, k=k, bw=bw)
+    a.set_optimizer(0.1, 0.9, 1e-3)
+    b.set_optimizer(0.1, 0.9, 1e-3)
+    batches = []
+    for s in range(1, 6):
+        idx = np.concatenate([spb.draw_batch(4, s, j, bw, N) for j in range(1, k + 1)])
+        batches.append((np.ascontiguousarray(X[idx], dtype=np.float32), np.ascontiguousarray(Y[idx], dtype=np.float32)))
+    want = [b.step_host(x, y) for x, y in batches]
+    got = np.zeros(len(batches), dtype=np.float32)
+    for i, (x, y) in enumerate(batches):
+        a.step_host_async(x, y, got[i:i + 1])
+    a.synchronize()
+    assert np.array_equal(got, np.array(want, dtype=np.float32))
+    for x, y in zip(a.get_params(), b.get_params()):
+        assert np.array_equal(x, y)
