@@ -177,10 +177,10 @@ SPB_API spb_status spb_step_host(spb_ctx* ctx, const float* X_rows, const float*
 /* spb_step_host without the synchronisation (a training loop's input
  * pipeline): the host rows go to a double-buffered device staging area on
  * the context's copy stream, so the next step's host-to-device copy runs
- * while this step computes; the loss is copied to *loss_out asynchronously.
- * X_rows / Y_rows (pinned memory for an asynchronous copy) and loss_out must
- * stay valid and unchanged until spb_synchronize. Same results as
- * spb_step_host. */
+ * while this step computes; the loss goes to a pinned ring and is written to
+ * *loss_out by the next spb_synchronize. X_rows / Y_rows (pinned memory for
+ * an asynchronous copy) and loss_out must stay valid and unchanged until
+ * then. Same results as spb_step_host. */
 SPB_API spb_status spb_step_host_async(spb_ctx* ctx, const float* X_rows, const float* Y_rows, int full_backprop,
                                        float* loss_out);
 /* The aggregated per-layer gradient the last unfused step applied

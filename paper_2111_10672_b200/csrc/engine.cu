@@ -235,6 +235,16 @@ struct Engine {
   long hx_n = 0, hy_n = 0;
   cudaStream_t hst = nullptr;
   unsigned host_calls = 0;
+  // Losses of async steps land in a pinned ring (a D2H copy into pageable
+  // memory would block the host until the step finished) and are copied to
+  // the callers' pointers at the next synchronisation.
+  static constexpr int kLossRing = 64;
+  float* loss_pin = nullptr;
+  std::vector<std::pair<float*, int>> loss_pending;
+  void flush_losses() {  // after a stream synchronisation
+    for (auto& pr : loss_pending) *pr.first = loss_pin[pr.second];
+    loss_pending.clear();
+  }
   cudaStream_t s4 = nullptr;
   std::vector<cudaStream_t> gpull, wpull;  // per-peer copy streams (copy engines run concurrently)
   // NVLS path (multi-GPU, NVSwitch multicast): p_hi / p_lo / grad live in
@@ -375,6 +385,7 @@ struct Engine {
         f(stage), f(pstage), f(trace_dev);
     for (int i = 0; i < 2; ++i) f(hx[i]), f(hy[i]);
     if (hst) cudaStreamDestroy(hst), hst = nullptr;
+    if (loss_pin) cudaFreeHost(loss_pin), loss_pin = nullptr;
     for (auto p : Hh) f(p);
     for (auto p : Hl) f(p);
     for (auto p : Ch) f(p);
@@ -2128,7 +2139,14 @@ spb_status spb_step_host_async(spb_ctx* ctx, const float* X_rows, const float* Y
     SPB_CUDA(cudaMemcpyAsync(e.ybatch, e.hy[b], ny * 4, cudaMemcpyDeviceToDevice, e.st));
     SPB_CUDA(cudaEventRecord(e.ev(ev_done), e.st));
     SPB_CUDA(cudaGraphLaunch(g, e.st));
-    SPB_CUDA(cudaMemcpyAsync(loss_out, e.loss_dev, 4, cudaMemcpyDeviceToHost, e.st));
+    if (!e.loss_pin) SPB_CUDA(cudaMallocHost(&e.loss_pin, Engine::kLossRing * sizeof(float)));
+    if (static_cast<int>(e.loss_pending.size()) == Engine::kLossRing) {  // ring full: drain it
+      SPB_CUDA(cudaStreamSynchronize(e.st));
+      e.flush_losses();
+    }
+    const int slot = static_cast<int>((e.host_calls - 1) % Engine::kLossRing);
+    SPB_CUDA(cudaMemcpyAsync(e.loss_pin + slot, e.loss_dev, 4, cudaMemcpyDeviceToHost, e.st));
+    e.loss_pending.push_back({loss_out, slot});
     e.last_launches = launches;
   });
 }
@@ -2158,7 +2176,10 @@ spb_status spb_loss(spb_ctx* ctx, double* out) {
 }
 
 spb_status spb_synchronize(spb_ctx* ctx) {
-  return guard(ctx, [&] { SPB_CUDA(cudaStreamSynchronize(ctx->e.st)); });
+  return guard(ctx, [&] {
+    SPB_CUDA(cudaStreamSynchronize(ctx->e.st));
+    ctx->e.flush_losses();
+  });
 }
 
 void* spb_stream(spb_ctx* ctx) { return ctx ? static_cast<void*>(ctx->e.st) : nullptr; }
