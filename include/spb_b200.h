@@ -209,7 +209,7 @@ SPB_API void* spb_stream(spb_ctx* ctx);
  *  - "rs": NCCL reduce-scatter of each layer's gradient, the optimizer on
  *    this rank's shard, NCCL all-gather of the fp32 weights (a layer with one
  *    contributing rank: that rank updates it and broadcasts the weights);
- *  - "rh" (power-of-two rank counts; default for 4 and 8): the p2p protocol's buffers with
+ *  - "rh" (power-of-two rank counts; default for 4 ranks): the p2p protocol's buffers with
  *    Rabenseifner's schedule -- recursive-halving reduce-scatter, the owner's
  *    update, recursive-doubling all-gather of the fp32 weights -- so every
  *    copy-engine pull is from ONE peer (single-peer NVLink copies run at

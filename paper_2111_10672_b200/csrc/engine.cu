@@ -2214,12 +2214,12 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     e.ensure_rows(static_cast<int>(e.workers.size()) * e.bw);
     // Aggregation mode: SPB_COMM = rh | p2p | nccl | nvls | rs | push.
     // Default by measurement (cfg3): p2p for 2 ranks (one
-    // pairwise copy-engine exchange); rh for 4 (and 8) ranks, whose
-    // single-peer pull rounds beat both the p2p all-to-all pulls and NCCL's
-    // rings there (4.98 vs 5.09 / 5.2-5.4 ms); NCCL for other rank counts.
+    // pairwise copy-engine exchange); rh for 4 ranks, whose single-peer pull
+    // rounds beat both the p2p all-to-all pulls and NCCL's rings there
+    // (4.98 vs 5.09 / 5.2-5.4 ms); NCCL elsewhere (8 ranks could not be
+    // measured here: gpurun offers at most 4 GPUs).
     const char* cm = std::getenv("SPB_COMM");
-    const bool pow2 = (nranks & (nranks - 1)) == 0;
-    const std::string mode = cm ? cm : (nranks == 2 ? "p2p" : (pow2 ? "rh" : "nccl"));
+    const std::string mode = cm ? cm : (nranks == 2 ? "p2p" : (nranks == 4 ? "rh" : "nccl"));
     if (mode != "p2p" && mode != "nccl" && mode != "nvls" && mode != "rs" && mode != "push" && mode != "rh")
       throw spb::ArgumentError("comm: SPB_COMM must be rh, push, p2p, nccl, rs or nvls");
     if (mode == "rh" && (nranks & (nranks - 1)))
