@@ -877,9 +877,7 @@ struct Engine {
     // Fused: wgrad_l updates W_l in place, so it also waits for dgrad_l (the
     // last reader of W_l). Collectives and per-layer updates hang off the
     // events recorded here.
-    // SPB_SERIAL_BWD=1 (experiment): wgrad on the dgrad stream.
-    static const bool serial_bwd = std::getenv("SPB_SERIAL_BWD") != nullptr;
-    const bool two = concurrent && !serial_bwd;
+    const bool two = concurrent;
     if (two) {
       SPB_CUDA(cudaEventRecord(ev(kEvFork), s));
       SPB_CUDA(cudaStreamWaitEvent(s2, ev(kEvFork), 0));
