@@ -458,7 +458,7 @@ def run_b200(args, world, rank, local, dist):
                    "parallelism": f"spb-dp{world} (workers/rank {len(workers)})", "l2": "inputs exceed L2 (2 GB weights)",
                    "aggregation": comm_mode or "local (1 GPU)",
                    "graph_chain": (max(1, min(16, int(os.environ["SPB_CHAIN"]))) if "SPB_CHAIN" in os.environ
-                                   else (8 if world == 1 else 1))},
+                                   else 1)},
         "spb_savings": spb_savings(widths, k, bw, world),
         "full_backprop": {"value": round(full_value, 2), "unit": UNIT, "ms_per_step": round(ms_full / K, 4),
                           "spb_speedup": round(value / full_value, 4)},

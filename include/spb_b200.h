@@ -116,8 +116,8 @@ SPB_API spb_status spb_get_params(spb_ctx* ctx, float* const* blocks);
  * the ConvNet always use per-layer updates. */
 SPB_API spb_status spb_set_fused_update(spb_ctx* ctx, int fused);
 /* Cross-step pipelining for spb_train_steps / spb_time_train_steps: up to
- * `steps` (1..16; env SPB_CHAIN; default 8 on one GPU and 1 with a
- * multi-GPU exchange, where it measured slower) consecutive SPB iterations are
+ * `steps` (1..16; env SPB_CHAIN; default 1: longer chains measured slower
+ * on most configurations) consecutive SPB iterations are
  * captured into ONE CUDA graph in which iteration t+1's forward of layer l
  * waits only for W_l of iteration t (its update and, multi-GPU, its exchange)
  * instead of for the whole iteration, so the exchange / update tail of one

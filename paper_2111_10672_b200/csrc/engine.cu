@@ -174,10 +174,11 @@ struct Engine {
   // fwd_wait[l] = event index the forward of layer l (the head for l = L)
   // must wait on, -1 = none; chain_sub = index of the step being enqueued.
   static constexpr int kMaxChain = 16;
-  // chain = 0: automatic -- 8 on one GPU (measured +1.7 % on cfg3), 1 with a
-  // multi-GPU exchange (the exchange tail running beside the next forward
-  // slowed both: -2 to -7 % at 2 and 4 ranks). SPB_CHAIN / spb_set_chain
-  // override.
+  // chain = 0: automatic = 1. Measured (cfg5 sweep, one box, chain 8 vs 1):
+  // -16 % / -8 % / -1 % / +1 % at widths 1k / 2k / 4k / 8k on one GPU,
+  // -2 to -7 % with a multi-GPU exchange (its tail running beside the next
+  // forward slows both), and slower on the launch-bound cfg2. Kept as an
+  // option (SPB_CHAIN / spb_set_chain).
   int chain = default_chain();
   int chain_sub = 0;
   static int default_chain() {
@@ -186,7 +187,7 @@ struct Engine {
     const int v = std::atoi(c);
     return v < 1 ? 1 : (v > kMaxChain ? kMaxChain : v);
   }
-  int chain_len() const { return chain > 0 ? chain : (comm ? 1 : 8); }
+  int chain_len() const { return chain > 0 ? chain : 1; }
   std::vector<int> fwd_wait;
   std::string err;
   // multi-GPU
