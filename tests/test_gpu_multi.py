@@ -1,11 +1,13 @@
 """Multi-GPU SPB step (needs >= 2 GPUs; skipped otherwise).
 
-Each rank runs its balanced worker set on its own B200. Three aggregation
-paths: p2p (copy-engine pulls of gradient shards, sharded update, pulls of
-the updated weights), NVLS (gradients reduced in the NVSwitch, each rank
-updates its shard and multicasts the new weights) and NCCL per-layer buckets
-(broadcast from a sole contributor, else all-reduce, then the same update on
-every rank).
+Each rank runs its balanced worker set on its own B200. Aggregation paths:
+p2p (copy-engine pulls of gradient shards, sharded update, pulls of the
+updated weights), rh (the same on a recursive-halving / -doubling schedule),
+push (gradient rows stored to their owners by the wgrad epilogue), rs (NCCL
+reduce-scatter / all-gather), NVLS (gradients reduced in the NVSwitch, each
+rank updates its shard and multicasts the new weights) and NCCL per-layer
+buckets (broadcast from a sole contributor, else all-reduce, then the same
+update on every rank).
 Weights after 3 steps must equal the single-process CPU oracle's SPB-SGD
 iterates (1e-4) and be bit-identical across ranks; batch indices must be
 bit-exact.
@@ -34,6 +36,19 @@ def _free_port():
     p = s.getsockname()[1]
     s.close()
     return p
+
+
+def _launch(fn, world, *rest):
+    """mp.start_processes(fn, args=(world, port, *rest)) on a fresh port,
+    retried when another process grabbed the port first (EADDRINUSE)."""
+    import torch.multiprocessing as mp
+
+    for attempt in range(4):
+        try:
+            return mp.start_processes(fn, args=(world, _free_port(), *rest), nprocs=world, start_method="spawn")
+        except Exception as ex:  # noqa: BLE001
+            if "EADDRINUSE" not in str(ex) or attempt == 3:
+                raise
 
 
 WIDTHS, N, K, BW, LR, SEED, DSEED = [96, 80, 72, 64, 56, 48, 40, 32, 1], 512, 8, 16, 0.05, 11, 5
@@ -74,12 +89,10 @@ def test_multi_gpu_step_matches_oracle(tmp_path, orc, full, mode):
     world = min(_gpus(), 4)
     if world < 2:
         pytest.skip("needs >= 2 GPUs")
-    import torch.multiprocessing as mp
 
     from paper_2111_10672_b200 import spb
 
-    mp.start_processes(_rank, args=(world, _free_port(), str(tmp_path), full, mode), nprocs=world,
-                       start_method="spawn")
+    _launch(_rank, world, str(tmp_path), full, mode)
     L = len(WIDTHS) - 1
     X, Y, W = orc.gen_chain_mlp(WIDTHS, N, DSEED)
     Xf, Yf, Wf = spb.gen_chain_mlp(WIDTHS, N, DSEED)
@@ -109,14 +122,12 @@ def test_multi_gpu_momentum_sharded_matches_nccl(tmp_path):
     world = min(_gpus(), 4)
     if world < 2:
         pytest.skip("needs >= 2 GPUs")
-    import torch.multiprocessing as mp
 
     res = {}
     for mode in ("rh", "push", "p2p", "rs", "nvls", "nccl"):
         d = tmp_path / mode
         d.mkdir()
-        mp.start_processes(_rank_momentum, args=(world, _free_port(), str(d), mode), nprocs=world,
-                           start_method="spawn")
+        _launch(_rank_momentum, world, str(d), mode)
         res[mode] = [np.load(d / f"r{r}.npz") for r in range(world)]
     L = len(WIDTHS) - 1
     for l in range(L):  # push and p2p sum the same contributions in the same order
@@ -144,14 +155,12 @@ def test_multi_gpu_chained_graph_bitwise(tmp_path, mode):
     world = min(_gpus(), 4)
     if world < 2:
         pytest.skip("needs >= 2 GPUs")
-    import torch.multiprocessing as mp
 
     res = {}
     for chain in (1, 8):
         d = tmp_path / f"c{chain}"
         d.mkdir()
-        mp.start_processes(_rank_chain, args=(world, _free_port(), str(d), mode, chain), nprocs=world,
-                           start_method="spawn")
+        _launch(_rank_chain, world, str(d), mode, chain)
         res[chain] = [np.load(d / f"r{r}.npz") for r in range(world)]
     for l in range(len(WIDTHS) - 1):
         a = res[1][0][f"arr_{l + 1}"]
@@ -188,9 +197,8 @@ def test_nvls_multicast_selftest(tmp_path):
     world = min(_gpus(), 4)
     if world < 2:
         pytest.skip("needs >= 2 GPUs")
-    import torch.multiprocessing as mp
 
-    mp.start_processes(_rank_selftest, args=(world, _free_port(), str(tmp_path)), nprocs=world, start_method="spawn")
+    _launch(_rank_selftest, world, str(tmp_path))
     for r in range(world):
         bad, on = np.load(tmp_path / f"s{r}.npy")
         assert on == 1 and bad == 0
@@ -231,12 +239,11 @@ def test_multi_gpu_convnet_matches_oracle(tmp_path, orc, mode):
     world = min(_gpus(), 4)
     if world < 2:
         pytest.skip("needs >= 2 GPUs")
-    import torch.multiprocessing as mp
 
     from oracle.conv_oracle import ConvOracle
     from paper_2111_10672_b200 import spb
 
-    mp.start_processes(_rank_conv, args=(world, _free_port(), str(tmp_path), mode), nprocs=world, start_method="spawn")
+    _launch(_rank_conv, world, str(tmp_path), mode)
     X, Y, W = spb.gen_convnet(CSHAPE, CCONVS, CNOUT, N, DSEED)
     o = ConvOracle(CSHAPE, CCONVS, CNOUT)
     B = [w.astype(np.float64) for w in W]
