@@ -50,6 +50,9 @@ CFG2 = dict(workload="cfg2: MLP 784-512-512-10 fp32, 4 SPB workers time-sliced o
 REF_BW = 2  # reference CPU arm: per-worker samples per step (bounded sample)
 
 
+NVLINK_GBS = 766.7  # measured: one-peer copy-engine pull / push per direction, 1 GiB (profiles/r01_nvlink_copy_engine.txt)
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -467,10 +470,22 @@ def run_b200(args, world, rank, local, dist):
         "clocks": clk,
         "e2e": e2e,
         "roofline": roofline_of(prof, load_peaks(), traffic_from_profiles()),
+        # (world > 1: "nvlink" added below -- this rank's exchange bytes per step
+        # over the step time, against the measured one-peer copy bandwidth)
         "phase_ms": {c: round(prof[c]["ms"], 3) for c in prof},
         "phase_ms_full_backprop": {c: round(prof_full[c]["ms"], 3) for c in prof_full},
         "eager_step_ms": round(prof_step_ms, 3),
     }
+    if world > 1:
+        comm_bytes = max_over_ranks(dist, float(prof["comm"]["work"]))
+        step_s = ms / K * 1e-3
+        nv = comm_bytes / step_s / 1e9
+        line["roofline"]["nvlink"] = {
+            "bound": "nvlink", "achieved": round(nv, 1), "peak": NVLINK_GBS, "unit": "GB/s",
+            "frac": round(nv / NVLINK_GBS, 4), "bytes_per_step": comm_bytes,
+            "note": f"{comm_mode}: bytes this rank pulls (p2p / rh) or reduces (nccl buckets, algorithmic) per step, "
+                    "max over ranks, averaged over the whole step; peak = measured one-peer copy-engine bandwidth "
+                    "per direction (profiles/r01_nvlink_copy_engine.txt)"}
     barrier(dist)
     m.close()
     del m

@@ -1197,7 +1197,7 @@ struct Engine {
         if (theirs && own) {
           pbeg(s3);
           launch_rh_add(grad + off + a0, st_buf + st_off, len, s3);
-          pend(kClsComm, static_cast<double>(len) * 12.0, s3);
+          pend(kClsUpdate, static_cast<double>(len) * 12.0, s3);
           ++n;
         }
         own = own || theirs;
