@@ -232,7 +232,7 @@ def _rank_conv(rank, world, port, out_dir, mode):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["p2p", "rs", "nvls", "nccl"])
+@pytest.mark.parametrize("mode", ["rh", "p2p", "rs", "nvls", "nccl"])
 def test_multi_gpu_convnet_matches_oracle(tmp_path, orc, mode):
     """The ConvNet (cfg4 shape family) on 2-4 GPUs: 3 SPB steps equal the
     single-process fp64 conv oracle (1e-4) and are bit-identical across ranks."""
