@@ -856,34 +856,39 @@ struct Engine {
     auto col_upd = [&](long off) {
       return ColUpdate{p_lo + off, mom ? mom + off : nullptr, lr, mu, wd};
     };
-    // Head gradients over the contributor rows of layer L.
-    if (row0[L] < rows) {
-      pbeg(s);
-      ColUpdate uw = col_upd(w_off[L]), ub = col_upd(b_off[L]);
-      const bool fL = lf(L);
-      launch_colreduce(Hh[L - 1], Hl[L - 1], ld[L - 1], row0[L], rows, w[L - 1], delta, nout, nout, alpha[L],
-                       fL ? p_hi + w_off[L] : grad + w_off[L], ld[L - 1], scratch, s, fL ? &uw : nullptr);
-      launch_colreduce(delta, nullptr, nout, row0[L], rows, nout, nullptr, 1, 0, alpha[L],
-                       fL ? p_hi + b_off[L] : grad + b_off[L], 0, scratch, s, fL ? &ub : nullptr);
-      pend(kClsColred, 0, s);
-      n += 4;
-    }
-    if (on_grad) n += on_grad(L, s);
-    if (on_layer) on_layer(L, s);  // W_L: read by the head only
-    // Truncated backward (model.cpp:161-185): layer l runs over its
-    // contributor rows only; dgrad stops at the lowest covered layer.
-    // Two streams: dgrad_l on s (the Delta chain), wgrad_l (+ bias) on s2.
-    // Delta is triple-buffered (Delta_l in buffer l % 3), so dgrad_l only has
-    // to wait for wgrad_{l+2}, the last reader of the buffer it overwrites.
-    // Fused: wgrad_l updates W_l in place, so it also waits for dgrad_l (the
-    // last reader of W_l). Collectives and per-layer updates hang off the
-    // events recorded here.
+    // Two streams from here on: the Delta chain (head, dgrads) on s, the
+    // gradient reductions (head gradients, wgrads, bias sums) on s2, so
+    // dgrad_{L-1} starts right after the head kernel.
     const bool two = concurrent;
     if (two) {
       SPB_CUDA(cudaEventRecord(ev(kEvFork), s));
       SPB_CUDA(cudaStreamWaitEvent(s2, ev(kEvFork), 0));
     }
     cudaStream_t sw = two ? s2 : s;
+    float* const scr = two ? scratch2 : scratch;  // the column-reduction scratch of sw
+    // Head gradients over the contributor rows of layer L (W_L was last read
+    // by the head kernel, so the fused update may rewrite it here).
+    if (row0[L] < rows) {
+      pbeg(sw);
+      ColUpdate uw = col_upd(w_off[L]), ub = col_upd(b_off[L]);
+      const bool fL = lf(L);
+      launch_colreduce(Hh[L - 1], Hl[L - 1], ld[L - 1], row0[L], rows, w[L - 1], delta, nout, nout, alpha[L],
+                       fL ? p_hi + w_off[L] : grad + w_off[L], ld[L - 1], scr, sw, fL ? &uw : nullptr);
+      launch_colreduce(delta, nullptr, nout, row0[L], rows, nout, nullptr, 1, 0, alpha[L],
+                       fL ? p_hi + b_off[L] : grad + b_off[L], 0, scr, sw, fL ? &ub : nullptr);
+      pend(kClsColred, 0, sw);
+      n += 4;
+    }
+    if (on_grad) n += on_grad(L, sw);
+    if (on_layer) on_layer(L, sw);  // W_L: read by the head only
+    // Truncated backward (model.cpp:161-185): layer l runs over its
+    // contributor rows only; dgrad stops at the lowest covered layer.
+    // dgrad_l on s (the Delta chain), wgrad_l (+ bias) on s2.
+    // Delta is triple-buffered (Delta_l in buffer l % 3), so dgrad_l only has
+    // to wait for wgrad_{l+2}, the last reader of the buffer it overwrites.
+    // Fused: wgrad_l updates W_l in place, so it also waits for dgrad_l (the
+    // last reader of W_l). Collectives and per-layer updates hang off the
+    // events recorded here.
     auto ev_delta = [&](int l) { return ev(kEvLayer + 2 * l); };     // Delta_l ready (on s)
     auto ev_wgrad = [&](int l) { return ev(kEvLayer + 2 * l + 1); }; // wgrad_l done (on s2)
     if (two) SPB_CUDA(cudaEventRecord(ev_delta(L - 1), s));          // from the head kernel
