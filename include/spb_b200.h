@@ -209,16 +209,16 @@ SPB_API void* spb_stream(spb_ctx* ctx);
  *  - "rs": NCCL reduce-scatter of each layer's gradient, the optimizer on
  *    this rank's shard, NCCL all-gather of the fp32 weights (a layer with one
  *    contributing rank: that rank updates it and broadcasts the weights);
- *  - "rh" (power-of-two rank counts; default for 4 ranks): the p2p protocol's buffers with
+ *  - "rh" (power-of-two rank counts; default for the ConvNet at 4 ranks): the p2p protocol's buffers with
  *    Rabenseifner's schedule -- recursive-halving reduce-scatter, the owner's
  *    update, recursive-doubling all-gather of the fp32 weights -- so every
  *    copy-engine pull is from ONE peer (single-peer NVLink copies run at
  *    ~760 GB/s, all-to-all pulls at ~450 GB/s);
- *  - "push": the wgrad GEMM epilogue stores each gradient row straight into
- *    the owning rank's staging slot (NVLink stores through CUDA IPC); the
- *    owner sums its rows, applies the optimizer and stores the new fp32 rows
- *    into every peer; peers split them into (hi, lo). No copy engines, no
- *    NCCL in the step;
+ *  - "push" (MLP; default at 4 ranks): the wgrad GEMM epilogue stores each
+ *    gradient row straight into the owning rank's staging slot (NVLink
+ *    stores through CUDA IPC, staged through shared memory into 128-byte row
+ *    segments); the owner sums its rows and applies the optimizer; the peers
+ *    pull the new fp32 rows (copy engines) and split them into (hi, lo);
  *  - "nccl" (default for other rank counts): per-layer NCCL buckets
  *    (broadcast / all-reduce), then the local optimizer update on every rank.
  * Ranks of one node only. */

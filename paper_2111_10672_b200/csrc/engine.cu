@@ -1436,6 +1436,9 @@ struct Engine {
       peer_flags.p[p] = static_cast<int*>(q);
     }
     SPB_CUDA(cudaStreamCreateWithFlags(&s4, cudaStreamNonBlocking));
+    wpull.assign(nranks, nullptr);
+    for (int p = 0; p < nranks; ++p)
+      if (p != rank) SPB_CUDA(cudaStreamCreateWithFlags(&wpull[p], cudaStreamNonBlocking));
     comm_mode = 4;
     invalidate_graphs();
     host_barrier();
@@ -1506,24 +1509,39 @@ struct Engine {
       }
       ++nsrc;
     }
-    for (int o = 0; o < nranks; ++o) {
-      if (o == rank) continue;
-      dw.p[ndst] = peer_w32[o] + w_off[l] + static_cast<long>(r0) * ldw;
-      db.p[ndst] = peer_w32[o] + b_off[l] + r0;
-      ++ndst;
-    }
+    // The owner's new fp32 rows go to its own w32; the peers pull them (copy
+    // engines), as in the p2p mode.
+    dw.p[ndst] = w32 + w_off[l] + static_cast<long>(r0) * ldw;
+    db.p[ndst] = w32 + b_off[l] + r0;
+    ++ndst;
     pbeg(s3);
     launch_push_update(sw, nsrc, p_hi + w_off[l] + r0 * ldw, p_lo + w_off[l] + r0 * ldw,
                        mom ? mom + w_off[l] + r0 * ldw : nullptr, dw, ndst, nw, lr, mu, wd, s3);
     launch_push_update(sb, nsrc, p_hi + b_off[l] + r0, p_lo + b_off[l] + r0, mom ? mom + b_off[l] + r0 : nullptr, db,
                        ndst, nb, lr, mu, wd, s3);
-    pend(kClsUpdate, static_cast<double>(nw + nb) * 4.0 * (nsrc + (mom ? 5 : 4)), s3);
+    pend(kClsUpdate, static_cast<double>(nw + nb) * 4.0 * (nsrc + (mom ? 6 : 5)), s3);
     launch_p2p_signal(peer_flags, 2 * l + 1, nranks, rank, epoch_dev, chain_sub, s3);
     SPB_CUDA(cudaEventRecord(evl(1), s3));
-    // 3. the other owners' rows: wait for their U[l] and for dgrad_l, split.
-    tbeg(s4);
-    launch_p2p_wait(flags, 2 * l + 1, nranks, peers, epoch_dev, chain_sub, s4);
-    tend(kTraceWait, s4);
+    // 3. every other owner's rows: wait for its U[l], pull (copy engines);
+    // then split after dgrad_l.
+    for (int o = 0; o < nranks; ++o) {
+      if (o == rank) continue;
+      const int q0 = std::min(w[l], o * rpo), q1 = std::min(w[l], (o + 1) * rpo);
+      cudaStream_t cs = wpull[o];
+      tbeg(cs);
+      launch_p2p_wait(flags, 2 * l + 1, nranks, 1u << o, epoch_dev, chain_sub, cs);
+      tend(kTraceWait, cs);
+      if (q1 > q0) {
+        pbeg(cs);
+        SPB_CUDA(cudaMemcpyAsync(w32 + w_off[l] + static_cast<long>(q0) * ldw, peer_w32[o] + w_off[l] + q0 * ldw,
+                                 static_cast<size_t>(q1 - q0) * ldw * 4, cudaMemcpyDeviceToDevice, cs));
+        SPB_CUDA(cudaMemcpyAsync(w32 + b_off[l] + q0, peer_w32[o] + b_off[l] + q0, static_cast<size_t>(q1 - q0) * 4,
+                                 cudaMemcpyDeviceToDevice, cs));
+        pend(kClsComm, static_cast<double>(q1 - q0) * (ldw + 1) * 4.0, cs);
+      }
+      SPB_CUDA(cudaEventRecord(evl(16 + o), cs));
+      SPB_CUDA(cudaStreamWaitEvent(s4, evl(16 + o), 0));
+    }
     SPB_CUDA(cudaStreamWaitEvent(s4, evl(0), 0));
     pbeg(s4);
     launch_push_split(w32 + w_off[l], p_hi + w_off[l], p_lo + w_off[l], static_cast<long>(w[l]) * ldw, r0 * ldw,
@@ -1683,10 +1701,12 @@ struct Engine {
     }
     if (comm && comm_mode == 4) {
       // Per layer (top down): gradient rows stored to their owners by the
-      // wgrad epilogue, G signal on the gradient stream, owner update + weight
-      // stores on s3, split of the received rows on s4.
-      fork(s3, kEvP2pFork);
-      fork(s4, kEvP2pFork + 1);
+      // wgrad epilogue, G signal on the gradient stream, owner update on s3,
+      // weight pulls on per-peer copy streams, split on s4.
+      std::vector<cudaStream_t> side = {s3, s4};
+      for (int p = 0; p < nranks; ++p)
+        if (p != rank) side.push_back(wpull[p]);
+      for (size_t i = 0; i < side.size(); ++i) fork(side[i], kEvP2pFork + static_cast<int>(i));
       route_push = true;
       try {
         n += enqueue_pass(rows, row0, alpha, s,
@@ -1698,8 +1718,7 @@ struct Engine {
       }
       route_push = false;
       if (!last) return n;
-      join(s3, kEvP2pFork + 32);
-      join(s4, kEvP2pFork + 33);
+      for (size_t i = 0; i < side.size(); ++i) join(side[i], kEvP2pFork + 32 + static_cast<int>(i));
       launch_p2p_epoch(epoch_dev, nsub, s);
       return n + 1;
     }
@@ -2218,12 +2237,13 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     e.ensure_rows(static_cast<int>(e.workers.size()) * e.bw);
     // Aggregation mode: SPB_COMM = rh | p2p | nccl | nvls | rs | push.
     // Default by measurement (cfg3): p2p for 2 ranks (one
-    // pairwise copy-engine exchange); rh for 4 ranks, whose single-peer pull
-    // rounds beat both the p2p all-to-all pulls and NCCL's rings there
-    // (4.98 vs 5.09 / 5.2-5.4 ms); NCCL elsewhere (8 ranks could not be
-    // measured here: gpurun offers at most 4 GPUs).
+    // pairwise copy-engine exchange); push for 4 ranks (gradient rows stored
+    // to their owners by the wgrad epilogue: 4.47 ms vs rh 5.02, p2p 5.2,
+    // nccl 5.09 on one box), rh for the ConvNet there (push is MLP-only);
+    // NCCL elsewhere (8 ranks could not be measured: gpurun offers 4 GPUs).
     const char* cm = std::getenv("SPB_COMM");
-    const std::string mode = cm ? cm : (nranks == 2 ? "p2p" : (nranks == 4 ? "rh" : "nccl"));
+    const std::string mode =
+        cm ? cm : (nranks == 2 ? "p2p" : (nranks == 4 ? (e.conv_model ? "rh" : "push") : "nccl"));
     if (mode != "p2p" && mode != "nccl" && mode != "nvls" && mode != "rs" && mode != "push" && mode != "rh")
       throw spb::ArgumentError("comm: SPB_COMM must be rh, push, p2p, nccl, rs or nvls");
     if (mode == "rh" && (nranks & (nranks - 1)))

@@ -98,8 +98,11 @@ struct GemmCfg {
   // W_lo, mom} x one 32 x 32 fp32 tile (4 KB, 128B-swizzled).
   static constexpr int kEpiTile = 32 * 32 * 4;
   static constexpr int kEpiBytes = TMA_UPD ? 4 * 2 * 3 * kEpiTile : 0;
+  // Routed kEpiStoreScaled epilogue (GemmEpilogue::route): per epilogue warp
+  // one 32 x 32 fp32 block staged with a 33-float row pitch.
+  static constexpr int kRouteBytes = 4 * 32 * 33 * 4;
   // stages | barrier page (1 KB) | epilogue tiles | + 1 KB alignment slack
-  static constexpr int kSmem = kStages * kStageBytes + (TMA_UPD ? 1024 + kEpiBytes : 256) + 1024;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + (TMA_UPD ? kEpiBytes : kRouteBytes) + 1024;
   static_assert(kSmem <= 232448, "exceeds 227 KB of dynamic shared memory");
 };
 
@@ -548,6 +551,38 @@ __global__ void __launch_bounds__(256, 1)
             }
           }
           __syncwarp();
+        }
+      } else if (EPI == kEpiStoreScaled && ep.route_rows > 0) {
+        // Rows routed to peer memory (multi-GPU push exchange): stage each
+        // 32 x 32 block in shared memory so that one warp store writes four
+        // 128-byte row segments over NVLink instead of 32 scattered 16-byte
+        // pieces (row-per-lane order).
+        float* stg = reinterpret_cast<float*>(epi_smem) + q * (32 * 33);
+        const int rbase = m0 + static_cast<int>(q * 32);
+        const int cc = 4 * static_cast<int>(lane & 7);
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          if (n0 + c0 < ep.N) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = ep.alpha * acc[c0 + j];
+            __syncwarp();
+            const int gcol = n0 + c0 + cc;
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int r = it * 4 + static_cast<int>(lane >> 3);
+              const int grow = rbase + r;
+              if (grow < ep.M && gcol < ep.N) {
+                const float* sp = stg + r * 33 + cc;
+                float* dp = store_addr(ep, grow, gcol, 0);
+                if (gcol + 3 < ep.N) {
+                  *reinterpret_cast<float4*>(dp) = make_float4(sp[0], sp[1], sp[2], sp[3]);
+                } else {
+                  for (int t = 0; t < 4 && gcol + t < ep.N; ++t) dp[t] = sp[t];
+                }
+              }
+            }
+            __syncwarp();
+          }
         }
       } else {
 #pragma unroll

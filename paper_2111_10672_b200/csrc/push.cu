@@ -16,10 +16,14 @@
 //   3. the owner waits for every rank's G[l], then push_update_kernel sums
 //      the contributions in rank order (the p2p mode's order: identical bits),
 //      applies momentum / weight decay / SGD to its rows (hi, lo, momentum)
-//      and stores the new fp32 weights into every peer's w32 (NVLink stores),
-//      then signals U[l];
-//   4. every rank waits for every owner's U[l] and splits the received rows
+//      and writes the new fp32 rows to its w32, then signals U[l];
+//   4. every rank waits for each owner's U[l], pulls its rows with the copy
+//      engines (as in the p2p mode; the first version stored them into every
+//      peer from the update kernel, which ran at ~130 GB/s) and splits them
 //      w32 -> (hi, lo) (p2p_split_kernel / push_split_kernel).
+// The GEMM epilogue stages each 32 x 32 block in shared memory so that the
+// NVLink stores are 128-byte row segments (gemm_tf32x3.cuh; the first version
+// stored row-per-lane 16-byte pieces at ~115 GB/s).
 #include <cuda_runtime.h>
 
 #include <cstdint>
