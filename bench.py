@@ -483,7 +483,8 @@ def run_b200(args, world, rank, local, dist):
         line["roofline"]["nvlink"] = {
             "bound": "nvlink", "achieved": round(nv, 1), "peak": NVLINK_GBS, "unit": "GB/s",
             "frac": round(nv / NVLINK_GBS, 4), "bytes_per_step": comm_bytes,
-            "note": f"{comm_mode}: bytes this rank pulls (p2p / rh) or reduces (nccl buckets, algorithmic) per step, "
+            "note": f"{comm_mode}: bytes this rank pulls (p2p / rh), pushes + pulls (push: gradient rows stored to "
+                    "their owners, weight rows pulled) or reduces (nccl buckets, algorithmic) per step, "
                     "max over ranks, averaged over the whole step; peak = measured one-peer copy-engine bandwidth "
                     "per direction (profiles/r01_nvlink_copy_engine.txt)"}
     barrier(dist)

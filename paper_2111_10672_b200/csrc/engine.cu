@@ -1484,7 +1484,9 @@ struct Engine {
     launch_push_signal(peer_flags, 2 * l, nranks, rank, epoch_dev, chain_sub,
                        mine && rows_in_signal ? grad + w_off[l] : nullptr, ldw, mine ? grad + b_off[l] : nullptr, rpo,
                        w[l], wdst, bdst, gs);
-    pend(kClsComm, 0, gs);
+    // Bytes this rank sends to the owners (the wgrad epilogue's routed rows
+    // and the bias rows): its share of the exchange, like a pull elsewhere.
+    pend(kClsComm, mine ? static_cast<double>(w[l] - (r1 - r0)) * (ldw + 1) * 4.0 : 0.0, gs);
     SPB_CUDA(cudaEventRecord(evl(0), s));  // dgrad_l issued on s before this point
     SPB_CUDA(cudaEventRecord(ev(kEvBucket + l), gs));
     // 2. owner update on s3: every rank's G[l], own gradient final, dgrad_l
