@@ -149,24 +149,46 @@ def barrier(dist):
         dist.barrier()
 
 
-def cpu_reference(cfg, steps: int, warmup: int, bw: int):
-    """The unmodified reference SPB core (oracle/_ref) on cfg's shape with
-    per-worker batch `bw`, worker threads = min(k, nproc). Falls back to the
-    C restatement when _ref is absent. Returns (samples/s, kind, cores, sample)."""
+def host_info() -> dict:
+    """The host the CPU numbers were taken on."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def bench_config(cfg, world: int) -> dict:
+    """The workload description shared by BOTH arms (b200 and reference), so
+    the driver's same-config check compares like with like."""
+    k = cfg["k"]
+    return {"workload": cfg["workload"], "widths": "4096x16+1", "k": k, "per_worker_batch": cfg["bw"],
+            "global_batch": k * cfg["bw"], "dataset": cfg["N"], "parallelism": f"spb-dp{world} (workers/rank {k // world})",
+            "l2": "inputs exceed L2 (2 GB weights)"}
+
+
+def cpu_reference(cfg, steps: int, warmup: int, bw: int, threads: int):
+    """The unmodified reference SPB core (oracle/_ref: spb.cpp + model.cpp
+    compiled from the reference's sources) on cfg's shape with per-worker
+    batch `bw`, on data from the reference's OWN generator
+    make_random_chain_mlp (model.cpp:208-231, via ref_chain_random) -- so
+    this process never loads the B200 library. `threads` workers run
+    concurrently (1 = the reference as shipped; > 1 is the k-thread harness,
+    legal because its model methods are const and thread-safe,
+    model.hpp:21-25). Falls back to the C restatement when _ref is absent.
+    Returns (samples/s, kind, threads, sample, ms per step)."""
     from oracle.oracle import REF_SO
 
     widths, k = cfg["widths"], cfg["k"]
-    threads = max(1, min(k, os.cpu_count() or 1))
-    from paper_2111_10672_b200 import spb
-
-    X, Y, W = spb.gen_chain_mlp(widths, cfg["N"], cfg["data_seed"])
-    X64, Y64 = X.astype(np.float64), Y[:, :1].astype(np.float64)
-    W64 = [b.astype(np.float64) for b in W]
-    del X, Y, W
     if os.path.exists(REF_SO):
         from oracle.oracle import Ref, RefModel
 
-        m = RefModel(Ref(), widths, X64, Y64, W64)
+        m = RefModel(Ref(), widths, samples=cfg["N"], seed=cfg["data_seed"])
         kind = "reference"
         for s in range(1, warmup + 1):
             m.step(k, k * bw, cfg["lr"], cfg["step_seed"], s, False, threads)
@@ -176,30 +198,34 @@ def cpu_reference(cfg, steps: int, warmup: int, bw: int):
 
         o = Oracle()
         kind, threads = "port", 1
+        X, Y, W = o.gen_chain_mlp(widths, cfg["N"], cfg["data_seed"])
         for s in range(1, warmup + 1):
-            o.spb_step(widths, X64, Y64, W64, k, k * bw, cfg["lr"], cfg["step_seed"], s)
+            o.spb_step(widths, X, Y, W, k, k * bw, cfg["lr"], cfg["step_seed"], s)
         t0 = time.perf_counter()
         for s in range(warmup + 1, warmup + 1 + steps):
-            o.spb_step(widths, X64, Y64, W64, k, k * bw, cfg["lr"], cfg["step_seed"], s)
+            o.spb_step(widths, X, Y, W, k, k * bw, cfg["lr"], cfg["step_seed"], s)
         t = time.perf_counter() - t0
     value = steps * k * bw / t
-    sample = (f"{steps} SPB step(s) of {cfg['workload'].split(':')[0]} widths with {bw} sample(s)/worker "
-              f"({k * bw} samples/step) after {warmup} warm-up, fp64, {threads} worker thread(s); "
-              f"cost is linear in samples (per-sample loop spb.cpp:63)")
-    return value, kind, threads, sample
+    sample = (f"{steps} SPB step(s) of {cfg['workload'].split(':')[0]} (widths 4096x16+1, k={k}) with {bw} sample(s) "
+              f"per worker ({k * bw} samples/step) after {warmup} warm-up, fp64, plain SGD x -= lr g (the reference's "
+              f"only update rule), {threads} worker thread(s); the reference's cost is per sample (per-sample loop "
+              f"spb.cpp:63) plus a per-step allocation of each worker's gradient, included here")
+    return value, kind, threads, sample, 1e3 * t / steps
 
 
 def run_reference_arm(args, world, rank):
     cfg = CFG3
     if rank != 0:
         return
-    value, kind, cores, sample = cpu_reference(cfg, max(1, args.steps), max(0, args.warmup), REF_BW)
+    threads = max(1, min(cfg["k"], os.cpu_count() or 1))
+    value, kind, cores, sample, ms = cpu_reference(cfg, max(1, args.steps), max(0, args.warmup), REF_BW, threads)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator make_random_chain_mlp)",
-            "config": {"workload": cfg["workload"], "k": cfg["k"], "per_worker_batch_sampled": REF_BW,
-                       "global_batch": cfg["k"] * REF_BW},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (the reference's own generator make_random_chain_mlp, seed 7)",
+            "config": bench_config(cfg, args.gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+                             "host": host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -226,7 +252,7 @@ def roofline_of(prof: dict, peaks, traffic=None):
     upd = prof["update"]
     upd_gbs = upd["work"] / (upd["ms"] * 1e-3) / 1e9 if upd["ms"] > 0 else 0.0
     return {
-        "bound": "tensor", "kernel": "forward GEMM: gemm_tf32x3_2sm_kernel (tcgen05.mma cta_group::2 kind::tf32, 3xTF32)",
+        "bound": "tensor", "kernel": f"forward GEMM: {FWD_KERNEL} (tcgen05.mma cta_group::2 kind::tf32, 3xTF32)",
         "achieved": round(6.0 * fwd_tf, 2), "peak": bf16, "unit": "TFLOP/s", "frac": round(6.0 * fwd_tf / bf16, 4),
         "traffic": traffic,
         "peak_source": f"{src} bf16_tflops (burst): every launch of the profiled step is timed alone (serialised, "
@@ -240,15 +266,26 @@ def roofline_of(prof: dict, peaks, traffic=None):
         "update_kernel": {"bound": "hbm", "achieved": round(upd_gbs, 1), "peak": hbm, "unit": "GB/s",
                           "frac": round(upd_gbs / hbm, 4) if hbm else None, "bytes_per_step": upd["work"],
                           "ms_per_step": round(upd["ms"], 4), "launches_per_step": upd["launches"],
-                          "note": "the per-layer update kernels of the unfused layers (28 B/param with momentum)"},
+                          "traffic_bytes_per_step": upd["work"] * 28.0 / 20.0,
+                          "note": "the per-layer update kernels of the unfused layers; achieved counts the algorithmic "
+                                  "20 B/param (read w, g, mom; write w, mom -- BASELINE.md section 4); the weights' "
+                                  "exact 3xTF32 split-pair storage moves 28 B/param (traffic_bytes_per_step)"},
     }
 
 
+FWD_KERNEL = "gemm_tf32x3_2sm_kernel<0,0,0,240>"  # the cfg3 forward GEMM the planner ships
+
+
 def traffic_from_profiles():
-    p = os.path.join(ROOT, "profiles", "r01_gemm_fwd_ncu_full.json")
+    """dram__bytes_read + write per launch of the SHIPPED forward kernel, from
+    the committed `ncu --set full` capture of that same kernel
+    (profiles/r02_gemm_fwd_ncu_full.json, tools/ncu_summary.py)."""
+    p = os.path.join(ROOT, "profiles", "r02_gemm_fwd_ncu_full.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("dram_bytes_per_launch")
+            d = json.load(open(p))
+            if FWD_KERNEL in d.get("kernel", "").replace(" ", ""):
+                return d.get("dram_bytes_per_launch")
         except Exception:  # noqa: BLE001
             return None
     return None
@@ -456,10 +493,8 @@ def run_b200(args, world, rank, local, dist):
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W_,
         "ms_per_step": round(ms / K, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05)", "data": "synthetic (reference generator make_random_chain_mlp, seed 7)",
-        "config": {"workload": cfg["workload"], "widths": "4096x16+1", "k": k, "per_worker_batch": bw,
-                   "global_batch": k * bw, "dataset": cfg["N"], "optimizer": "momentum 0.9, wd 1e-4, lr 0.01",
-                   "parallelism": f"spb-dp{world} (workers/rank {len(workers)})", "l2": "inputs exceed L2 (2 GB weights)",
-                   "aggregation": comm_mode or "local (1 GPU)",
+        "config": bench_config(cfg, world),
+        "engine": {"optimizer": "momentum 0.9, wd 1e-4, lr 0.01", "aggregation": comm_mode or "local (1 GPU)",
                    "graph_chain": (max(1, min(16, int(os.environ["SPB_CHAIN"]))) if "SPB_CHAIN" in os.environ
                                    else 1)},
         "spb_savings": spb_savings(widths, k, bw, world),
@@ -500,8 +535,13 @@ def run_b200(args, world, rank, local, dist):
     except Exception as ex:  # noqa: BLE001
         line["cfg2_mlp"] = {"error": repr(ex)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, kind, cores, sample = cpu_reference(cfg, 1, 0, REF_BW)
-        line["cpu_baseline"] = {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+        # the reference is single-threaded -> 1 core is
+        # the baseline; the k-thread harness (one worker per thread) beside it.
+        v, kind, cores, sample, _ = cpu_reference(cfg, 1, 0, 1, 1)
+        v8, _, t8, sample8, _ = cpu_reference(cfg, 1, 0, REF_BW, max(1, min(cfg["k"], os.cpu_count() or 1)))
+        line["cpu_baseline"] = {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+                                "host": host_info(),
+                                "threaded_harness": {"value": round(v8, 3), "cores": t8, "sample": sample8}}
     if rank == 0:
         print(json.dumps(line), flush=True)
 

@@ -210,6 +210,9 @@ struct Engine {
   // 2 = peer-to-peer copy-engine pulls (p2p.cu), 3 = NCCL reduce-scatter +
   // sharded update + all-gather of the fp32 weights ("rs").
   int comm_mode = 0;
+  // SMs the persistent GEMMs of this context leave free (spb_comm_init: 16
+  // with NCCL collectives in the step, 0 for the copy-engine modes).
+  int reserved_sms = 0;
   // p2p mode: fp32 weights (own shards published to the peers), epoch-stamped
   // flags [2 * (L + 1)][nranks], gradient staging [2][nranks - 1][shard], and
   // the peers' IPC-mapped grad / w32 / flags.
@@ -821,6 +824,7 @@ struct Engine {
   int enqueue_pass(int rows, const std::vector<int>& row0, const std::vector<float>& alpha, cudaStream_t s,
                    const std::function<int(int, cudaStream_t)>& on_grad = nullptr, bool fused = false,
                    int* step_dev = nullptr, const std::function<void(int, cudaStream_t)>& on_layer = nullptr) {
+    SmReserve reserve(reserved_sms);  // this context's SMs-left-free for its collectives
     if (conv_model) return enqueue_pass_conv(rows, row0, alpha, s, on_grad, step_dev, on_layer);
     int n = 0;
     // Forward, hidden layers (mlp_forward model.cpp:108-128 batched).
@@ -1181,8 +1185,14 @@ struct Engine {
       const long a0 = lo_of(s0), a1 = lo_of(s1), len = a1 - a0;
       const bool theirs = (covers(p, b) & contrib) != 0;
       cudaStream_t cs = gpull[p];
-      // Staging reuse: the buffer of layer l % 2 was last read by layer l + 2's update.
-      if (k == 0 && l + 2 <= L) SPB_CUDA(cudaStreamWaitEvent(cs, ev(kEvP2pLayer + 32 * (l + 2) + 1), 0));
+      // Staging reuse: the buffer of layer l % 2 was last read by layer l + 2's
+      // update, or (top layers, chained step) by layer 1 / 2's update of the
+      // previous step -- the same explicit wait as the p2p mode, instead of
+      // relying on the transitive cross-rank flag ordering alone.
+      if (k == 0 && l + 2 <= L)
+        SPB_CUDA(cudaStreamWaitEvent(cs, ev(kEvP2pLayer + 32 * (l + 2) + 1), 0));
+      else if (k == 0 && chain_sub > 0 && l + 2 - L >= 1 && l + 2 - L <= 2)
+        SPB_CUDA(cudaStreamWaitEvent(cs, ev(kEvP2pLayer + 32 * ((l % 2) == 1 ? 1 : 2) + 1), 0));
       if (k > 0) SPB_CUDA(cudaStreamWaitEvent(cs, evl(3 + k - 1 + 8), 0));  // my previous round's sum done
       tbeg(cs);
       launch_p2p_wait(flags, k == 0 ? slot(0) : slot(k), nranks, 1u << p, epoch_dev, chain_sub, cs);
@@ -1752,7 +1762,10 @@ struct Engine {
       const long off = w_off[l], cnt = b_off[l] + round_up(w[l], 32) - w_off[l];
       pbeg(us);
       launch_sgd_update(p_hi + off, p_lo + off, grad + off, mom ? mom + off : nullptr, cnt, lr, mu, wd, us);
-      pend(kClsUpdate, static_cast<double>(cnt) * 4.0 * (mom ? 7 : 5), us);
+      // Algorithmic bytes: read w, g (+ mom), write w
+      // (+ mom), 4 B each, over the layer's real parameters. The split-pair
+      // storage moves 28 B / 20 B per stored element (hi and lo for w).
+      pend(kClsUpdate, static_cast<double>(w[l]) * (fan[l] + 1) * (mom ? 20.0 : 12.0), us);
       ++n;
       if (us != s) {  // W_l final on us
         SPB_CUDA(cudaEventRecord(ev(ev_ready(l)), us));
@@ -1921,7 +1934,8 @@ spb_status spb_create_conv(const int* geom, int nconv, int nout, int k, int per_
 spb_status spb_destroy(spb_ctx* ctx) {
   if (ctx) {
     cudaSetDevice(ctx->e.dev);
-    cudaStreamSynchronize(ctx->e.st);
+    if (cudaStreamSynchronize(ctx->e.st) == cudaSuccess && ctx->e.loss_pin)
+      ctx->e.flush_losses();  // spb_step_host_async losses not yet handed out
     delete ctx;
   }
   return SPB_OK;
@@ -2080,25 +2094,42 @@ spb_status spb_aggregate(spb_ctx* ctx, int k, int L, const float* const* blocks,
       for (int wkr = k - m + 1; wkr <= k; ++wkr)
         if (dims[(wkr - 1) * L + l - 1] != dim) throw spb::ProtocolError("aggregate: block dimension mismatch");
     }
+    // One staging allocation for every layer (RAII: freed on any throw), the
+    // copies and per-layer reductions queued on the context stream, one sync.
+    std::vector<long> base(L + 1, 0), pbase(L + 1, 0);
     for (int l = 1; l <= L; ++l) {
       const int m = chunk_of[l - 1];
       const long dim = dims[(k - m) * L + l - 1];
-      float* stage = Engine::alloc<float>(dim * (m + 1));
-      const float** ptrs = nullptr;
-      SPB_CUDA(cudaMalloc(&ptrs, m * sizeof(float*)));
-      std::vector<const float*> hp(m);
-      for (int i = 0; i < m; ++i) {
-        hp[i] = stage + i * dim;
-        SPB_CUDA(cudaMemcpyAsync(stage + i * dim, blocks[(k - m + i) * L + l - 1], dim * 4, cudaMemcpyHostToDevice,
-                                 e.st));
-      }
-      SPB_CUDA(cudaMemcpyAsync(ptrs, hp.data(), m * sizeof(float*), cudaMemcpyHostToDevice, e.st));
-      spb::launch_aggregate(ptrs, m, dim, stage + m * dim, e.st);
-      SPB_CUDA(cudaMemcpyAsync(out[l - 1], stage + m * dim, dim * 4, cudaMemcpyDeviceToHost, e.st));
-      SPB_CUDA(cudaStreamSynchronize(e.st));
-      cudaFree(stage);
-      cudaFree(ptrs);
+      base[l] = base[l - 1] + spb::round_up(dim * (m + 1), 32);
+      pbase[l] = pbase[l - 1] + m;
     }
+    struct DevBuf {
+      void* p = nullptr;
+      ~DevBuf() {
+        if (p) cudaFree(p);
+      }
+    } stage_buf, ptr_buf;
+    SPB_CUDA(cudaMalloc(&stage_buf.p, std::max(1L, base[L]) * sizeof(float)));
+    SPB_CUDA(cudaMalloc(&ptr_buf.p, std::max(1L, pbase[L]) * sizeof(float*)));
+    float* stage = static_cast<float*>(stage_buf.p);
+    const float** ptrs = static_cast<const float**>(ptr_buf.p);
+    std::vector<const float*> hp(pbase[L]);
+    for (int l = 1; l <= L; ++l) {
+      const int m = chunk_of[l - 1];
+      const long dim = dims[(k - m) * L + l - 1];
+      for (int i = 0; i < m; ++i) hp[pbase[l - 1] + i] = stage + base[l - 1] + i * dim;
+    }
+    SPB_CUDA(cudaMemcpyAsync(ptrs, hp.data(), hp.size() * sizeof(float*), cudaMemcpyHostToDevice, e.st));
+    for (int l = 1; l <= L; ++l) {
+      const int m = chunk_of[l - 1];
+      const long dim = dims[(k - m) * L + l - 1];
+      float* st = stage + base[l - 1];
+      for (int i = 0; i < m; ++i)
+        SPB_CUDA(cudaMemcpyAsync(st + i * dim, blocks[(k - m + i) * L + l - 1], dim * 4, cudaMemcpyHostToDevice, e.st));
+      spb::launch_aggregate(ptrs + pbase[l - 1], m, dim, st + m * dim, e.st);
+      SPB_CUDA(cudaMemcpyAsync(out[l - 1], st + m * dim, dim * 4, cudaMemcpyDeviceToHost, e.st));
+    }
+    SPB_CUDA(cudaStreamSynchronize(e.st));  // also orders the frees after the copies
   });
 }
 
@@ -2111,7 +2142,10 @@ spb_status spb_train_steps(spb_ctx* ctx, uint64_t seed, int step0, int steps, in
     spb::Ctl c{seed, step0, 0};
     SPB_CUDA(cudaMemcpyAsync(e.ctl, &c, sizeof c, cudaMemcpyHostToDevice, e.st));
     e.run_steps(full_backprop != 0, steps, losses);
-    if (losses) SPB_CUDA(cudaStreamSynchronize(e.st));
+    if (losses) {
+      SPB_CUDA(cudaStreamSynchronize(e.st));
+      e.flush_losses();
+    }
   });
 }
 
@@ -2127,6 +2161,7 @@ spb_status spb_step_host(spb_ctx* ctx, const float* X_rows, const float* Y_rows,
     SPB_CUDA(cudaGraphLaunch(g, e.st));
     SPB_CUDA(cudaMemcpyAsync(loss_out, e.loss_dev, 4, cudaMemcpyDeviceToHost, e.st));
     SPB_CUDA(cudaStreamSynchronize(e.st));
+    e.flush_losses();  // earlier spb_step_host_async steps are complete too
   });
 }
 
@@ -2230,9 +2265,6 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     e.rank = rank;
     e.nranks = nranks;
     SPB_CUDA(cudaStreamCreateWithFlags(&e.cst, cudaStreamNonBlocking));
-    // NCCL's kernels need SMs while the backward GEMMs run: keep some free.
-    const char* rs = std::getenv("SPB_COMM_SMS");
-    spb::gemm_reserve_sms(rs ? std::atoi(rs) : 16);
     e.buckets[0] = spb::bucket_plan(e.k, e.L, nranks, false);
     e.buckets[1] = spb::bucket_plan(e.k, e.L, nranks, true);
     e.set_workers(spb::rank_workers(e.k, e.L, rank, nranks));
@@ -2248,6 +2280,10 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
         cm ? cm : (nranks == 2 ? "p2p" : (nranks == 4 ? (e.conv_model ? "rh" : "push") : "nccl"));
     if (mode != "p2p" && mode != "nccl" && mode != "nvls" && mode != "rs" && mode != "push" && mode != "rh")
       throw spb::ArgumentError("comm: SPB_COMM must be rh, push, p2p, nccl, rs or nvls");
+    // NCCL's kernels need SMs while the backward GEMMs run: keep some free
+    // (the copy-engine modes' few SM kernels measured the same with 0 / 16).
+    const char* rs = std::getenv("SPB_COMM_SMS");
+    e.reserved_sms = rs ? std::max(0, std::atoi(rs)) : ((mode == "nccl" || mode == "rs" || mode == "nvls") ? 16 : 0);
     if (mode == "rh" && (nranks & (nranks - 1)))
       throw spb::ArgumentError("comm: rh mode needs a power-of-two rank count");
     if (nranks > 1 && mode == "p2p") e.setup_p2p();

@@ -81,7 +81,11 @@ CUtensorMap tmap2d(const float* base, long inner, long outer, long ld, int box_i
   return m;
 }
 
-int g_reserved_sms = 0;  // SMs left free for concurrent NCCL kernels (multi-GPU)
+// SMs left free for concurrent NCCL kernels (multi-GPU). Thread-local and
+// set per launch sequence by the engine context that owns the communicator
+// (SmReserve in engine.cu), so one context's reservation never leaks into
+// another context's GEMMs.
+thread_local int g_reserved_sms = 0;
 
 // SMs a persistent GEMM grid may occupy.
 int num_sms() {
@@ -236,6 +240,7 @@ void launch_splitk(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
 
 int g_force_variant = -1;  // -1 auto, 0 = 1-CTA 128x128, 1 = CTA pair
 Plan g_force_plan{false, 0, 0};  // splits == 0: not forced
+Plan g_last_plan{false, 1, 128};  // the plan of the last gemm_tf32x3 launch (test hook)
 
 // Wave-quantised cost model (microseconds), fitted on B200 to the plan
 // sweep of tests/native/gemm_bench.cu (`gemm_bench 10 sweep`: every plan on
@@ -369,7 +374,17 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
   return 1;
 }
 
-void gemm_reserve_sms(int n) { g_reserved_sms = n < 0 ? 0 : n; }
+int gemm_reserve_sms(int n) {
+  const int prev = g_reserved_sms;
+  g_reserved_sms = n < 0 ? 0 : n;
+  return prev;
+}
+
+void gemm_last_plan(int* two_sm, int* pn, int* splits) {
+  *two_sm = g_last_plan.two_sm ? 1 : 0;
+  *pn = g_last_plan.pn;
+  *splits = g_last_plan.splits;
+}
 
 int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue& ep, cudaStream_t s) {
   if (A.k != B.k) throw std::invalid_argument("gemm: K mismatch");
@@ -382,6 +397,7 @@ int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue&
                                                      epi == kEpiFwdLinear || epi == kEpiStoreScaled);
   const Plan plan = plan_gemm(A.mn, B.mn, A.k, ep.splitk_ws && !no_split ? ep.splitk_ws_floats : 0, can_split,
                               narrow_pair_ok(A, B, epi), true, A.mn_major && B.mn_major);
+  g_last_plan = plan;
   if (plan.splits > 1) {
     switch (epi) {
       case kEpiFwdTanh: launch_splitk<kEpiFwdTanh>(A, B, ep, s, plan); break;
@@ -395,6 +411,7 @@ int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue&
   // The in-place optimizer epilogue is HBM bound: it always takes the 1-CTA
   // kernel with TMA-staged W / momentum tiles (unless a test forces the pair kernel).
   if (epi == kEpiWgradUpdate && g_force_variant != 1) {
+    g_last_plan = {false, 1, BN};
     launch_inst<BN, true, true, kEpiWgradUpdate, true>(A, B, ep, s);
     return 1;
   }
@@ -410,6 +427,7 @@ int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue&
     }
     return 1;
   }
+  g_last_plan.pn = B.mn <= 64 && epi != kEpiWgradUpdate ? 64 : BN;
   if (B.mn <= 64 && epi != kEpiWgradUpdate) {  // narrow outputs (64-channel convs): 128 x 64 tiles, no idle MMA half
     switch (epi) {
       case kEpiFwdTanh: dispatch_major<64, kEpiFwdTanh>(A, B, ep, s); break;

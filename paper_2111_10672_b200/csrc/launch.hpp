@@ -64,8 +64,17 @@ void gemm_force_variant(int v);
 // Tuning aid: force every GEMM onto one plan (two_sm: CTA-pair kernel of
 // width pn; splits K-splits); splits = 0 restores the planner.
 void gemm_force_plan(int two_sm, int pn, int splits);
-// Persistent GEMM grids leave n SMs free (for NCCL kernels running beside them).
-void gemm_reserve_sms(int n);
+// Test hook: the plan of the last gemm_tf32x3 call (CTA pair?, tile width, K-splits).
+void gemm_last_plan(int* two_sm, int* pn, int* splits);
+// Persistent GEMM grids launched by this thread leave n SMs free (for NCCL
+// kernels running beside them); returns the previous value.
+int gemm_reserve_sms(int n);
+// Scoped reservation: the engine wraps each launch sequence of a context.
+struct SmReserve {
+  int prev;
+  explicit SmReserve(int n) : prev(gemm_reserve_sms(n)) {}
+  ~SmReserve() { gemm_reserve_sms(prev); }
+};
 
 // ---- non-GEMM kernels (kernels.cu) ----
 // H0 / Ybatch rows from the dataset. Indices come from `idx` (host-provided,

@@ -404,7 +404,29 @@ class ChainMlp:
                                               _fp(buf) if buf is not None else None), self._ctx)
         return buf[:steps] if buf is not None else None
 
+    def _check_host_rows(self, X_rows, Y_rows):
+        """The C side copies hosted_rows * n_0 and hosted_rows * n_L floats
+        straight from these pointers (possibly later, on a copy stream): the
+        arrays must be exactly that, float32 and C-contiguous. No silent
+        conversion -- a temporary copy could be freed before an asynchronous
+        copy reads it."""
+        rows = self.hosted_workers * self.per_worker_batch
+        for name, a, cols in (("X_rows", X_rows, self._row_width()), ("Y_rows", Y_rows, self.widths[-1])):
+            if not isinstance(a, np.ndarray) or a.dtype != np.float32 or not a.flags.c_contiguous:
+                raise ArgumentError(f"{name}: need a C-contiguous float32 numpy array")
+            if a.size != rows * cols or (a.ndim == 2 and a.shape != (rows, cols)):
+                raise ArgumentError(f"{name}: need shape ({rows}, {cols}), got {a.shape}")
+
+    def _row_width(self) -> int:
+        return self.widths[0]
+
+    @property
+    def hosted_workers(self) -> int:
+        """Workers whose rows this rank's steps consume (all k on one GPU)."""
+        return getattr(self, "_hosted", self.k)
+
     def step_host(self, X_rows: np.ndarray, Y_rows: np.ndarray, full_backprop: bool = False) -> float:
+        self._check_host_rows(X_rows, Y_rows)
         loss = np.zeros(1, dtype=np.float32)
         _check(load_library().spb_step_host(self._ctx, _fp(X_rows), _fp(Y_rows), int(full_backprop), _fp(loss)),
                self._ctx)
@@ -414,7 +436,9 @@ class ChainMlp:
         """spb_step_host_async: enqueue one step on host rows (pinned for an
         asynchronous copy); loss_out (float32, >= 1 element) receives the
         loss. The arrays must stay alive and unchanged until synchronize()."""
-        assert loss_out.dtype == np.float32 and X_rows.dtype == np.float32 and Y_rows.dtype == np.float32
+        self._check_host_rows(X_rows, Y_rows)
+        if not isinstance(loss_out, np.ndarray) or loss_out.dtype != np.float32 or loss_out.size < 1:
+            raise ArgumentError("loss_out: need a float32 numpy array with >= 1 element")
         _check(load_library().spb_step_host_async(self._ctx, _fp(X_rows), _fp(Y_rows), int(full_backprop),
                                                   _fp(loss_out)), self._ctx)
 
@@ -442,6 +466,7 @@ class ChainMlp:
         buf = (C.c_char * 128).from_buffer_copy(unique_id)
         _check(load_library().spb_comm_init(self._ctx, C.cast(buf, C.c_void_p), rank, nranks), self._ctx)
         self.rank, self.nranks = rank, nranks
+        self._hosted = len(rank_workers(self.k, self.layer_count(), rank, nranks))
 
     def comm_init_torch(self, dist, rank: int, nranks: int):
         """Rendezvous through an initialised torch.distributed group (plumbing only)."""
@@ -539,6 +564,10 @@ class ConvNet(ChainMlp):
         self._N = X.shape[0]
         self._initial = [np.asarray(b, dtype=np.float32).copy() for b in weights]
         self.set_params(self._initial)
+
+    def _row_width(self) -> int:
+        h, w, c = self.in_shape
+        return h * w * c
 
 
 def convnet_block_dims(in_shape, convs, nout: int) -> List[int]:

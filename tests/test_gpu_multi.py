@@ -145,7 +145,7 @@ def _rank_chain(rank, world, port, out_dir, mode, chain):
     _rank(rank, world, port, out_dir, False, mode, 0.9, 1e-3, chain=chain, steps=7)
 
 
-@pytest.mark.parametrize("mode", ["push", "p2p", "nccl"])
+@pytest.mark.parametrize("mode", ["push", "p2p", "rh", "nccl"])
 def test_multi_gpu_chained_graph_bitwise(tmp_path, mode):
     """Cross-step pipelining (spb_set_chain): with 7 iterations captured in one
     graph, iteration t+1's forward of layer l waits only for W_l of

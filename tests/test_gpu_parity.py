@@ -433,3 +433,21 @@ def test_step_host_async_equals_step_host():
     assert np.array_equal(got, np.array(want, dtype=np.float32))
     for x, y in zip(a.get_params(), b.get_params()):
         assert np.array_equal(x, y)
+
+
+def test_step_host_rejects_bad_host_arrays():
+    """the C side copies hosted_rows x n_0 / n_L floats straight
+    from the pointers, so wrong dtypes, non-contiguous views and short batches
+    are rejected before the call instead of reading garbage."""
+    widths, N, k, bw = [64, 48, 32, 1], 256, 4, 8
+    m, X, Y, W = make(widths, N, 8, k=k, bw=bw)
+    x = np.ascontiguousarray(X[:k * bw], dtype=np.float32)
+    y = np.ascontiguousarray(Y[:k * bw], dtype=np.float32)
+    for bad_x, bad_y in ((x.astype(np.float64), y), (np.asfortranarray(x), y), (x[:-1], y), (x, y[:, :0]),
+                         (np.ascontiguousarray(np.zeros((k * bw, 65), np.float32))[:, :64], y)):
+        with pytest.raises(spb.ArgumentError):
+            m.step_host(bad_x, bad_y)
+        with pytest.raises(spb.ArgumentError):
+            m.step_host_async(bad_x, bad_y, np.zeros(1, np.float32))
+    m.step_host(x, y)
+    m.close()

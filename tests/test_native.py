@@ -2,6 +2,7 @@
 drop-in adapter test. Compiling them needs no GPU (CPU tests); running them
 does (gpu tests)."""
 import os
+import re
 import subprocess
 
 import pytest
@@ -47,6 +48,20 @@ def test_gemm_probe_numerics():
     r = subprocess.run([_build_probe()], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "GEMM PROBE OK" in r.stdout
+
+
+@pytest.mark.gpu
+def test_gemm_probe_benchmark_shapes():
+    """The exact cfg3 GEMM shapes / layouts / epilogues with the planner's own
+    choices (pair 240 forward, pair 192 wgrad at K = 1024, split-K dgrads,
+    the fused-optimizer wgrad at K <= 512) against fp64."""
+    r = subprocess.run([_build_probe(), "shapes"], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "GEMM SHAPES OK" in r.stdout
+    # the plans the 1-GPU cfg3 step ships (profiles/r01_launches_cfg3_summary_v2.json)
+    assert re.search(r"shape forward \(tanh epilogue\)\s+M=1024 N=4096 K=4096 plan=2sm/pn240/sp1", r.stdout)
+    assert re.search(r"shape wgrad \(alpha epilogue\)\s+M=4096 N=4096 K=1024 plan=2sm/pn192/sp1", r.stdout)
 
 
 @pytest.mark.gpu
