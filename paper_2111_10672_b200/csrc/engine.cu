@@ -150,9 +150,10 @@ struct Engine {
   std::vector<float*> Hh, Hl;
   static constexpr int kDbuf = 3;  // Delta_l lives in buffer l % 3
   float *Dh[kDbuf] = {nullptr, nullptr, nullptr}, *Dl[kDbuf] = {nullptr, nullptr, nullptr};
-  float *delta = nullptr, *row_loss = nullptr, *ybatch = nullptr, *scratch = nullptr, *scratch2 = nullptr,
-        *xin = nullptr;
-  long scratch_n = 0;
+  // delta_L (head output error) as a split pair [rows x ldq], ldq = round_up(n_L, 4):
+  // the A operand of the head's wgrad GEMM.
+  float *delta = nullptr, *delta_lo = nullptr, *row_loss = nullptr, *ybatch = nullptr, *xin = nullptr;
+  long ldq = 4;
   int* idx = nullptr;
   int* idx_in = nullptr;
   float* loss_dev = nullptr;
@@ -160,6 +161,8 @@ struct Engine {
   long tmp_n = 0;
   float* splitk_ws = nullptr;  // split-K partials (forward / dgrad GEMMs, stream s only)
   static constexpr long kSplitkWsFloats = 16L << 20;
+  float* splitk_ws2 = nullptr;  // split-K partials of the head wgrad (the gradient stream s2)
+  static constexpr long kSplitkWs2Floats = 1L << 20;
   Ctl* ctl = nullptr;
   int* workers_dev = nullptr;
   std::vector<int> workers;  // hosted workers, ascending
@@ -384,7 +387,8 @@ struct Engine {
       if (p) cudaFree(p);
     };
     f(splitk_ws);
-    f(p_hi), f(p_lo), f(grad), f(mom), f(X), f(Y), f(delta), f(row_loss), f(ybatch), f(scratch), f(scratch2), f(xin), f(idx),
+    f(splitk_ws2);
+    f(p_hi), f(p_lo), f(grad), f(mom), f(X), f(Y), f(delta), f(delta_lo), f(row_loss), f(ybatch), f(xin), f(idx),
         f(idx_in), f(loss_dev), f(tmp), f(ctl), f(workers_dev), f(epoch_dev), f(bar_dev), f(w32), f(flags),
         f(stage), f(pstage), f(trace_dev);
     for (int i = 0; i < 2; ++i) f(hx[i]), f(hy[i]);
@@ -427,6 +431,7 @@ struct Engine {
     bw = bw_;
     dev = device;
     SPB_CUDA(cudaSetDevice(dev));
+    gemm_prepare_device();
     SPB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     SPB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
     SPB_CUDA(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
@@ -456,6 +461,7 @@ struct Engine {
     bw = bw_;
     dev = device;
     SPB_CUDA(cudaSetDevice(dev));
+    gemm_prepare_device();
     SPB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     SPB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
     SPB_CUDA(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
@@ -507,6 +513,7 @@ struct Engine {
     tmp_n = maxblk;
     tmp = alloc<float>(tmp_n);
     splitk_ws = alloc<float>(kSplitkWsFloats);
+    splitk_ws2 = alloc<float>(kSplitkWs2Floats);
     ctl = alloc<Ctl>(1);
     loss_dev = alloc<float>(kMaxChain);
     workers_dev = alloc<int>(k);
@@ -552,8 +559,7 @@ struct Engine {
     for (int i = 0; i < kDbuf; ++i) {
       if (Dh[i]) cudaFree(Dh[i]), cudaFree(Dl[i]);
     }
-    for (void* p : {(void*)delta, (void*)row_loss, (void*)ybatch, (void*)scratch, (void*)scratch2, (void*)xin, (void*)idx,
-                    (void*)idx_in})
+    for (void* p : {(void*)delta, (void*)delta_lo, (void*)row_loss, (void*)ybatch, (void*)xin, (void*)idx, (void*)idx_in})
       if (p) cudaFree(p);
     cap_rows = rows;
     for (int l = 0; l < L; ++l) {
@@ -564,14 +570,11 @@ struct Engine {
       Dh[i] = alloc<float>(rows * ldd);
       Dl[i] = alloc<float>(rows * ldd);
     }
-    delta = alloc<float>(static_cast<long>(rows) * nout);
+    ldq = round_up(nout, 4);
+    delta = alloc<float>(static_cast<long>(rows) * ldq);
+    delta_lo = alloc<float>(static_cast<long>(rows) * ldq);
     row_loss = alloc<float>(rows);
     ybatch = alloc<float>(static_cast<long>(rows) * nout);
-    long sc = colreduce_scratch(rows, static_cast<int>(ldd), 1);
-    for (int l = 1; l <= L; ++l) sc = std::max(sc, colreduce_scratch(rows, w[l - 1], nout));
-    scratch_n = sc;
-    scratch = alloc<float>(sc);
-    scratch2 = alloc<float>(sc);
     xin = alloc<float>(static_cast<long>(rows) * w[0]);
     idx = alloc<int>(rows);
     idx_in = alloc<int>(rows);
@@ -587,7 +590,7 @@ struct Engine {
     for (auto p : Ch) f(p);
     for (auto p : Cl) f(p);
     for (int i = 0; i < kDbuf; ++i) f(Dh[i]), f(Dl[i]);
-    for (void* p : {(void*)delta, (void*)row_loss, (void*)ybatch, (void*)scratch, (void*)scratch2, (void*)xin, (void*)idx,
+    for (void* p : {(void*)delta, (void*)delta_lo, (void*)row_loss, (void*)ybatch, (void*)xin, (void*)idx,
                     (void*)idx_in, (void*)Ph, (void*)Pl, (void*)Gh, (void*)Gl, (void*)dcol, (void*)iota_dev})
       f(p);
     cap_rows = samples;
@@ -596,7 +599,7 @@ struct Engine {
     Hl.assign(L, nullptr);
     Ch.assign(L, nullptr);
     Cl.assign(L, nullptr);
-    long dmax = 1, cmax = 1, sc = colreduce_scratch(samples, static_cast<int>(ld[L - 1]), nout);
+    long dmax = 1, cmax = 1;
     for (int l = 0; l < L; ++l) {
       Hh[l] = alloc<float>(S * pix[l] * ld[l]);
       Hl[l] = alloc<float>(S * pix[l] * ld[l]);
@@ -607,7 +610,6 @@ struct Engine {
         }
         dmax = std::max(dmax, S * pix[l] * ld[l]);
         cmax = std::max(cmax, S * pix[l] * ldf[l]);
-        sc = std::max(sc, colreduce_scratch(static_cast<int>(S * pix[l]), w[l], 1));
       }
     }
     for (int i = 0; i < kDbuf; ++i) Dh[i] = alloc<float>(dmax), Dl[i] = alloc<float>(dmax);
@@ -619,12 +621,11 @@ struct Engine {
     Pl = alloc<float>(S * ld[L - 1]);
     Gh = alloc<float>(S * ld[L - 1]);
     Gl = alloc<float>(S * ld[L - 1]);
-    delta = alloc<float>(S * nout);
+    ldq = round_up(nout, 4);
+    delta = alloc<float>(S * ldq);
+    delta_lo = alloc<float>(S * ldq);
     row_loss = alloc<float>(S);
     ybatch = alloc<float>(S * nout);
-    scratch_n = sc;
-    scratch = alloc<float>(sc);
-    scratch2 = alloc<float>(sc);
     xin = alloc<float>(S * ldx);
     idx = alloc<int>(S);
     idx_in = alloc<int>(S);
@@ -706,19 +707,15 @@ struct Engine {
     pbeg(s);
     launch_avgpool(Hh[Lc], Hl[Lc], ld[Lc], samples, static_cast<int>(pix[Lc]), w[Lc], Ph, Pl, ld[Lc], s);
     launch_head(Ph, Pl, ld[Lc], samples, w[Lc], nout, p_hi + w_off[L], p_lo + w_off[L], ldf[L], p_hi + b_off[L],
-                p_lo + b_off[L], ybatch, delta, row_loss, has_next ? Gh : nullptr, has_next ? Gl : nullptr, ld[Lc],
-                has_next ? row0[Lc] : samples, false, s, /*dn_act=*/false);
+                p_lo + b_off[L], ybatch, delta, delta_lo, ldq, row_loss, has_next ? Gh : nullptr,
+                has_next ? Gl : nullptr, ld[Lc], has_next ? row0[Lc] : samples, false, s, /*dn_act=*/false);
     launch_sum_loss(row_loss, samples, 1.0f / static_cast<float>(samples), loss_dev + chain_sub, step_dev, s);
     pend(kClsHead, 0, s);
     n += 3;
-    if (row0[L] < samples) {
+    if (row0[L] < samples) {  // head wgrad + bias: alpha delta^T [P | 1] over the contributor samples
       pbeg(s);
-      launch_colreduce(Ph, Pl, ld[Lc], row0[L], samples, w[Lc], delta, nout, nout, alpha[L], grad + w_off[L], ldf[L],
-                       scratch, s);
-      launch_colreduce(delta, nullptr, nout, row0[L], samples, nout, nullptr, 1, 0, alpha[L], grad + b_off[L], 0,
-                       scratch, s);
-      pend(kClsColred, 0, s);
-      n += 4;
+      n += enqueue_head_wgrad(Ph, Pl, ld[Lc], row0[L], samples, w[Lc], alpha[L], false, splitk_ws, kSplitkWsFloats, s);
+      pend(kClsWgrad, 2.0 * (samples - row0[L]) * nout * (w[Lc] + 1), s);
     }
     if (on_grad) n += on_grad(L, s);
     if (on_layer) on_layer(L, s);
@@ -771,20 +768,23 @@ struct Engine {
         launch_col2im_tanh(dcol, ldf[l], cg[l], static_cast<int>(row0[l - 1] * pix[l - 1]),
                            static_cast<int>((samples - row0[l - 1]) * pix[l - 1]), Hh[l - 1], Hl[l - 1], ld[l - 1],
                            Dh[bn], Dl[bn], ld[l - 1], s);
-        pend(kClsColred, 0, s);
+        pend(kClsDgrad, 0, s);  // the gather half of the stride-2 dgrad
         ++n;
       }
-      {  // wgrad: dW_l = alpha_l * Delta_l[r0:]^T col_l[r0:]
+      {  // wgrad + bias: [dW_l | db_l] = alpha_l * Delta_l[r0:]^T [col_l[r0:] | 1]
         Operand A{Dh[b] + r0 * ld[l], Dl[b] + r0 * ld[l], ld[l], w[l], static_cast<int>(cnt), true};
         const bool tma = conv_tma(l);
-        Operand B{tma ? nullptr : Ch[l] + r0 * ldf[l], tma ? nullptr : Cl[l] + r0 * ldf[l], ldf[l], fan[l],
-                  static_cast<int>(cnt), true};
+        const int bc = static_cast<int>(round_up(fan[l], 32));  // the fused bias column (ones box)
+        Operand B{tma ? nullptr : Ch[l] + r0 * ldf[l], tma ? nullptr : Cl[l] + r0 * ldf[l], ldf[l], bc + 1,
+                  static_cast<int>(cnt), true, fan[l]};
         GemmEpilogue ep{};
         ep.out_hi = grad + w_off[l];
         ep.ld_out = ldf[l];
         ep.alpha = alpha[l];
         ep.M = w[l];
         ep.N = fan[l];
+        ep.bias_col_p1 = ep.ones_col_p1 = bc + 1;
+        ep.gb_hi = grad + b_off[l];
         ep.splitk_ws = splitk_ws;  // few output tiles, K = pixel rows: split K (single stream)
         ep.splitk_ws_floats = kSplitkWsFloats;
         pbeg(s);
@@ -796,11 +796,6 @@ struct Engine {
         }
         pend(kClsWgrad, 2.0 * cnt * w[l] * fan[l], s);
       }
-      pbeg(s);
-      launch_colreduce(Dh[b], Dl[b], ld[l], static_cast<int>(r0), static_cast<int>(samples * pix[l]), w[l], nullptr, 1,
-                       0, alpha[l], grad + b_off[l], 0, scratch, s);
-      pend(kClsColred, 0, s);
-      n += 2;
       if (on_grad) n += on_grad(l, s);
       if (on_layer) on_layer(l, s);
     }
@@ -852,14 +847,12 @@ struct Engine {
     fwd_gate(L, s);
     pbeg(s);
     launch_head(Hh[L - 1], Hl[L - 1], ld[L - 1], rows, w[L - 1], nout, p_hi + w_off[L], p_lo + w_off[L], ld[L - 1],
-                p_hi + b_off[L], p_lo + b_off[L], ybatch, delta, row_loss, has_next ? Dh[(L - 1) % kDbuf] : nullptr,
+                p_hi + b_off[L], p_lo + b_off[L], ybatch, delta, delta_lo, ldq, row_loss,
+                has_next ? Dh[(L - 1) % kDbuf] : nullptr,
                 has_next ? Dl[(L - 1) % kDbuf] : nullptr, ldd, has_next ? row0[L - 1] : rows, false, s);
     launch_sum_loss(row_loss, rows, 1.0f / static_cast<float>(rows), loss_dev + chain_sub, step_dev, s);
     pend(kClsHead, 0, s);
     n += 2;
-    auto col_upd = [&](long off) {
-      return ColUpdate{p_lo + off, mom ? mom + off : nullptr, lr, mu, wd};
-    };
     // Two streams from here on: the Delta chain (head, dgrads) on s, the
     // gradient reductions (head gradients, wgrads, bias sums) on s2, so
     // dgrad_{L-1} starts right after the head kernel.
@@ -869,19 +862,14 @@ struct Engine {
       SPB_CUDA(cudaStreamWaitEvent(s2, ev(kEvFork), 0));
     }
     cudaStream_t sw = two ? s2 : s;
-    float* const scr = two ? scratch2 : scratch;  // the column-reduction scratch of sw
-    // Head gradients over the contributor rows of layer L (W_L was last read
-    // by the head kernel, so the fused update may rewrite it here).
+    // Head gradients over the contributor rows of layer L: one wgrad GEMM,
+    // alpha_L delta_L^T [H_{L-1} | 1] (weights and bias; never fused with the
+    // optimizer -- enqueue_step keeps layer L unfused).
     if (row0[L] < rows) {
       pbeg(sw);
-      ColUpdate uw = col_upd(w_off[L]), ub = col_upd(b_off[L]);
-      const bool fL = lf(L);
-      launch_colreduce(Hh[L - 1], Hl[L - 1], ld[L - 1], row0[L], rows, w[L - 1], delta, nout, nout, alpha[L],
-                       fL ? p_hi + w_off[L] : grad + w_off[L], ld[L - 1], scr, sw, fL ? &uw : nullptr);
-      launch_colreduce(delta, nullptr, nout, row0[L], rows, nout, nullptr, 1, 0, alpha[L],
-                       fL ? p_hi + b_off[L] : grad + b_off[L], 0, scr, sw, fL ? &ub : nullptr);
-      pend(kClsColred, 0, sw);
-      n += 4;
+      n += enqueue_head_wgrad(Hh[L - 1], Hl[L - 1], ld[L - 1], row0[L], rows, w[L - 1], alpha[L], route_push,
+                              two ? splitk_ws2 : splitk_ws, two ? kSplitkWs2Floats : kSplitkWsFloats, sw);
+      pend(kClsWgrad, 2.0 * (rows - row0[L]) * nout * (w[L - 1] + 1), sw);
     }
     if (on_grad) n += on_grad(L, sw);
     if (on_layer) on_layer(L, sw);  // W_L: read by the head only
@@ -928,35 +916,35 @@ struct Engine {
         SPB_CUDA(cudaEventRecord(ev_delta(l - 1), s));
         SPB_CUDA(cudaStreamWaitEvent(s2, lf(l) ? ev_delta(l - 1) : ev_delta(l), 0));
       }
-      {  // wgrad: dW_l = alpha_l * Delta_l[r0:]^T H_{l-1}[r0:] (or the fused update of W_l)
+      {  // wgrad + bias: [dW_l | db_l] = alpha_l * Delta_l[r0:]^T [H_{l-1}[r0:] | 1] (or the fused update)
+        const int bc = static_cast<int>(round_up(w[l - 1], 32));  // the fused bias column (ones box)
         Operand A{Dh[b] + r0 * ldd, Dl[b] + r0 * ldd, ldd, w[l], cnt, true};
-        Operand B{Hh[l - 1] + r0 * ld[l - 1], Hl[l - 1] + r0 * ld[l - 1], ld[l - 1], w[l - 1], cnt, true};
+        Operand B{Hh[l - 1] + r0 * ld[l - 1], Hl[l - 1] + r0 * ld[l - 1], ld[l - 1], bc + 1, cnt, true, w[l - 1]};
         GemmEpilogue ep{};
         ep.ld_out = ld[l - 1];
         ep.alpha = alpha[l];
         ep.M = w[l];
         ep.N = w[l - 1];
+        ep.bias_col_p1 = ep.ones_col_p1 = bc + 1;
         if (lf(l)) {
           ep.out_hi = p_hi + w_off[l];
           ep.out_lo = p_lo + w_off[l];
           ep.mom = mom ? mom + w_off[l] : nullptr;
+          ep.gb_hi = p_hi + b_off[l];
+          ep.gb_lo = p_lo + b_off[l];
+          ep.gb_mom = mom ? mom + b_off[l] : nullptr;
           ep.lr = lr;
           ep.mu = mu;
           ep.wd = wd;
         } else {
           ep.out_hi = grad + w_off[l];
+          ep.gb_hi = grad + b_off[l];  // local even when the weight rows are routed (the push signal sends it)
           if (route_push) push_route(l, ep);  // rows stored straight to their owners
         }
         pbeg(sw);
         n += gemm_tf32x3(A, B, lf(l) ? kEpiWgradUpdate : kEpiStoreScaled, ep, sw);
         pend(kClsWgrad, 2.0 * cnt * w[l] * w[l - 1], sw);
       }
-      pbeg(sw);
-      ColUpdate ub = col_upd(b_off[l]);
-      launch_colreduce(Dh[b], Dl[b], ldd, r0, rows, w[l], nullptr, 1, 0, alpha[l],
-                       lf(l) ? p_hi + b_off[l] : grad + b_off[l], 0, scratch2, sw, lf(l) ? &ub : nullptr);
-      pend(kClsColred, 0, sw);
-      n += 2;
       if (two) SPB_CUDA(cudaEventRecord(ev_wgrad(l), s2));
       if (on_grad) n += on_grad(l, sw);
       if (on_layer) on_layer(l, sw);  // grad of layer l final on sw; dgrad_l (last W_l reader) done on s
@@ -970,6 +958,29 @@ struct Engine {
       if (on_layer) on_layer(l, s);
     }
     return n;
+  }
+
+  // The head layer's wgrad over rows [r0, rows): [dW_L | db_L] =
+  // alpha delta_L[r0:]^T [H[r0:] | 1] as ONE tcgen05 GEMM (M = n_L <= 16 rows
+  // of one tile, N = n_{L-1} + the fused bias column, K = contributor rows;
+  // split-K over `ws`). The old two column-reduction kernels are gone. In the
+  // push exchange the head's rows travel with the signal, so it is never routed.
+  int enqueue_head_wgrad(const float* h_hi, const float* h_lo, long ldh, int r0, int rows, int n_in, float a,
+                         bool /*push*/, float* ws, long ws_floats, cudaStream_t q) {
+    const int cnt = rows - r0, bc = static_cast<int>(round_up(n_in, 32));
+    Operand A{delta + static_cast<long>(r0) * ldq, delta_lo + static_cast<long>(r0) * ldq, ldq, nout, cnt, true};
+    Operand B{h_hi + static_cast<long>(r0) * ldh, h_lo + static_cast<long>(r0) * ldh, ldh, bc + 1, cnt, true, n_in};
+    GemmEpilogue ep{};
+    ep.out_hi = grad + w_off[L];
+    ep.ld_out = ldf[L];
+    ep.alpha = a;
+    ep.M = nout;
+    ep.N = n_in;
+    ep.bias_col_p1 = ep.ones_col_p1 = bc + 1;
+    ep.gb_hi = grad + b_off[L];
+    ep.splitk_ws = ws;
+    ep.splitk_ws_floats = ws_floats;
+    return gemm_tf32x3(A, B, kEpiStoreScaled, ep, q);
   }
 
   cudaEvent_t ev(size_t i) {
@@ -1668,7 +1679,9 @@ struct Engine {
     fuse_layer.assign(L + 1, 0);
     bool any_unfused = !fused_ok;
     for (int l = 1; l <= L; ++l) {
-      fuse_layer[l] = fused_ok && row0[l] < rows && (fused_mode == 1 || rows - row0[l] <= kFuseMaxRows);
+      // The head (layer L) is never fused: its wgrad is a split-K GEMM, which
+      // has no in-place optimizer epilogue.
+      fuse_layer[l] = fused_ok && l < L && row0[l] < rows && (fused_mode == 1 || rows - row0[l] <= kFuseMaxRows);
       if (!fuse_layer[l]) any_unfused = true;
     }
     const bool per_layer = comm || any_unfused;

@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include <mutex>
+#include <vector>
 
 #include <algorithm>
 #include <cstdlib>
@@ -98,9 +99,29 @@ int num_sms() {
   return std::max(2, (n - g_reserved_sms) & ~1);
 }
 
+// The TMA extent along MN: the operand's real columns (mn_map) when the GEMM
+// extends past them (the fused-bias ones column of a wgrad B operand).
 CUtensorMap operand_map(const Operand& X, const float* base, int tile_rows) {
-  if (!X.mn_major) return tmap2d(base, X.k, X.mn, X.ld, kBK, tile_rows, CU_TENSOR_MAP_SWIZZLE_128B);
-  return tmap2d(base, X.mn, X.k, X.ld, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  const int mn = X.mn_map > 0 ? X.mn_map : X.mn;
+  if (!X.mn_major) return tmap2d(base, X.k, mn, X.ld, kBK, tile_rows, CU_TENSOR_MAP_SWIZZLE_128B);
+  return tmap2d(base, mn, X.k, X.ld, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+}
+
+// Constant boxes for the fused-bias ones column (GemmEpilogue::ones_col_p1):
+// a [64 x 32] fp32 array per device, rows 0-31 ones (the hi half of the
+// column), rows 32-63 zeros (its lo half), read as 32 x 32 MN-major boxes.
+// Allocated once per device by gemm_prepare_device (not capturable).
+const float* g_ones[64] = {};
+
+const float* ones_buffer() {
+  int dev = 0;
+  SPB_CUDA(cudaGetDevice(&dev));
+  if (!g_ones[dev]) throw CudaError("gemm: gemm_prepare_device() was not called on this device");
+  return g_ones[dev];
+}
+
+CUtensorMap ones_map() {
+  return tmap2d(ones_buffer(), 32, 64, 32, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
 template <int BN, bool AM, bool BM_, int EPI, bool TMA_UPD = false, int IC = 0>
@@ -123,12 +144,13 @@ void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cud
   const int units = tiles * ((num_kb + kbs - 1) / kbs);
   const int grid = units < num_sms() ? units : num_sms();
   CUtensorMap wh{}, wl{}, wm{};
-  if (TMA_UPD) {  // the W tile the optimizer epilogue updates in place: [M rows x N cols]
-    wh = tmap2d(ep.out_hi, B.mn, A.mn, ep.ld_out, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-    wl = tmap2d(ep.out_lo, B.mn, A.mn, ep.ld_out, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-    wm = ep.mom ? tmap2d(ep.mom, B.mn, A.mn, ep.ld_out, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B) : wh;
+  if (TMA_UPD) {  // the W tile the optimizer epilogue updates in place: [M rows x N cols] (no bias column)
+    wh = tmap2d(ep.out_hi, ep.N, ep.M, ep.ld_out, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    wl = tmap2d(ep.out_lo, ep.N, ep.M, ep.ld_out, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    wm = ep.mom ? tmap2d(ep.mom, ep.N, ep.M, ep.ld_out, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B) : wh;
   }
-  kern<<<grid, 256, smem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, ep, wh, wl, wm, ic);
+  const CUtensorMap ones = ep.ones_col_p1 > 0 ? ones_map() : ah;
+  kern<<<grid, 256, smem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, ep, wh, wl, wm, ic, ones);
   SPB_CUDA(cudaGetLastError());
 }
 
@@ -151,7 +173,8 @@ void launch_2sm_pn(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
   const int units = tiles * ((num_kb + kbs - 1) / kbs);
   const int pairs = num_sms() / 2;
   const int clusters = units < pairs ? units : pairs;
-  kern<<<2 * clusters, Cfg::kThreads, Cfg::kSmem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, ep);
+  const CUtensorMap ones = ep.ones_col_p1 > 0 ? ones_map() : ah;
+  kern<<<2 * clusters, Cfg::kThreads, Cfg::kSmem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, ep, ones);
   SPB_CUDA(cudaGetLastError());
 }
 
@@ -196,10 +219,11 @@ bool narrow_pair_ok(const Operand& A, const Operand& B, int epi) {
 // result is deterministic) and apply the real epilogue.
 template <int EPI>
 __global__ void splitk_fixup_kernel(const float* __restrict__ ws, int splits, long stride, long ldw, GemmEpilogue ep) {
-  const long n = static_cast<long>(ep.M) * ep.N;
+  const int cols = epi_cols(ep);  // including the fused bias column
+  const long n = static_cast<long>(ep.M) * cols;
   for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(i / ep.N), c = static_cast<int>(i % ep.N);
+    const int r = static_cast<int>(i / cols), c = static_cast<int>(i % cols);
     float v = 0.f;
     for (int sp = 0; sp < splits; ++sp) v += ws[sp * stride + r * ldw + c];
     epilogue_one<EPI>(ep, v, r, c);
@@ -224,6 +248,7 @@ void launch_splitk(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
   part.M = A.mn;
   part.N = B.mn;
   part.split_stride = stride;
+  part.ones_col_p1 = ep.ones_col_p1;  // the partials compute the bias column like any other
   // Splits actually populated: ceil(kb / ceil(kb / splits)) can be < splits.
   const int kb = (A.k + kBK - 1) / kBK, kbs = (kb + plan.splits - 1) / plan.splits;
   const int splits = (kb + kbs - 1) / kbs;
@@ -253,12 +278,14 @@ Plan g_last_plan{false, 1, 128};  // the plan of the last gemm_tf32x3 launch (te
 //    32-row boxes: pn 240 loads 256 when A is MN-major too);
 //  - split-K: + 3.0 us + (splits + 2) M N fp32 streamed at 3.17 TB/s (fixup;
 //    the constant is the old small-shape calibration, the slope the new fit).
+// no240: the bias-fused wgrads need 32-aligned B boxes (the ones box), which
+// the 120-row CTA halves of the 240-wide pair tile do not have.
 Plan plan_gemm(int M, int N, int K, long ws_floats, bool can_split, bool narrow_ok, bool allow_pair = true,
-               bool both_mn = false) {
+               bool both_mn = false, bool no240 = false) {
   const int sms = num_sms();
   const int kb = (K + kBK - 1) / kBK;
   const long t1 = static_cast<long>((M + 127) / 128) * ((N + 127) / 128);
-  if (allow_pair && g_force_plan.splits > 0) return g_force_plan;
+  if (allow_pair && g_force_plan.splits > 0 && !(no240 && g_force_plan.pn == 240)) return g_force_plan;
   if (g_force_variant >= 0) return {allow_pair && g_force_variant == 1, 1, 256};
   Plan best{false, 1, 256};
   double best_t = 1e30;
@@ -281,6 +308,7 @@ Plan plan_gemm(int M, int N, int K, long ws_floats, bool can_split, bool narrow_
   for (int pn : kPairNs) {
     if (!allow_pair) break;
     if (pn < 240 && !narrow_ok) continue;
+    if (pn == 240 && no240) continue;
     const int pe = both_mn ? 64 * ((pn + 63) / 64) : pn;
     for (int sp : {1, 2, 3, 4, 6, 8}) {
       if (!split_ok(sp)) break;
@@ -306,6 +334,20 @@ void dispatch_major(const Operand& A, const Operand& B, const GemmEpilogue& ep, 
 }  // namespace
 
 void gemm_force_variant(int v) { g_force_variant = v; }
+
+void gemm_prepare_device() {
+  int dev = 0;
+  SPB_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (g_ones[dev]) return;
+  float* p = nullptr;
+  SPB_CUDA(cudaMalloc(&p, 64 * 32 * sizeof(float)));
+  std::vector<float> h(64 * 32, 0.f);
+  std::fill(h.begin(), h.begin() + 32 * 32, 1.f);
+  SPB_CUDA(cudaMemcpy(p, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+  g_ones[dev] = p;
+}
 
 void gemm_force_plan(int two_sm, int pn, int splits) { g_force_plan = {two_sm != 0, splits, pn}; }
 
@@ -346,7 +388,11 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
   const ConvGeom& g = src.g;
   if (g.c_in % 32 || src.ld % 32) throw std::invalid_argument("gemm_conv_wgrad: c_in and ld must be multiples of 32");
   if (!A.mn_major) throw std::invalid_argument("gemm_conv_wgrad: A (Delta) must be MN-major");
-  const int N = 9 * g.c_in;
+  // N output columns: 9 c_in weights, plus the fused bias column (9 c_in is a
+  // multiple of 32 here) when ep.bias_col_p1 is set.
+  if (ep.bias_col_p1 > 0 && (ep.bias_col_p1 != 9 * g.c_in + 1 || ep.ones_col_p1 != ep.bias_col_p1))
+    throw std::invalid_argument("gemm_conv_wgrad: the bias column must follow the 9 c_in weights");
+  const int N = ep.bias_col_p1 > 0 ? 9 * g.c_in + 1 : 9 * g.c_in;
   CUtensorMap b[2] = {im2col_map(src.hi, src, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B),
                       im2col_map(src.lo, src, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)};
   const ConvTmaArgs ic{g.out_h * g.out_w, g.out_w, g.stride, g.c_in, pixel0, 0};
@@ -362,10 +408,12 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
     part.M = A.mn;
     part.N = N;
     part.split_stride = stride;
+    part.ones_col_p1 = ep.ones_col_p1;
     launch_inst<128, true, true, kEpiStoreScaled, false, 2>(A, B, part, s, plan.splits, nullptr, b, ic);
     const long n = static_cast<long>(A.mn) * N;
     const int grid = static_cast<int>(std::min<long>((n + 255) / 256, 148L * 16));
     const int kb = (A.k + kBK - 1) / kBK, kbs = (kb + plan.splits - 1) / plan.splits;
+    // (the fixup's epilogue `ep` routes column 9 c_in to the bias)
     splitk_fixup_kernel<kEpiStoreScaled><<<grid, 256, 0, s>>>(ep.splitk_ws, (kb + kbs - 1) / kbs, stride, ldw, ep);
     SPB_CUDA(cudaGetLastError());
     return 2;
@@ -395,8 +443,13 @@ int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue&
   static const bool no_split = std::getenv("SPB_NO_SPLITK") != nullptr;  // tuning experiments
   const bool can_split = ep.splitk_ws != nullptr && (epi == kEpiFwdTanh || epi == kEpiDgradTanh ||
                                                      epi == kEpiFwdLinear || epi == kEpiStoreScaled);
+  if (ep.ones_col_p1 > 0) {  // fused bias: a 32-aligned ones box at or beyond the real MN extent
+    const int oc = ep.ones_col_p1 - 1;
+    if (!B.mn_major || oc % 32 || oc < (B.mn_map > 0 ? B.mn_map : B.mn) || B.mn != oc + 1)
+      throw std::invalid_argument("gemm: bad fused-bias column");
+  }
   const Plan plan = plan_gemm(A.mn, B.mn, A.k, ep.splitk_ws && !no_split ? ep.splitk_ws_floats : 0, can_split,
-                              narrow_pair_ok(A, B, epi), true, A.mn_major && B.mn_major);
+                              narrow_pair_ok(A, B, epi), true, A.mn_major && B.mn_major, ep.ones_col_p1 > 0);
   g_last_plan = plan;
   if (plan.splits > 1) {
     switch (epi) {

@@ -41,14 +41,21 @@ struct Gemm2smCfg {
   static constexpr int kEpiCols = 64;  // accumulator columns per epilogue thread
 };
 
+// ones_col / t_ones / ones_row: the fused-bias ones box (load_operand in gemm_tf32x3.cuh).
 template <bool MN_MAJOR, int ROWS>
-__device__ __forceinline__ void load_operand_2sm(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, int mn0,
-                                                 int k0) {
+__device__ __forceinline__ void load_operand_2sm(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, int mn0, int k0,
+                                                 const CUtensorMap* t_ones = nullptr, int ones_col = -1,
+                                                 int ones_row = 0) {
   if constexpr (!MN_MAJOR) {
     tma_load_2d_2sm(dst, tm, bar, k0, mn0);
   } else {
 #pragma unroll
-    for (int c = 0; c < (ROWS + 31) / 32; ++c) tma_load_2d_2sm(dst + c * 4096, tm, bar, mn0 + c * 32, k0);
+    for (int c = 0; c < (ROWS + 31) / 32; ++c) {
+      if (mn0 + c * 32 == ones_col)
+        tma_load_2d_2sm(dst + c * 4096, t_ones, bar, 0, ones_row);
+      else
+        tma_load_2d_2sm(dst + c * 4096, tm, bar, mn0 + c * 32, k0);
+    }
   }
 }
 
@@ -57,7 +64,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
     gemm_tf32x3_2sm_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                            const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                            int num_kb, int num_m_pairs, int num_tiles, int kb_per_split, int num_units,
-                           const __grid_constant__ GemmEpilogue ep) {
+                           const __grid_constant__ GemmEpilogue ep, const __grid_constant__ CUtensorMap t_ones) {
   using Cfg = Gemm2smCfg<PN>;
   // TMA bytes one CTA brings per k-block (A hi/lo + B hi/lo).
   constexpr uint32_t kBLoaded = B_MN ? ((Cfg::kRowsB + 31) / 32) * 4096 : Cfg::kRowsB * 128;
@@ -118,6 +125,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
   if (warp < 4) {
     if (warp == 0) {
       if (elect_one()) {
+        const int ones_col = B_MN ? ep.ones_col_p1 - 1 : -1;
         int it = 0;
         for (int u = cluster_id; u < num_units; u += nclusters) {
           int t, kb0, kb1, split;
@@ -132,9 +140,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
             uint8_t* base = smem + s * Cfg::kStageBytes;
             load_operand_2sm<A_MN, Cfg::kRowsA>(base, &ta_hi, &full_bar[s], m0, kb * kBK);
             load_operand_2sm<A_MN, Cfg::kRowsA>(base + Cfg::kABytes, &ta_lo, &full_bar[s], m0, kb * kBK);
-            load_operand_2sm<B_MN, Cfg::kRowsB>(base + 2 * Cfg::kABytes, &tb_hi, &full_bar[s], n0, kb * kBK);
+            load_operand_2sm<B_MN, Cfg::kRowsB>(base + 2 * Cfg::kABytes, &tb_hi, &full_bar[s], n0, kb * kBK, &t_ones,
+                                                ones_col, 0);
             load_operand_2sm<B_MN, Cfg::kRowsB>(base + 2 * Cfg::kABytes + Cfg::kBBytes, &tb_lo, &full_bar[s], n0,
-                                                kb * kBK);
+                                                kb * kBK, &t_ones, ones_col, 32);
           }
         }
       }
@@ -191,6 +200,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       const int n_pair0 = (t / num_m_pairs) * Cfg::kPairN;
       const int n0 = n_pair0 + colbase;
       const int n_lim = min(ep.N, n_pair0 + PN);
+      const int bias_col = epi_bias_col(ep);
       float acc[Cfg::kEpiCols];
 #pragma unroll
       for (int j = 0; j < Cfg::kEpiCols; ++j) acc[j] = 0.f;
@@ -212,8 +222,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       }
       const int row = m0 + static_cast<int>(q * 32 + lane);
 #pragma unroll
-      for (int c0 = 0; c0 < Cfg::kEpiCols; c0 += 32)
-        if (n0 + c0 < n_lim) epilogue_chunk<EPI>(ep, acc + c0, row, n0 + c0, out_shift, n_lim);
+      for (int c0 = 0; c0 < Cfg::kEpiCols; c0 += 32) {
+        if (n0 + c0 == bias_col && c0 < width) bias_store<EPI>(ep, acc[c0], row);
+        else if (n0 + c0 < n_lim) epilogue_chunk<EPI>(ep, acc + c0, row, n0 + c0, out_shift, n_lim);
+      }
     }
   }
   tc_fence_before();

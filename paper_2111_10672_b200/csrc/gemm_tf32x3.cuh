@@ -63,7 +63,29 @@ struct GemmEpilogue {
   // staging slot in peer memory (NVLink stores), or this rank's own buffer.
   float* route[8];
   int route_rows;
+  // Fused bias gradient (wgrad GEMMs): the B operand carries a virtual column
+  // of ones at output column bias_col_p1 - 1 (a 32-aligned column >= N: the
+  // producer TMA-loads a constant ones box there, gemm.cu), so that column of
+  // the product is sum_k A[m, k] = the bias gradient of output row m
+  // (model.cpp:169, gb[o] += delta). The epilogue routes it to gb_hi[row]
+  // (kEpiStoreScaled, scaled by alpha) or applies the optimizer to the bias
+  // split pair gb_hi / gb_lo (+ gb_mom) in place (kEpiWgradUpdate). Columns
+  // in [N, bias col) are padding and never stored. bias_col_p1 = 0: no bias.
+  // ones_col_p1 (same encoding) is where the PRODUCER puts the ones box: equal
+  // to bias_col_p1, except in split-K partial GEMMs, which compute the column
+  // like any other into the workspace and leave the routing to the fixup.
+  int bias_col_p1;
+  int ones_col_p1;
+  float* gb_hi;
+  float* gb_lo;
+  float* gb_mom;
 };
+
+__host__ __device__ __forceinline__ int epi_bias_col(const GemmEpilogue& ep) { return ep.bias_col_p1 - 1; }
+// Output columns a GEMM with this epilogue computes (N, or up to the bias column).
+__host__ __device__ __forceinline__ int epi_cols(const GemmEpilogue& ep) {
+  return ep.bias_col_p1 > 0 ? ep.bias_col_p1 : ep.N;
+}
 
 // Address of output element (row, col) of a kEpiStoreScaled epilogue.
 __device__ __forceinline__ float* store_addr(const GemmEpilogue& ep, int row, int col, long out_shift) {
@@ -111,16 +133,25 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int chunk16) {
   return static_cast<uint32_t>(r * 128 + ((chunk16 ^ (r & 7)) << 4));
 }
 
-// TMA for one operand tile of ROWS (MN) x kBK (K) elements.
+// TMA for one operand tile of ROWS (MN) x kBK (K) elements. MN-major B
+// operands of bias-fused wgrads: the 32-column box starting at ones_col (the
+// virtual ones column, GemmEpilogue::bias_col_p1) comes from the constant map
+// t_ones instead: rows 0-31 of it are ones (the hi half), rows 32-63 zeros
+// (the lo half: ones are exact in tf32). ones_col < 0: none.
 template <bool MN_MAJOR, int ROWS>
-__device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, int mn0,
-                                             int k0) {
+__device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, int mn0, int k0,
+                                             const CUtensorMap* t_ones = nullptr, int ones_col = -1,
+                                             int ones_row = 0) {
   if constexpr (!MN_MAJOR) {
     tma_load_2d(dst, tm, bar, k0, mn0);  // box {32 (K), ROWS (MN)}
   } else {
 #pragma unroll
-    for (int c = 0; c < (ROWS + 31) / 32; ++c)  // boxes {32 (MN), 32 (K)}, 4 KB apart
-      tma_load_2d(dst + c * 4096, tm, bar, mn0 + c * 32, k0);
+    for (int c = 0; c < (ROWS + 31) / 32; ++c) {  // boxes {32 (MN), 32 (K)}, 4 KB apart
+      if (mn0 + c * 32 == ones_col)
+        tma_load_2d(dst + c * 4096, t_ones, bar, 0, ones_row);
+      else
+        tma_load_2d(dst + c * 4096, tm, bar, mn0 + c * 32, k0);
+    }
   }
 }
 
@@ -144,9 +175,28 @@ __device__ __forceinline__ void store_split4(float* hi, float* lo, float4 v) {
   *reinterpret_cast<float4*>(lo) = l;
 }
 
+// The bias column of a wgrad GEMM (GemmEpilogue::bias_col_p1): v = sum_k A[row, k].
+template <int EPI>
+__device__ __forceinline__ void bias_store(const GemmEpilogue& ep, float v, int row) {
+  if (row >= ep.M) return;
+  if constexpr (EPI == kEpiStoreScaled) {
+    ep.gb_hi[row] = ep.alpha * v;
+  } else if constexpr (EPI == kEpiWgradUpdate) {
+    const float b = sgd_apply(ep.gb_hi[row] + ep.gb_lo[row], ep.alpha * v, ep.gb_mom ? ep.gb_mom + row : nullptr, ep.lr,
+                              ep.mu, ep.wd);
+    const float bh = tf32_rna(b);
+    ep.gb_hi[row] = bh;
+    ep.gb_lo[row] = b - bh;
+  }
+}
+
 // The epilogue of one output element (split-K fixup path).
 template <int EPI>
 __device__ __forceinline__ void epilogue_one(const GemmEpilogue& ep, float v, int row, int col) {
+  if (col >= ep.N) {  // the fused bias column, or padding before it
+    if (col == epi_bias_col(ep)) bias_store<EPI>(ep, v, row);
+    return;
+  }
   const long at = row * ep.ld_out + col;
   if constexpr (EPI == kEpiStoreScaled) {
     *store_addr(ep, row, col, 0) = ep.alpha * v;
@@ -304,7 +354,10 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
 // buffer; the epilogue warps drain each chunk into fp32 registers
 // (round-to-nearest adds) while the MMA warp fills the other buffer. The error
 // is then bounded independently of K.
-constexpr int kChunkKb = 4;  // 128 of K per TMEM chunk
+#ifndef SPB_CHUNK_KB
+#define SPB_CHUNK_KB 4
+#endif
+constexpr int kChunkKb = SPB_CHUNK_KB;  // 32 * kChunkKb of K per TMEM chunk
 
 // Implicit-GEMM convolution operands (3x3, padding 1, NHWC, c_in % 32 == 0):
 // the tensor maps are TMA im2col maps of the activation tensor and the tile
@@ -336,7 +389,7 @@ __global__ void __launch_bounds__(256, 1)
                        int num_kb, int num_m_tiles, int num_tiles, int kb_per_split, int num_units,
                        const __grid_constant__ GemmEpilogue ep, const __grid_constant__ CUtensorMap tw_hi,
                        const __grid_constant__ CUtensorMap tw_lo, const __grid_constant__ CUtensorMap tw_mom,
-                       const ConvTmaArgs ic) {
+                       const ConvTmaArgs ic, const __grid_constant__ CUtensorMap t_ones) {
   using Cfg = GemmCfg<BN, TMA_UPD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -386,6 +439,7 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0) {
     if (elect_one()) {
+      const int ones_col = B_MN ? ep.ones_col_p1 - 1 : -1;
       int it = 0;
       for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
         int m0, n0, kb0, kb1, split;
@@ -413,14 +467,20 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
             for (int cc = 0; cc < BN / 32; ++cc) {
               const int col = n0 + cc * 32, tap = col / ic.c_in, c = col - tap * ic.c_in;
+              uint8_t* dh = base + 2 * Cfg::kABytes + cc * 4096;
+              if (col == ones_col) {  // the fused bias column: constant ones / zeros boxes
+                tma_load_2d(dh, &t_ones, &full_bar[s], 0, 0);
+                tma_load_2d(dh + Cfg::kBBytes, &t_ones, &full_bar[s], 0, 32);
+                continue;
+              }
               const uint16_t ox = static_cast<uint16_t>(tap % 3), oy = static_cast<uint16_t>(tap / 3);
-              tma_load_im2col_4d(base + 2 * Cfg::kABytes + cc * 4096, &tb_hi, &full_bar[s], c, w, h, n, ox, oy);
-              tma_load_im2col_4d(base + 2 * Cfg::kABytes + Cfg::kBBytes + cc * 4096, &tb_lo, &full_bar[s], c, w, h, n,
-                                 ox, oy);
+              tma_load_im2col_4d(dh, &tb_hi, &full_bar[s], c, w, h, n, ox, oy);
+              tma_load_im2col_4d(dh + Cfg::kBBytes, &tb_lo, &full_bar[s], c, w, h, n, ox, oy);
             }
           } else {
-            load_operand<B_MN, BN>(base + 2 * Cfg::kABytes, &tb_hi, &full_bar[s], n0, kb * kBK);
-            load_operand<B_MN, BN>(base + 2 * Cfg::kABytes + Cfg::kBBytes, &tb_lo, &full_bar[s], n0, kb * kBK);
+            load_operand<B_MN, BN>(base + 2 * Cfg::kABytes, &tb_hi, &full_bar[s], n0, kb * kBK, &t_ones, ones_col, 0);
+            load_operand<B_MN, BN>(base + 2 * Cfg::kABytes + Cfg::kBBytes, &tb_lo, &full_bar[s], n0, kb * kBK, &t_ones,
+                                   ones_col, 32);
           }
         }
       }
@@ -552,6 +612,8 @@ __global__ void __launch_bounds__(256, 1)
           }
           __syncwarp();
         }
+        const int bc = epi_bias_col(ep) - n0;  // the fused bias column in this tile (its W box was out of bounds)
+        if (bc >= 0 && bc < BN) bias_store<EPI>(ep, acc[bc], row);
       } else if (EPI == kEpiStoreScaled && ep.route_rows > 0) {
         // Rows routed to peer memory (multi-GPU push exchange): stage each
         // 32 x 32 block in shared memory so that one warp store writes four
@@ -562,7 +624,9 @@ __global__ void __launch_bounds__(256, 1)
         const int cc = 4 * static_cast<int>(lane & 7);
 #pragma unroll
         for (int c0 = 0; c0 < BN; c0 += 32) {
-          if (n0 + c0 < ep.N) {
+          if (n0 + c0 == epi_bias_col(ep)) {
+            bias_store<EPI>(ep, acc[c0], row);  // the bias row stays local (it travels with the push signal)
+          } else if (n0 + c0 < ep.N) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = ep.alpha * acc[c0 + j];
             __syncwarp();
@@ -586,8 +650,10 @@ __global__ void __launch_bounds__(256, 1)
         }
       } else {
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 32)
-          if (n0 + c0 < ep.N) epilogue_chunk<EPI>(ep, acc + c0, row, n0 + c0, out_shift);
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          if (n0 + c0 == epi_bias_col(ep)) bias_store<EPI>(ep, acc[c0], row);
+          else if (n0 + c0 < ep.N) epilogue_chunk<EPI>(ep, acc + c0, row, n0 + c0, out_shift);
+        }
       }
     }
     if constexpr (TMA_UPD) {

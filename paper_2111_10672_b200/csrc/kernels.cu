@@ -83,9 +83,9 @@ constexpr int kMaxOut = 16;
 __global__ void head_kernel(const float* __restrict__ h_hi, const float* __restrict__ h_lo, long ldh, int rows,
                             int n_in, int n_out, const float* __restrict__ w_hi, const float* __restrict__ w_lo,
                             long ldw, const float* __restrict__ b_hi, const float* __restrict__ b_lo,
-                            const float* __restrict__ y, float* __restrict__ delta, float* __restrict__ row_loss,
-                            float* __restrict__ dn_hi, float* __restrict__ dn_lo, long ldd, int cont_row0,
-                            int tanh_out, int dn_act) {
+                            const float* __restrict__ y, float* __restrict__ delta, float* __restrict__ delta_lo,
+                            long ldq, float* __restrict__ row_loss, float* __restrict__ dn_hi,
+                            float* __restrict__ dn_lo, long ldd, int cont_row0, int tanh_out, int dn_act) {
   const int warps = blockDim.x / 32;
   const int r = blockIdx.x * warps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
@@ -123,8 +123,12 @@ __global__ void head_kernel(const float* __restrict__ h_hi, const float* __restr
       loss += 0.5f * d[o] * d[o];
     }
   }
-  if (lane == 0) {
-    for (int o = 0; o < n_out; ++o) delta[r * n_out + o] = d[o];
+  if (lane == 0) {  // delta_L as a split pair (the head wgrad GEMM's A operand), row stride ldq
+    for (int o = 0; o < n_out; ++o) {
+      const float dh = tf32_rna(d[o]);
+      delta[r * ldq + o] = dh;
+      delta_lo[r * ldq + o] = d[o] - dh;
+    }
     row_loss[r] = loss;
   }
   if (dn_hi && r >= cont_row0) {
@@ -338,13 +342,14 @@ void launch_split_rows(const float* x, long ldx_in, int rows, int cols, float* h
 
 void launch_head(const float* h_hi, const float* h_lo, long ldh, int rows, int n_in, int n_out, const float* w_hi,
                  const float* w_lo, long ldw, const float* b_hi, const float* b_lo, const float* y, float* delta,
-                 float* row_loss, float* dn_hi, float* dn_lo, long ldd, int cont_row0, bool tanh_out,
-                 cudaStream_t s, bool dn_act) {
+                 float* delta_lo, long ldq, float* row_loss, float* dn_hi, float* dn_lo, long ldd, int cont_row0,
+                 bool tanh_out, cudaStream_t s, bool dn_act) {
   if (rows <= 0) return;
   if (n_out > kMaxOut) throw std::invalid_argument("head: n_out > 16");
   const int warps = 8;
   head_kernel<<<(rows + warps - 1) / warps, warps * 32, 0, s>>>(h_hi, h_lo, ldh, rows, n_in, n_out, w_hi, w_lo, ldw,
-                                                                b_hi, b_lo, y, delta, row_loss, dn_hi, dn_lo, ldd,
+                                                                b_hi, b_lo, y, delta, delta_lo, ldq, row_loss, dn_hi,
+                                                                dn_lo, ldd,
                                                                 cont_row0, tanh_out ? 1 : 0, dn_act ? 1 : 0);
   SPB_CUDA(cudaGetLastError());
 }

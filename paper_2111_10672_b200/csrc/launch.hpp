@@ -32,6 +32,7 @@ struct Operand {
   int mn;   // extent along the GEMM M (for A) / N (for B) dimension
   int k;    // extent along K
   bool mn_major;
+  int mn_map = 0;  // > 0: the stored MN extent when mn runs past it (TMA zero-fills beyond)
 };
 
 struct GemmEpilogue;  // gemm_tf32x3.cuh
@@ -59,6 +60,9 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
 // (kEpiDgradTanh), Wf = the spatially flipped, channel-transposed kernel
 // [c_below x 9 c_out] (launch_conv_flip). src.g describes Delta as input.
 int gemm_conv_dgrad(const ConvSrc& src, long pixel0, int rows, const Operand& B, const GemmEpilogue& ep, cudaStream_t s);
+// Per-device constants of the GEMMs (the fused-bias ones boxes); call once
+// per device before capturing any GEMM with a fused bias column.
+void gemm_prepare_device();
 // Test hook: -1 automatic choice, 0 force 1-CTA, 1 force CTA pair.
 void gemm_force_variant(int v);
 // Tuning aid: force every GEMM onto one plan (two_sm: CTA-pair kernel of
@@ -91,10 +95,11 @@ void launch_split_rows(const float* x, long ldx_in, int rows, int cols, float* h
 // Head layer L (n_out <= 16): out = H W^T + b, delta = out - y, row_loss,
 // and for rows >= cont_row0: dnext = (delta W) * (1 - H^2) as a split pair
 // (dn_act = false: dnext = delta W, for the pooled conv features).
+// delta_L is written as a split pair (delta, delta_lo) with row stride ldq.
 void launch_head(const float* h_hi, const float* h_lo, long ldh, int rows, int n_in, int n_out, const float* w_hi,
                  const float* w_lo, long ldw, const float* b_hi, const float* b_lo, const float* y,
-                 float* delta, float* row_loss, float* dn_hi, float* dn_lo, long ldd, int cont_row0,
-                 bool tanh_out, cudaStream_t s, bool dn_act = true);
+                 float* delta, float* delta_lo, long ldq, float* row_loss, float* dn_hi, float* dn_lo, long ldd,
+                 int cont_row0, bool tanh_out, cudaStream_t s, bool dn_act = true);
 // out[o * ld_out + c] = alpha * sum_{r in [r0,r1)} vec(r,o) * (hi + lo)[r, c]
 // (vec = 1 when rowvec == nullptr, nvec = 1), deterministic two-pass column
 // reduction. scratch must hold colreduce_scratch(...) floats.

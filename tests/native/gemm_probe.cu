@@ -132,6 +132,7 @@ static int report(const char* name, int M, int N, int K, double rel, double tol)
 static int run_shapes() {
   const int n = 4096;
   int bad = 0;
+  gemm_prepare_device();  // the fused-bias ones boxes
   std::mt19937_64 rng(77);
   float *ws;
   const long ws_floats = 16L << 20;
@@ -198,16 +199,66 @@ static int run_shapes() {
     std::vector<double> Ra(R.size());
     for (size_t i = 0; i < R.size(); ++i) Ra[i] = R[i] * alpha;
     bad += report("wgrad (alpha epilogue)", n, n, K, rel_err(got, Ra), 2e-6);
+    {  // bias fused as the virtual ones column 4096 of B: [dW | db] in one GEMM, on the
+       // automatic plan and forced 1-CTA split-K / pair plans (split-K routes the bias in the fixup)
+      std::vector<double> Rb(n, 0.0);
+      for (int q = 0; q < K; ++q)
+        for (int i = 0; i < n; ++i) Rb[i] += D[static_cast<long>(q) * n + i];
+      for (double& v : Rb) v *= alpha;
+      float* gb;
+      cudaMalloc(&gb, n * 4);
+      const struct { int two, pn, sp; } fp[] = {{-1, 0, 0}, {0, 128, 3}, {1, 192, 2}, {1, 256, 1}};
+      for (const auto& f : fp) {
+        if (f.two >= 0 && K != 1024) continue;
+        if (f.two >= 0) gemm_force_plan(f.two, f.pn, f.sp);
+        cudaMemset(G, 0, static_cast<long>(n) * n * 4);
+        cudaMemset(gb, 0, n * 4);
+        GemmEpilogue eb{};
+        eb.out_hi = G, eb.ld_out = n, eb.alpha = alpha, eb.M = n, eb.N = n, eb.gb_hi = gb;
+        eb.bias_col_p1 = eb.ones_col_p1 = n + 1;
+        eb.splitk_ws = ws, eb.splitk_ws_floats = ws_floats;
+        Operand OB{Hh, Hl, n, n + 1, K, true, n};
+        gemm_tf32x3(Operand{Dh, Dl, n, n, K, true}, OB, kEpiStoreScaled, eb, 0);
+        cudaDeviceSynchronize();
+        gemm_force_plan(0, 0, 0);
+        std::vector<float> gw(static_cast<long>(n) * n), gbh(n);
+        cudaMemcpy(gw.data(), G, gw.size() * 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(gbh.data(), gb, n * 4, cudaMemcpyDeviceToHost);
+        const double e = std::max(rel_err(gw, Ra), rel_err(gbh, Rb));
+        bad += report(f.two < 0 ? "wgrad + fused bias" : "wgrad + fused bias (forced)", n, n + 1, K, e, 2e-6);
+      }
+      cudaFree(gb);
+    }
     if (K <= 512) {  // the fused optimizer epilogue of the <= 512-row layers: W -= lr (mu buf + g + wd W)
       std::vector<float> M0 = rand_vec(static_cast<long>(n) * n, rng, 1e-4f);
       float *Uh, *Ul, *Mom;
       upload_exact(W, n, n, &Uh, &Ul);
       cudaMalloc(&Mom, M0.size() * 4);
       cudaMemcpy(Mom, M0.data(), M0.size() * 4, cudaMemcpyHostToDevice);
+      // with the bias fused (ones column): b -= lr (mu mb + g_b + wd b) on its split pair
+      std::vector<float> b0 = rand_vec(n, rng, 1.f / 64), mb0 = rand_vec(n, rng, 1e-4f);
+      float *Bh, *Bl, *Mb;
+      upload_exact(b0, 1, n, &Bh, &Bl);
+      cudaMalloc(&Mb, n * 4);
+      cudaMemcpy(Mb, mb0.data(), n * 4, cudaMemcpyHostToDevice);
       GemmEpilogue eu{};
       eu.out_hi = Uh, eu.out_lo = Ul, eu.ld_out = n, eu.alpha = alpha, eu.M = n, eu.N = n, eu.mom = Mom;
       eu.lr = 1.0f, eu.mu = 0.9f, eu.wd = 1e-2f;
-      gemm_tf32x3(Operand{Dh, Dl, n, n, K, true}, Operand{Hh, Hl, n, n, K, true}, kEpiWgradUpdate, eu, 0);
+      eu.bias_col_p1 = eu.ones_col_p1 = n + 1, eu.gb_hi = Bh, eu.gb_lo = Bl, eu.gb_mom = Mb;
+      gemm_tf32x3(Operand{Dh, Dl, n, n, K, true}, Operand{Hh, Hl, n, n + 1, K, true, n}, kEpiWgradUpdate, eu, 0);
+      {
+        std::vector<double> db(n), gsum(n, 0.0);
+        for (int q = 0; q < K; ++q)
+          for (int i = 0; i < n; ++i) gsum[i] += D[static_cast<long>(q) * n + i];
+        std::vector<float> bn = fetch_pair(Bh, Bl, n), d(n);
+        for (int i = 0; i < n; ++i) {
+          const double g = gsum[i] * alpha + 1e-2 * b0[i], buf = 0.9 * mb0[i] + g;
+          db[i] = -buf;
+          d[i] = static_cast<float>(static_cast<double>(bn[i]) - b0[i]);
+        }
+        bad += report("wgrad fused update (db)", n, n + 1, K, rel_err(d, db), 1e-5);
+      }
+      cudaFree(Bh), cudaFree(Bl), cudaFree(Mb);
       std::vector<double> Wn(R.size()), dW(R.size());
       for (size_t i = 0; i < R.size(); ++i) {
         const double g = Ra[i] + 1e-2 * W[i], buf = 0.9 * M0[i] + g;

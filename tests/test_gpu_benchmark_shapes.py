@@ -18,8 +18,10 @@ here against CPU checkers on the same inputs:
 * cfg4's ConvNet widths at 32 x 32 against oracle/conv_oracle.py.
 
 Tolerances as everywhere (north_star): aggregated per-layer gradients 1e-5
-relative, weights after N steps 1e-4 relative (norm-wise per layer); we also
-check the weight CHANGE W_N - W_0 at 1e-4, which is the stricter test.
+relative, weights after N steps 1e-4 relative (norm-wise per layer). The
+weight CHANGE W_N - W_0 is checked too, at 1e-4 of its norm plus the fp32
+storage rounding of the weights (4 roundings of 2^-24 |w|): the updates of
+the first layers are ~1e-4 of the weights, below fp32 resolution otherwise.
 """
 import os
 
@@ -34,6 +36,13 @@ pytestmark = pytest.mark.gpu
 
 GRAD_TOL = 1e-5
 WEIGHT_TOL = 1e-4
+
+
+def delta_ok(got, w0, want) -> bool:
+    """||(got - w0) - (want - w0)|| within 1e-4 of ||want - w0|| plus fp32 storage rounding."""
+    d = np.asarray(got, np.float64) - w0
+    dw = want - w0
+    return np.linalg.norm(d - dw) <= 1e-4 * np.linalg.norm(dw) + 4 * 2.0**-24 * np.linalg.norm(want)
 
 
 def _rows(orc, seed, s, k, bw, N):
@@ -73,7 +82,7 @@ def test_cfg3_width_step_matches_reference(orc, ref):
     for l, (a, b, w0) in enumerate(zip(after, g_ref, W64)):
         want = w0 - 0.01 * b  # x -= lr g (spb.cpp:196)
         assert rel_err(a, want) <= WEIGHT_TOL
-        assert rel_err(a.astype(np.float64) - w0, want - w0) <= WEIGHT_TOL, l
+        assert delta_ok(a, w0, want), l
 
 
 @pytest.mark.parametrize("full", [False, True])
@@ -113,7 +122,7 @@ def test_cfg3_full_depth_matches_batched_oracle(orc, full):
         batched.sgd_update(P, g, lr, mu, wd, bufs)
     for l, (a, b, w0) in enumerate(zip(after, P, W0)):
         assert rel_err(a, b) <= WEIGHT_TOL
-        assert rel_err(a.astype(np.float64) - w0, b - w0) <= WEIGHT_TOL, (l, rel_err(a.astype(np.float64) - w0, b - w0))
+        assert delta_ok(a, w0, b), (l, rel_err(a.astype(np.float64) - w0, b - w0))
 
 
 def test_cfg4_resnet18_widths_match_conv_oracle(orc):
@@ -151,4 +160,4 @@ def test_cfg4_resnet18_widths_match_conv_oracle(orc):
         o.spb_step(B, X64, Y64, k, bw, lr, seed, s, orc)
     for l in range(o.L):
         assert rel_err(after[l], B[l]) <= WEIGHT_TOL
-        assert rel_err(after[l].astype(np.float64) - W0[l], B[l] - W0[l]) <= WEIGHT_TOL, l
+        assert delta_ok(after[l], W0[l], B[l]), l
