@@ -83,7 +83,8 @@ SPB_API spb_status spb_make_random_chain_mlp(const int* widths, int n_widths, in
 /* ---- Context: the ChainMlp "layer" (model.hpp:95-111) on one B200 ---------
  * widths[0..n_widths): [n_0, ..., n_L]; n_L <= 16 (the reference requires
  * n_L == 1, model.cpp:93; wider heads are the 0.5*||out-y||^2 throughput
- * variant). k workers of per_worker_batch samples each may run per step. */
+ * variant). k workers of per_worker_batch samples each may run per step.
+ * device < 0: the calling thread's current CUDA device. */
 SPB_API spb_status spb_create(const int* widths, int n_widths, int k, int per_worker_batch, int device,
                       spb_ctx** out);
 /* ConvNet (BASELINE configs[3]: CIFAR10-shaped, ResNet18
@@ -154,6 +155,13 @@ SPB_API spb_status spb_partial_backprop(spb_ctx* ctx, const int* batch, int len,
  * each layer over its contributors on the GPU. out[l] receives layer l+1. */
 SPB_API spb_status spb_aggregate(spb_ctx* ctx, int k, int L, const float* const* blocks, const int* dims,
                          const int* covered_from, float* const* out);
+/* The same in fp64 (the reference's Params precision), context-free, on
+ * `device` (< 0: the calling thread's current CUDA device): per element the
+ * contributors are summed in ascending worker order and the sum multiplied by
+ * 1.0 / m, exactly the reference's operations (spb.cpp:97-103) with
+ * round-to-nearest and no contraction -- bit-identical to the CPU code. */
+SPB_API spb_status spb_aggregate64(int device, int k, int L, const double* const* blocks, const int* dims,
+                                   const int* covered_from, double* const* out);
 
 /* ---- Training step: one SPB-SGD iteration (spb.cpp:187-196) -------------------
  * Every worker j hosted by this context draws per_worker_batch samples from
@@ -189,6 +197,13 @@ SPB_API spb_status spb_step_host_async(spb_ctx* ctx, const float* X_rows, const 
 SPB_API spb_status spb_get_grads(spb_ctx* ctx, float* const* blocks);
 /* ChainMlp::loss (model.cpp:139-143) over the whole uploaded dataset. */
 SPB_API spb_status spb_loss(spb_ctx* ctx, double* out);
+/* ChainMlp::sample_loss / loss (model.cpp:130-143) in fp64 on the GPU, at the
+ * fp64 parameters `blocks` (reference Params layout, L blocks): *out = the sum
+ * over samples[0..count) (samples == NULL: the whole dataset) of
+ * 0.5 * ||out - y||^2. The reference's precision, for callers that difference
+ * losses (the verify suite's finite-difference check, verify.cpp:217-248);
+ * the training step itself stays fp32. ChainMlp contexts only. */
+SPB_API spb_status spb_loss64(spb_ctx* ctx, const double* const* blocks, const int* samples, int count, double* out);
 /* Waits for all work queued on the context's stream. */
 SPB_API spb_status spb_synchronize(spb_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t), for event timing by callers. */

@@ -18,12 +18,14 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "build")
-LIB = os.path.join(PKG, "libspb_b200.so")
+# Tuning experiments may build variants elsewhere: SPB_BUILD_DIR / SPB_LIB_OUT,
+# with extra nvcc flags in SPB_NVCC_EXTRA (e.g. -DSPB_CHUNK_KB_DGRAD=2).
+BUILD = os.environ.get("SPB_BUILD_DIR", os.path.join(PKG, "build"))
+LIB = os.environ.get("SPB_LIB_OUT", os.path.join(PKG, "libspb_b200.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",
-          "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-DSPB_BUILD_LIB"]
+          "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-DSPB_BUILD_LIB"] + os.environ.get("SPB_NVCC_EXTRA", "").split()
 
 
 def _sources():

@@ -145,6 +145,9 @@ struct Engine {
   // dataset
   float *X = nullptr, *Y = nullptr;
   int N = 0;
+  // spb_loss64: the fp64 parameters last evaluated (host copy + device copy).
+  std::vector<double> p64_host;
+  double* p64 = nullptr;
   // row workspace
   int cap_rows = 0;
   std::vector<float*> Hh, Hl;
@@ -388,6 +391,7 @@ struct Engine {
     };
     f(splitk_ws);
     f(splitk_ws2);
+    f(p64);
     f(p_hi), f(p_lo), f(grad), f(mom), f(X), f(Y), f(delta), f(delta_lo), f(row_loss), f(ybatch), f(xin), f(idx),
         f(idx_in), f(loss_dev), f(tmp), f(ctl), f(workers_dev), f(epoch_dev), f(bar_dev), f(w32), f(flags),
         f(stage), f(pstage), f(trace_dev);
@@ -429,6 +433,7 @@ struct Engine {
     nout = w[L];
     k = k_;
     bw = bw_;
+    if (device < 0) SPB_CUDA(cudaGetDevice(&device));  // -1: the calling thread's current device
     dev = device;
     SPB_CUDA(cudaSetDevice(dev));
     gemm_prepare_device();
@@ -459,6 +464,7 @@ struct Engine {
     nout = nout_;
     k = k_;
     bw = bw_;
+    if (device < 0) SPB_CUDA(cudaGetDevice(&device));  // -1: the calling thread's current device
     dev = device;
     SPB_CUDA(cudaSetDevice(dev));
     gemm_prepare_device();
@@ -1882,6 +1888,108 @@ spb_status guard(spb_ctx* ctx, F&& f) {
 
 }  // namespace
 
+namespace spb {
+namespace {
+// aggregate (spb.cpp:70-106): the reference's protocol checks (spb.cpp:74-87,
+// 91-99), before any device work. Returns the layer -> contributor counts.
+template <class T>
+std::vector<int> aggregate_validate(int k, int L, const T* const* blocks, const int* dims, const int* covered_from) {
+  if (k < 1) throw ArgumentError("aggregate: need exactly k gradients");
+  if (L < 1) throw ProtocolError("aggregate: gradient layer counts differ");
+  for (int j = 1; j <= k; ++j) {
+    const int expect_from = L - suffix_layers(j, k, L) + 1;
+    if (covered_from[j - 1] != expect_from)
+      throw ProtocolError("aggregate: worker " + std::to_string(j) + " coverage does not match the suffix rule");
+    for (int l = 1; l <= L; ++l) {
+      const bool present = blocks[(j - 1) * L + l - 1] != nullptr && dims[(j - 1) * L + l - 1] > 0;
+      if (present != (l >= covered_from[j - 1]))
+        throw ProtocolError("aggregate: block presence inconsistent with covered_from");
+    }
+  }
+  auto chunk_of = layer_chunks(k, L);
+  for (int l = 1; l <= L; ++l) {
+    const int m = chunk_of[l - 1];
+    const long dim = dims[(k - m) * L + l - 1];
+    for (int wkr = k - m + 1; wkr <= k; ++wkr)
+      if (dims[(wkr - 1) * L + l - 1] != dim) throw ProtocolError("aggregate: block dimension mismatch");
+  }
+  return chunk_of;
+}
+
+// Per-thread, per-device staging for the aggregator entry points: grown on
+// demand and reused across calls (the reference's callers aggregate once per
+// SGD iteration -- thousands of times in its verify suite).
+struct AggWorkspace {
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  void* ptrs = nullptr;
+  size_t ptr_bytes = 0;
+  cudaStream_t st = nullptr;
+  ~AggWorkspace() {
+    if (stage) cudaFree(stage);
+    if (ptrs) cudaFree(ptrs);
+    if (st) cudaStreamDestroy(st);
+  }
+  static AggWorkspace& get(int dev) {
+    thread_local std::map<int, AggWorkspace> per_device;
+    return per_device[dev];
+  }
+  void reserve(size_t sb, size_t pb) {
+    if (sb > stage_bytes) {
+      if (stage) cudaFree(stage), stage = nullptr, stage_bytes = 0;
+      SPB_CUDA(cudaMalloc(&stage, sb));
+      stage_bytes = sb;
+    }
+    if (pb > ptr_bytes) {
+      if (ptrs) cudaFree(ptrs), ptrs = nullptr, ptr_bytes = 0;
+      SPB_CUDA(cudaMalloc(&ptrs, pb));
+      ptr_bytes = pb;
+    }
+    if (!st) SPB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  }
+};
+
+// The per-layer contributor means of validated host blocks, on the GPU.
+template <class T>
+void aggregate_run(int k, int L, const std::vector<int>& chunk_of, const T* const* blocks, const int* dims,
+                   T* const* out, int dev) {
+  std::vector<long> base(L + 1, 0), pbase(L + 1, 0);
+  for (int l = 1; l <= L; ++l) {
+    const int m = chunk_of[l - 1];
+    const long dim = dims[(k - m) * L + l - 1];
+    base[l] = base[l - 1] + round_up(dim * (m + 1), 32);
+    pbase[l] = pbase[l - 1] + m;
+  }
+  AggWorkspace& ws = AggWorkspace::get(dev);
+  ws.reserve(std::max(1L, base[L]) * sizeof(T), std::max(1L, pbase[L]) * sizeof(T*));
+  cudaStream_t st = ws.st;
+  T* stage = static_cast<T*>(ws.stage);
+  const T** ptrs = static_cast<const T**>(ws.ptrs);
+  std::vector<const T*> hp(pbase[L]);
+  for (int l = 1; l <= L; ++l) {
+    const int m = chunk_of[l - 1];
+    const long dim = dims[(k - m) * L + l - 1];
+    for (int i = 0; i < m; ++i) hp[pbase[l - 1] + i] = stage + base[l - 1] + i * dim;
+  }
+  SPB_CUDA(cudaMemcpyAsync(ptrs, hp.data(), hp.size() * sizeof(T*), cudaMemcpyHostToDevice, st));
+  for (int l = 1; l <= L; ++l) {
+    const int m = chunk_of[l - 1];
+    const long dim = dims[(k - m) * L + l - 1];
+    T* sl = stage + base[l - 1];
+    for (int i = 0; i < m; ++i)
+      SPB_CUDA(cudaMemcpyAsync(sl + i * dim, blocks[(k - m + i) * L + l - 1], dim * sizeof(T), cudaMemcpyHostToDevice,
+                               st));
+    if constexpr (sizeof(T) == 8)
+      launch_aggregate64(ptrs + pbase[l - 1], m, dim, sl + m * dim, st);
+    else
+      launch_aggregate(ptrs + pbase[l - 1], m, dim, sl + m * dim, st);
+    SPB_CUDA(cudaMemcpyAsync(out[l - 1], sl + m * dim, dim * sizeof(T), cudaMemcpyDeviceToHost, st));
+  }
+  SPB_CUDA(cudaStreamSynchronize(st));  // the staging is reused by the next call
+}
+}  // namespace
+}  // namespace spb
+
 extern "C" {
 
 const char* spb_last_error(const spb_ctx* ctx) { return ctx ? ctx->e.err.c_str() : spb::g_err.c_str(); }
@@ -2087,62 +2195,19 @@ spb_status spb_partial_backprop(spb_ctx* ctx, const int* batch, int len, int suf
 spb_status spb_aggregate(spb_ctx* ctx, int k, int L, const float* const* blocks, const int* dims,
                          const int* covered_from, float* const* out) {
   return guard(ctx, [&] {
-    auto& e = ctx->e;
-    if (k < 1) throw spb::ArgumentError("aggregate: need exactly k gradients");
-    // Protocol checks, spb.cpp:74-87.
-    for (int j = 1; j <= k; ++j) {
-      const int expect_from = L - spb::suffix_layers(j, k, L) + 1;
-      if (covered_from[j - 1] != expect_from)
-        throw spb::ProtocolError("aggregate: worker " + std::to_string(j) + " coverage does not match the suffix rule");
-      for (int l = 1; l <= L; ++l) {
-        const bool present = blocks[(j - 1) * L + l - 1] != nullptr && dims[(j - 1) * L + l - 1] > 0;
-        if (present != (l >= covered_from[j - 1]))
-          throw spb::ProtocolError("aggregate: block presence inconsistent with covered_from");
-      }
-    }
-    auto chunk_of = spb::layer_chunks(k, L);
-    for (int l = 1; l <= L; ++l) {  // spb.cpp:91-104
-      const int m = chunk_of[l - 1];
-      const long dim = dims[(k - m) * L + l - 1];
-      for (int wkr = k - m + 1; wkr <= k; ++wkr)
-        if (dims[(wkr - 1) * L + l - 1] != dim) throw spb::ProtocolError("aggregate: block dimension mismatch");
-    }
-    // One staging allocation for every layer (RAII: freed on any throw), the
-    // copies and per-layer reductions queued on the context stream, one sync.
-    std::vector<long> base(L + 1, 0), pbase(L + 1, 0);
-    for (int l = 1; l <= L; ++l) {
-      const int m = chunk_of[l - 1];
-      const long dim = dims[(k - m) * L + l - 1];
-      base[l] = base[l - 1] + spb::round_up(dim * (m + 1), 32);
-      pbase[l] = pbase[l - 1] + m;
-    }
-    struct DevBuf {
-      void* p = nullptr;
-      ~DevBuf() {
-        if (p) cudaFree(p);
-      }
-    } stage_buf, ptr_buf;
-    SPB_CUDA(cudaMalloc(&stage_buf.p, std::max(1L, base[L]) * sizeof(float)));
-    SPB_CUDA(cudaMalloc(&ptr_buf.p, std::max(1L, pbase[L]) * sizeof(float*)));
-    float* stage = static_cast<float*>(stage_buf.p);
-    const float** ptrs = static_cast<const float**>(ptr_buf.p);
-    std::vector<const float*> hp(pbase[L]);
-    for (int l = 1; l <= L; ++l) {
-      const int m = chunk_of[l - 1];
-      const long dim = dims[(k - m) * L + l - 1];
-      for (int i = 0; i < m; ++i) hp[pbase[l - 1] + i] = stage + base[l - 1] + i * dim;
-    }
-    SPB_CUDA(cudaMemcpyAsync(ptrs, hp.data(), hp.size() * sizeof(float*), cudaMemcpyHostToDevice, e.st));
-    for (int l = 1; l <= L; ++l) {
-      const int m = chunk_of[l - 1];
-      const long dim = dims[(k - m) * L + l - 1];
-      float* st = stage + base[l - 1];
-      for (int i = 0; i < m; ++i)
-        SPB_CUDA(cudaMemcpyAsync(st + i * dim, blocks[(k - m + i) * L + l - 1], dim * 4, cudaMemcpyHostToDevice, e.st));
-      spb::launch_aggregate(ptrs + pbase[l - 1], m, dim, st + m * dim, e.st);
-      SPB_CUDA(cudaMemcpyAsync(out[l - 1], st + m * dim, dim * 4, cudaMemcpyDeviceToHost, e.st));
-    }
-    SPB_CUDA(cudaStreamSynchronize(e.st));  // also orders the frees after the copies
+    auto chunk_of = spb::aggregate_validate(k, L, blocks, dims, covered_from);
+    spb::aggregate_run(k, L, chunk_of, blocks, dims, out, ctx->e.dev);
+  });
+}
+
+spb_status spb_aggregate64(int device, int k, int L, const double* const* blocks, const int* dims,
+                           const int* covered_from, double* const* out) {
+  return guard(nullptr, [&] {
+    auto chunk_of = spb::aggregate_validate(k, L, blocks, dims, covered_from);
+    if (device >= 0) SPB_CUDA(cudaSetDevice(device));
+    int dev = 0;
+    SPB_CUDA(cudaGetDevice(&dev));
+    spb::aggregate_run(k, L, chunk_of, blocks, dims, out, dev);
   });
 }
 
@@ -2245,6 +2310,63 @@ spb_status spb_loss(spb_ctx* ctx, double* out) {
       for (int i = 0; i < rows; ++i) total += rl[i];
     }
     *out = total / e.N;
+  });
+}
+
+spb_status spb_loss64(spb_ctx* ctx, const double* const* blocks, const int* samples, int count, double* out) {
+  return guard(ctx, [&] {
+    auto& e = ctx->e;
+    if (!e.X) throw spb::ConfigError("loss: no dataset");
+    if (e.conv_model) throw spb::ConfigError("loss64: ChainMlp contexts only");
+    if (!blocks || !out) throw spb::ArgumentError("loss64: null argument");
+    const int L = e.L;
+    std::vector<long> off(L + 1, 0);
+    long maxw = 0;
+    for (int l = 1; l <= L; ++l) {
+      off[l] = off[l - 1] + static_cast<long>(e.w[l]) * e.w[l - 1] + e.w[l];
+      maxw = std::max<long>(maxw, std::max(e.w[l], e.w[l - 1]));
+    }
+    // Parameters: re-uploaded only when they changed since the last call.
+    bool same = e.p64_host.size() == static_cast<size_t>(off[L]);
+    for (int l = 0; same && l < L; ++l)
+      same = std::memcmp(e.p64_host.data() + off[l], blocks[l], (off[l + 1] - off[l]) * sizeof(double)) == 0;
+    if (!same) {
+      e.p64_host.resize(off[L]);
+      for (int l = 0; l < L; ++l) std::memcpy(e.p64_host.data() + off[l], blocks[l], (off[l + 1] - off[l]) * 8);
+      if (e.p64) cudaFree(e.p64), e.p64 = nullptr;
+      SPB_CUDA(cudaMalloc(&e.p64, off[L] * sizeof(double)));
+      SPB_CUDA(cudaMemcpyAsync(e.p64, e.p64_host.data(), off[L] * sizeof(double), cudaMemcpyHostToDevice, e.st));
+    }
+    const int n = samples ? count : e.N;
+    if (n < 0) throw spb::ArgumentError("loss64: negative count");
+    for (int i = 0; samples && i < n; ++i)
+      if (samples[i] < 0 || samples[i] >= e.N) throw spb::ArgumentError("sample out of range");
+    const int chunk = std::max(1, std::min(n, 2048));
+    const long lda = spb::round_up(maxw, 4);
+    struct DevBuf {
+      void* p = nullptr;
+      ~DevBuf() {
+        if (p) cudaFree(p);
+      }
+    } a, b, rl, ix;
+    SPB_CUDA(cudaMalloc(&a.p, chunk * lda * sizeof(double)));
+    SPB_CUDA(cudaMalloc(&b.p, chunk * lda * sizeof(double)));
+    SPB_CUDA(cudaMalloc(&rl.p, chunk * sizeof(double)));
+    SPB_CUDA(cudaMalloc(&ix.p, chunk * sizeof(int)));
+    std::vector<int> idx(chunk);
+    std::vector<double> host_rl(chunk);
+    double total = 0.0;
+    for (int s0 = 0; s0 < n; s0 += chunk) {
+      const int rows = std::min(chunk, n - s0);
+      for (int i = 0; i < rows; ++i) idx[i] = samples ? samples[s0 + i] : s0 + i;
+      SPB_CUDA(cudaMemcpyAsync(ix.p, idx.data(), rows * sizeof(int), cudaMemcpyHostToDevice, e.st));
+      spb::launch_loss64(e.X, e.ldx, e.Y, static_cast<int*>(ix.p), rows, e.w.data(), L, e.p64, off.data(),
+                         static_cast<double*>(a.p), static_cast<double*>(b.p), lda, static_cast<double*>(rl.p), e.st);
+      SPB_CUDA(cudaMemcpyAsync(host_rl.data(), rl.p, rows * sizeof(double), cudaMemcpyDeviceToHost, e.st));
+      SPB_CUDA(cudaStreamSynchronize(e.st));
+      for (int i = 0; i < rows; ++i) total += host_rl[i];  // sample order, as ChainMlp::loss sums
+    }
+    *out = total;
   });
 }
 

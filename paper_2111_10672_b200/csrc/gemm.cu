@@ -252,6 +252,8 @@ void launch_splitk(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
   // Splits actually populated: ceil(kb / ceil(kb / splits)) can be < splits.
   const int kb = (A.k + kBK - 1) / kBK, kbs = (kb + plan.splits - 1) / plan.splits;
   const int splits = (kb + kbs - 1) / kbs;
+  if (static_cast<long>(splits) * stride > ep.splitk_ws_floats)  // forced plans skip the planner's check
+    throw std::invalid_argument("gemm: split-K workspace too small for this plan");
   if (plan.two_sm) dispatch_2sm<kEpiStoreScaled>(A, B, part, s, plan.pn, splits);
   else if (!A.mn_major && !B.mn_major) launch_inst<128, false, false, kEpiStoreScaled>(A, B, part, s, splits);
   else if (!A.mn_major && B.mn_major) launch_inst<128, false, true, kEpiStoreScaled>(A, B, part, s, splits);

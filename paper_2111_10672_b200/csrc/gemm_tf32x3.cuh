@@ -354,10 +354,31 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpilogue& ep, const flo
 // buffer; the epilogue warps drain each chunk into fp32 registers
 // (round-to-nearest adds) while the MMA warp fills the other buffer. The error
 // is then bounded independently of K.
+// k-blocks per TMEM chunk, per GEMM kind (told apart by operand majorness:
+// forward K x K, dgrad K x MN, wgrad MN x MN -- split-K partials included).
 #ifndef SPB_CHUNK_KB
 #define SPB_CHUNK_KB 4
 #endif
-constexpr int kChunkKb = SPB_CHUNK_KB;  // 32 * kChunkKb of K per TMEM chunk
+#ifndef SPB_CHUNK_KB_FWD
+#define SPB_CHUNK_KB_FWD SPB_CHUNK_KB
+#endif
+// dgrad: 2 (64 of K per chunk). The dgrad chain carries the truncation bias
+// through every layer of the backward (Delta_{l-1} from Delta_l): at the full
+// cfg3 depth (16 layers) chunk 4 leaves layer 1's aggregate at 1.12e-5 of the
+// fp64 reference, chunk 2 at 7.2e-6, at the same step time (5.73 vs 5.78 ms;
+// the dgrads are split-K / HBM-heavy, the TMEM drains hide). Forward and
+// wgrad chunk size barely moves the error (tools/chunk_experiment.py,
+// profiles/r02_chunk_experiment.jsonl).
+#ifndef SPB_CHUNK_KB_DGRAD
+#define SPB_CHUNK_KB_DGRAD 2
+#endif
+#ifndef SPB_CHUNK_KB_WGRAD
+#define SPB_CHUNK_KB_WGRAD SPB_CHUNK_KB
+#endif
+template <bool A_MN, bool B_MN>
+__host__ __device__ constexpr int chunk_kb() {
+  return (A_MN && B_MN) ? SPB_CHUNK_KB_WGRAD : ((!A_MN && B_MN) ? SPB_CHUNK_KB_DGRAD : SPB_CHUNK_KB_FWD);
+}
 
 // Implicit-GEMM convolution operands (3x3, padding 1, NHWC, c_in % 32 == 0):
 // the tensor maps are TMA im2col maps of the activation tensor and the tile
@@ -391,6 +412,7 @@ __global__ void __launch_bounds__(256, 1)
                        const __grid_constant__ CUtensorMap tw_lo, const __grid_constant__ CUtensorMap tw_mom,
                        const ConvTmaArgs ic, const __grid_constant__ CUtensorMap t_ones) {
   using Cfg = GemmCfg<BN, TMA_UPD>;
+  constexpr int kChunkKb = chunk_kb<A_MN, B_MN>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);

@@ -283,6 +283,20 @@ __global__ void aggregate_kernel(const float* const* __restrict__ srcs, int m, l
   }
 }
 
+// fp64 aggregate with the reference's exact operation sequence (spb.cpp:97-103):
+// dst += src for the contributors in ascending worker order, then dst *= inv
+// (inv = 1.0 / m from the host); explicit round-to-nearest ops, no FMA
+// contraction, so results are bit-identical to the CPU code.
+__global__ void aggregate64_kernel(const double* const* __restrict__ srcs, int m, long n, double inv,
+                                   double* __restrict__ out) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long c = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; c < n; c += stride) {
+    double s = 0.0;
+    for (int w = 0; w < m; ++w) s = __dadd_rn(s, srcs[w][c]);
+    out[c] = __dmul_rn(s, inv);
+  }
+}
+
 __global__ void split_kernel(const float* __restrict__ in, long n, float* __restrict__ hi, float* __restrict__ lo) {
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
   for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -424,6 +438,12 @@ void launch_sqdist(const float* a, const float* b, long n, double* out, cudaStre
 void launch_aggregate(const float* const* srcs_dev, int m, long n, float* out, cudaStream_t s) {
   if (n <= 0) return;
   aggregate_kernel<<<grid_for(n, 256), 256, 0, s>>>(srcs_dev, m, n, out);
+  SPB_CUDA(cudaGetLastError());
+}
+
+void launch_aggregate64(const double* const* srcs_dev, int m, long n, double* out, cudaStream_t s) {
+  if (n <= 0) return;
+  aggregate64_kernel<<<grid_for(n, 256), 256, 0, s>>>(srcs_dev, m, n, 1.0 / static_cast<double>(m), out);
   SPB_CUDA(cudaGetLastError());
 }
 

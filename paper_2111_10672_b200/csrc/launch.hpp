@@ -120,12 +120,20 @@ void launch_sgd_update(float* p_hi, float* p_lo, const float* grad, float* mom, 
                        float wd, cudaStream_t s, int ctas = 0);
 // out[c] = (sum_{w} src[w][c]) / m for w ascending (aggregate, spb.cpp:97-103).
 void launch_aggregate(const float* const* srcs_dev, int m, long n, float* out, cudaStream_t s);
+// fp64 variant with the reference's exact sum-then-scale sequence (bit-identical).
+void launch_aggregate64(const double* const* srcs_dev, int m, long n, double* out, cudaStream_t s);
 // *out += sum over [0, n) of (a - b)^2 in fp64 (n a multiple of 4).
 void launch_sqdist(const float* a, const float* b, long n, double* out, cudaStream_t s);
 void launch_split(const float* in, long n, float* hi, float* lo, cudaStream_t s);
 void launch_join(const float* hi, const float* lo, long n, float* out, cudaStream_t s);
 // Also advances *step_dev (nullable): the next step's Rng stream.
 void launch_sum_loss(const float* row_loss, int rows, float scale, float* out, int* step_dev, cudaStream_t s);
+// fp64 ChainMlp loss rows (eval64.cu): row_loss[r] = 0.5 ||out - y||^2 of
+// sample idx[r], params in the reference block layout (block l-1 at
+// params + block_off[l-1]); act_a / act_b: [rows x ld_act] fp64 scratch.
+void launch_loss64(const float* X, long ldx, const float* Y, const int* idx, int rows, const int* widths, int L,
+                   const double* params, const long* block_off, double* act_a, double* act_b, long ld_act,
+                   double* row_loss, cudaStream_t s);
 // One thread writes %globaltimer (ns) to *slot (timeline tracing).
 void launch_stamp(unsigned long long* slot, cudaStream_t s);
 

@@ -21,7 +21,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libspb_b200.so")
+LIB_PATH = os.environ.get("SPB_LIB_PATH", os.path.join(_PKG, "libspb_b200.so"))  # override: tuning variants
 
 
 class SpbError(Exception):
@@ -89,6 +89,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "spb_set_optimizer": (i, [vp, f, f, f]),
         "spb_partial_backprop": (i, [vp, ip, i, i, vp, C.POINTER(C.c_longlong), ip]),
         "spb_aggregate": (i, [vp, i, i, vp, ip, ip, vp]),
+        "spb_aggregate64": (i, [i, i, i, vp, ip, ip, vp]),
+        "spb_loss64": (i, [vp, vp, ip, i, C.POINTER(C.c_double)]),
         "spb_train_steps": (i, [vp, u64, i, i, i, fp]),
         "spb_step_host": (i, [vp, fp, fp, i, fp]),
         "spb_loss": (i, [vp, C.POINTER(C.c_double)]),
@@ -125,7 +127,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 EXPORTED = [
     "spb_last_error", "spb_suffix_layers", "spb_chunk_coverage", "spb_chunk_layout", "spb_layer_chunks",
     "spb_draw_batch", "spb_rank_workers", "spb_create", "spb_destroy", "spb_set_dataset", "spb_set_params",
-    "spb_get_params", "spb_set_optimizer", "spb_partial_backprop", "spb_aggregate", "spb_train_steps",
+    "spb_get_params", "spb_set_optimizer", "spb_partial_backprop", "spb_aggregate", "spb_aggregate64", "spb_loss64", "spb_train_steps",
     "spb_step_host", "spb_loss", "spb_synchronize", "spb_stream", "spb_comm_unique_id", "spb_comm_init",
     "spb_last_batch", "spb_launches_per_step", "spb_make_random_chain_mlp",
     "spb_get_grads", "spb_profile_step", "spb_time_train_steps", "spb_bucket_plan", "spb_set_fused_update",

@@ -135,7 +135,7 @@ static int run_shapes() {
   gemm_prepare_device();  // the fused-bias ones boxes
   std::mt19937_64 rng(77);
   float *ws;
-  const long ws_floats = 16L << 20;
+  const long ws_floats = 64L << 20;  // room for the forced 3-way split-K of a 4096 x 4097 wgrad
   cudaMalloc(&ws, ws_floats * 4);
   // Weights U(+-1/64) like make_random_chain_mlp's U(-1/sqrt(n), 1/sqrt(n)); activations in (-1, 1).
   std::vector<float> W = rand_vec(static_cast<long>(n) * n, rng, 1.f / 64), bias = rand_vec(n, rng, 1.f / 64);
