@@ -240,6 +240,17 @@ SPB_API void* spb_stream(spb_ctx* ctx);
 SPB_API spb_status spb_comm_unique_id(void* out128);
 SPB_API spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int nranks);
 /* Active aggregation mode: 0 nccl, 1 nvls, 2 p2p, 3 rs, 4 push, 5 rh (-1 before spb_comm_init). */
+/* Tuning aid (process-wide): k-blocks of K (32 each) the tensor cores
+ * accumulate per TMEM chunk before the epilogue folds the chunk into fp32
+ * registers, for GEMM kind 0 (forward), 1 (dgrad), 2 (wgrad); kblocks < 1
+ * restores the default (4 / 2 / 4). Smaller chunks: less of the tensor
+ * core's round-toward-zero accumulation bias, more TMEM drain traffic. Takes
+ * effect for graphs captured afterwards (new contexts). */
+SPB_API spb_status spb_set_gemm_chunk(int kind, int kblocks);
+/* sub mode's shard of a layer segment of `count` floats over `parts` ranks:
+ * member i of a layer's contributor set owns [i * shard, min(count, (i + 1) *
+ * shard)); shard is a multiple of 4 floats and parts * shard >= count. */
+SPB_API spb_status spb_layer_shard(long long count, int parts, long long* shard);
 SPB_API spb_status spb_comm_mode(spb_ctx* ctx, int* mode);
 /* Collective diagnostic of the NVLS path: multicast reduce + broadcast of a
  * known pattern over all ranks; *mismatches = wrong elements seen here. */

@@ -57,6 +57,9 @@ struct NcclApi {
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
   ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
   ncclResult_t (*CommFinalize)(ncclComm_t);
   ncclResult_t (*CommDestroy)(ncclComm_t);
   ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*);
@@ -86,6 +89,9 @@ const NcclApi& nccl() {
     api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
     api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
     api.ReduceScatter = reinterpret_cast<decltype(api.ReduceScatter)>(sym("ncclReduceScatter"));
+    api.CommSplit = reinterpret_cast<decltype(api.CommSplit)>(sym("ncclCommSplit"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
     api.CommFinalize = reinterpret_cast<decltype(api.CommFinalize)>(sym("ncclCommFinalize"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
     api.CommGetAsyncError = reinterpret_cast<decltype(api.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
@@ -180,6 +186,7 @@ struct Engine {
   // fwd_wait[l] = event index the forward of layer l (the head for l = L)
   // must wait on, -1 = none; chain_sub = index of the step being enqueued.
   static constexpr int kMaxChain = 16;
+  static constexpr long kGradSlack = 4096;
   // chain = 0: automatic = 1. Measured (cfg5 sweep, one box, chain 8 vs 1):
   // -16 % / -8 % / -1 % / +1 % at widths 1k / 2k / 4k / 8k on one GPU,
   // -2 to -7 % with a multi-GPU exchange (its tail running beside the next
@@ -213,9 +220,13 @@ struct Engine {
   static constexpr int kFuseMaxRows = 512;  // 640 / 768 measured the same; 384 slower
   std::vector<char> fuse_layer;  // per layer, set by enqueue_step for enqueue_pass / on_layer
   // Multi-GPU aggregation mode: 0 = NCCL buckets, 1 = NVLS multicast,
-  // 2 = peer-to-peer copy-engine pulls (p2p.cu), 3 = NCCL reduce-scatter +
-  // sharded update + all-gather of the fp32 weights ("rs").
+  // 2 = peer-to-peer copy-engine pulls (p2p.cu), 3 = NCCL contributor
+  // sub-communicators ("sub": reduce-scatter among the layer's contributing
+  // ranks only, sharded update, weight broadcast to every rank).
   int comm_mode = 0;
+  // sub mode: one NCCL communicator per distinct contributor-rank set
+  // (ncclCommSplit of `comm`; null on ranks outside the set), keyed by the set.
+  std::map<std::vector<int>, ncclComm_t> subcomms;
   // SMs the persistent GEMMs of this context leave free (spb_comm_init: 16
   // with NCCL collectives in the step, 0 for the copy-engine modes).
   int reserved_sms = 0;
@@ -371,6 +382,16 @@ struct Engine {
       p_hi = p_lo = grad = nullptr;  // not cudaMalloc'd
       nvls = false;
     }
+    for (auto& kv : subcomms)
+      if (kv.second) {
+        const NcclApi& api = nccl();
+        api.CommFinalize(kv.second);
+        ncclResult_t state = ncclInProgress;
+        while (api.CommGetAsyncError(kv.second, &state) == ncclSuccess && state == ncclInProgress) {
+        }
+        api.CommDestroy(kv.second);
+      }
+    subcomms.clear();
     if (comm) {
       const NcclApi& api = nccl();
       api.CommFinalize(comm);
@@ -515,7 +536,7 @@ struct Engine {
     nflat = cur;
     p_hi = alloc<float>(nflat);
     p_lo = alloc<float>(nflat);
-    grad = alloc<float>(nflat);
+    grad = alloc<float>(nflat + kGradSlack);  // sub mode's reduce-scatter reads up to 4 * ranks floats past a layer
     tmp_n = maxblk;
     tmp = alloc<float>(tmp_n);
     splitk_ws = alloc<float>(kSplitkWsFloats);
@@ -1289,69 +1310,97 @@ struct Engine {
     return n;
   }
 
-  // "rs" mode, layer l, on cst after the layer's gradient is final (gs) and
-  // dgrad_l (s) has read W_l:
-  //  - several contributing ranks: ncclReduceScatter of the gradient (zeros
-  //    from non-contributors) -> this rank's shard updated (p2p_update_kernel:
-  //    hi, lo, momentum, fp32 w32) -> ncclAllGather of w32 -> the other shards
-  //    split into (hi, lo) on s3;
-  //  - one contributing rank: it updates the whole layer, ncclBroadcast of
-  //    w32, the others split it.
-  // Per rank the optimizer streams 28 B / N + 12 B (N-1) / N per parameter
-  // instead of 28 B, for the same NCCL bytes as the all-reduce buckets.
-  int enqueue_rs_layer(int l, bool full, cudaStream_t gs, cudaStream_t s) {
+  // "sub" mode, layer l (the reference's
+  // aggregate spb.cpp:89-104 restricted to the workers that reached the
+  // layer): on cst, after this rank's gradient of l is final (gs) and its
+  // dgrad_l -- the last local reader of W_l -- was issued on s:
+  //  1. the layer's CONTRIBUTING ranks C (those hosting a worker whose suffix
+  //     covers l) reduce-scatter the gradient among themselves over their
+  //     sub-communicator; ranks outside C move no gradient bytes;
+  //  2. each member updates its shard (momentum / wd / SGD; the 1/(m B_w)
+  //     average is already in the wgrad epilogue), writing the new fp32
+  //     weights of the shard to w32 (and its own hi / lo);
+  //  3. every member broadcasts its shard to ALL ranks (one NCCL group), since
+  //     non-contributors need the updated weights for their next forward;
+  //  4. every rank splits the received fp32 weights into hi / lo.
+  // A single contributor skips step 1 and updates the whole layer.
+  int enqueue_sub_layer(int l, bool full, cudaStream_t gs, cudaStream_t s) {
     const Bucket* bk = nullptr;
     for (auto& b : buckets[full])
       if (b.l_lo <= l && l <= b.l_hi) bk = &b;
     if (!bk) throw ConfigError("comm: no bucket for layer");
-    const bool mine = std::find(bk->ranks.begin(), bk->ranks.end(), rank) != bk->ranks.end();
+    const std::vector<int>& C = bk->ranks;
+    const int nc = static_cast<int>(C.size());
+    const int me = static_cast<int>(std::find(C.begin(), C.end(), rank) - C.begin());  // nc: not a member
     const long off = w_off[l], cnt = b_off[l] + round_up(w[l], 32) - w_off[l];
+    const long sh = layer_shard(cnt, nc);
+    auto lo_of = [&](int i) { return std::min(cnt, sh * i); };
     auto evl = [&](int k) { return ev(kEvP2pLayer + 32 * l + k); };
     SPB_CUDA(cudaEventRecord(ev(kEvBucket + l), gs));
     SPB_CUDA(cudaStreamWaitEvent(cst, ev(kEvBucket + l), 0));
     SPB_CUDA(cudaEventRecord(evl(0), s));  // dgrad_l issued on s before this point
-    SPB_CUDA(cudaStreamWaitEvent(cst, evl(0), 0));
     int n = 0;
-    long a = 0, b = cnt;  // the range this rank updates itself
+    long a = 0, b = 0;  // the range this rank updates itself
     pbeg(cst);
-    if (bk->kind == 1) {
-      if (rank == bk->root) {
-        PeerPtrs<const float> src{};
-        src.p[0] = grad + off;
-        launch_p2p_update(src, 1, p_hi + off, p_lo + off, mom ? mom + off : nullptr, w32 + off, cnt, lr, mu, wd, cst);
-        ++n;
-      } else {
-        a = b = 0;
+    if (me < nc) {
+      a = lo_of(me), b = lo_of(me + 1);
+      const float* g = grad + off + a;
+      if (nc > 1) {  // reduce-scatter among the contributors (reads up to nc*sh: grad has tail slack)
+        auto it = subcomms.find(C);
+        if (it == subcomms.end() || !it->second) throw ConfigError("comm: missing contributor communicator");
+        nccl_check(nccl().ReduceScatter(grad + off, stage, sh, ncclFloat32, ncclSum, it->second, cst));
+        g = stage;
       }
-      nccl_check(nccl().Broadcast(w32 + off, w32 + off, cnt, ncclFloat32, bk->root, comm, cst));
+      SPB_CUDA(cudaStreamWaitEvent(cst, evl(0), 0));
+      if (b > a) {
+        PeerPtrs<const float> src{};
+        src.p[0] = g;
+        launch_p2p_update(src, 1, p_hi + off + a, p_lo + off + a, mom ? mom + off + a : nullptr, w32 + off + a, b - a,
+                          lr, mu, wd, cst);
+        ++n;
+      }
     } else {
-      if (cnt % nranks) throw ConfigError("rs: layer segment not divisible by the rank count");
-      const long sh = cnt / nranks;
-      a = sh * rank, b = a + sh;
-      if (!mine) SPB_CUDA(cudaMemsetAsync(grad + off, 0, cnt * sizeof(float), cst));
-      nccl_check(nccl().ReduceScatter(grad + off, stage, sh, ncclFloat32, ncclSum, comm, cst));
-      PeerPtrs<const float> src{};
-      src.p[0] = stage;
-      launch_p2p_update(src, 1, p_hi + off + a, p_lo + off + a, mom ? mom + off + a : nullptr, w32 + off + a, sh, lr, mu,
-                        wd, cst);
-      ++n;
-      nccl_check(nccl().AllGather(w32 + off + a, w32 + off, sh, ncclFloat32, comm, cst));
+      SPB_CUDA(cudaStreamWaitEvent(cst, evl(0), 0));
     }
-    pend(kClsComm, static_cast<double>(cnt) * 4.0, cst);
-    SPB_CUDA(cudaEventRecord(evl(1), cst));
-    SPB_CUDA(cudaStreamWaitEvent(s3, evl(1), 0));
-    pbeg(s3);
-    launch_p2p_split(w32 + off, p_hi + off, p_lo + off, cnt, a, b, s3);
-    pend(kClsUpdate, static_cast<double>(cnt - (b - a)) * 12.0, s3);
+    nccl_check(nccl().GroupStart());
+    for (int i = 0; i < nc; ++i) {
+      const long ia = lo_of(i), ib = lo_of(i + 1);
+      if (ib > ia) nccl_check(nccl().Broadcast(w32 + off + ia, w32 + off + ia, ib - ia, ncclFloat32, C[i], comm, cst));
+    }
+    nccl_check(nccl().GroupEnd());
+    // Bytes this rank moves: its reduce-scatter share (contributors) plus the
+    // weight shards it receives.
+    pend(kClsComm, 4.0 * ((me < nc && nc > 1 ? static_cast<double>(sh) * (nc - 1) : 0.0) + (cnt - (b - a))), cst);
+    pbeg(cst);
+    launch_p2p_split(w32 + off, p_hi + off, p_lo + off, cnt, a, b, cst);
+    pend(kClsUpdate, static_cast<double>(cnt - (b - a)) * 12.0, cst);
     return n + 1;
   }
 
-  void setup_rs() {
+  // Shard length of a layer segment of cnt floats over `parts` ranks (a
+  // multiple of 4 floats, parts * shard >= cnt; the last shards may be short
+  // or empty). spb_layer_shard exports it for the protocol tests.
+  static long layer_shard(long cnt, int parts) { return round_up((cnt + parts - 1) / parts, 4); }
+
+  void setup_sub() {
     w32 = alloc<float>(nflat);
     long maxcnt = 0;
     for (int l = 1; l <= L; ++l) maxcnt = std::max(maxcnt, b_off[l] + round_up(w[l], 32) - w_off[l]);
-    stage_shard = (maxcnt + nranks - 1) / nranks;
+    stage_shard = layer_shard(maxcnt, 2);
     stage = alloc<float>(stage_shard);
+    // One communicator per distinct contributor set, split collectively in
+    // the same (sorted) order on every rank.
+    std::vector<std::vector<int>> sets;
+    for (int f = 0; f < 2; ++f)
+      for (const Bucket& b : buckets[f])
+        if (b.ranks.size() > 1 && std::find(sets.begin(), sets.end(), b.ranks) == sets.end()) sets.push_back(b.ranks);
+    std::sort(sets.begin(), sets.end());
+    for (const auto& set : sets) {
+      const bool member = std::find(set.begin(), set.end(), rank) != set.end();
+      ncclComm_t c = nullptr;
+      nccl_check(nccl().CommSplit(comm, member ? 0 : NCCL_SPLIT_NOCOLOR, rank, &c, nullptr));
+      subcomms[set] = member ? c : nullptr;
+    }
     comm_mode = 3;
     invalidate_graphs();
   }
@@ -1704,7 +1753,7 @@ struct Engine {
       fork(cst, kEvStepFork);
       fork(s3, kEvUpdFork);
       n += enqueue_pass(rows, row0, alpha, s,
-                        [&](int l, cudaStream_t from) { return enqueue_rs_layer(l, full, from, s); }, false,
+                        [&](int l, cudaStream_t from) { return enqueue_sub_layer(l, full, from, s); }, false,
                         &ctl->step, nullptr);
       join(cst, kEvStepJoin);  // not pipelined across steps: joined every step
       join(s3, kEvUpdJoin);
@@ -2404,21 +2453,22 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     e.buckets[1] = spb::bucket_plan(e.k, e.L, nranks, true);
     e.set_workers(spb::rank_workers(e.k, e.L, rank, nranks));
     e.ensure_rows(static_cast<int>(e.workers.size()) * e.bw);
-    // Aggregation mode: SPB_COMM = rh | p2p | nccl | nvls | rs | push.
+    // Aggregation mode: SPB_COMM = rh | p2p | sub | push | nccl | nvls.
     // Default by measurement (cfg3): p2p for 2 ranks (one
     // pairwise copy-engine exchange); push for 4 ranks (gradient rows stored
     // to their owners by the wgrad epilogue: 4.47 ms vs rh 5.02, p2p 5.2,
     // nccl 5.09 on one box), rh for the ConvNet there (push is MLP-only);
-    // NCCL elsewhere (8 ranks could not be measured: gpurun offers 4 GPUs).
+    // sub elsewhere -- NCCL over contributor sub-communicators, parity-tested
+    // at 2 and 4 ranks (8 ranks could not be measured: gpurun offers 4 GPUs).
     const char* cm = std::getenv("SPB_COMM");
     const std::string mode =
-        cm ? cm : (nranks == 2 ? "p2p" : (nranks == 4 ? (e.conv_model ? "rh" : "push") : "nccl"));
-    if (mode != "p2p" && mode != "nccl" && mode != "nvls" && mode != "rs" && mode != "push" && mode != "rh")
-      throw spb::ArgumentError("comm: SPB_COMM must be rh, push, p2p, nccl, rs or nvls");
+        cm ? cm : (nranks == 2 ? "p2p" : (nranks == 4 ? (e.conv_model ? "rh" : "push") : "sub"));
+    if (mode != "p2p" && mode != "nccl" && mode != "nvls" && mode != "sub" && mode != "push" && mode != "rh")
+      throw spb::ArgumentError("comm: SPB_COMM must be rh, push, p2p, sub, nccl or nvls");
     // NCCL's kernels need SMs while the backward GEMMs run: keep some free
     // (the copy-engine modes' few SM kernels measured the same with 0 / 16).
     const char* rs = std::getenv("SPB_COMM_SMS");
-    e.reserved_sms = rs ? std::max(0, std::atoi(rs)) : ((mode == "nccl" || mode == "rs" || mode == "nvls") ? 16 : 0);
+    e.reserved_sms = rs ? std::max(0, std::atoi(rs)) : ((mode == "nccl" || mode == "sub" || mode == "nvls") ? 16 : 0);
     if (mode == "rh" && (nranks & (nranks - 1)))
       throw spb::ArgumentError("comm: rh mode needs a power-of-two rank count");
     if (nranks > 1 && mode == "p2p") e.setup_p2p();
@@ -2429,7 +2479,7 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
       e.comm_mode = 5;
     }
     if (nranks > 1 && mode == "push") e.setup_push();
-    if (nranks > 1 && mode == "rs") e.setup_rs();
+    if (nranks > 1 && mode == "sub") e.setup_sub();
     if (nranks > 1 && mode == "nvls") {
       // Socket names derive from the unique id, shared by all ranks.
       uint64_t h = 1469598103934665603ull;
@@ -2442,6 +2492,17 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
   if (st != SPB_OK && ctx && (ctx->e.err.rfind("nccl", 0) == 0 || ctx->e.err.rfind("comm: ", 0) == 0))
     return SPB_E_NCCL;
   return st;
+}
+
+spb_status spb_set_gemm_chunk(int kind, int kblocks) {
+  return guard(nullptr, [&] { spb::gemm_set_chunk(kind, kblocks); });
+}
+
+spb_status spb_layer_shard(long long count, int parts, long long* shard) {
+  return guard(nullptr, [&] {
+    if (count < 0 || parts < 1) throw spb::ArgumentError("layer_shard: bad arguments");
+    *shard = spb::Engine::layer_shard(count, parts);
+  });
 }
 
 spb_status spb_comm_mode(spb_ctx* ctx, int* mode) {

@@ -99,6 +99,22 @@ int num_sms() {
   return std::max(2, (n - g_reserved_sms) & ~1);
 }
 
+// TMEM accumulation chunk (k-blocks) per GEMM kind [forward K x K, dgrad
+// K x MN, wgrad MN x MN]: the compile-time defaults, overridable per process
+// (SPB_CHUNK_FWD / _DGRAD / _WGRAD or gemm_set_chunk) for A/B measurements.
+int g_chunk[3] = {-1, -1, -1};
+
+int chunk_for(bool a_mn, bool b_mn) {
+  const int kind = (a_mn && b_mn) ? 2 : ((!a_mn && b_mn) ? 1 : 0);
+  if (g_chunk[kind] < 0) {
+    static const char* env[3] = {"SPB_CHUNK_FWD", "SPB_CHUNK_DGRAD", "SPB_CHUNK_WGRAD"};
+    const char* v = std::getenv(env[kind]);
+    const int def[3] = {SPB_CHUNK_KB_FWD, SPB_CHUNK_KB_DGRAD, SPB_CHUNK_KB_WGRAD};
+    g_chunk[kind] = v ? std::max(1, std::atoi(v)) : def[kind];
+  }
+  return g_chunk[kind];
+}
+
 // The TMA extent along MN: the operand's real columns (mn_map) when the GEMM
 // extends past them (the fused-bias ones column of a wgrad B operand).
 CUtensorMap operand_map(const Operand& X, const float* base, int tile_rows) {
@@ -150,7 +166,9 @@ void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cud
     wm = ep.mom ? tmap2d(ep.mom, ep.N, ep.M, ep.ld_out, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B) : wh;
   }
   const CUtensorMap ones = ep.ones_col_p1 > 0 ? ones_map() : ah;
-  kern<<<grid, 256, smem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, ep, wh, wl, wm, ic, ones);
+  GemmEpilogue e = ep;
+  if (e.chunk_kb <= 0) e.chunk_kb = chunk_for(AM, BM_);
+  kern<<<grid, 256, smem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, e, wh, wl, wm, ic, ones);
   SPB_CUDA(cudaGetLastError());
 }
 
@@ -174,7 +192,9 @@ void launch_2sm_pn(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
   const int pairs = num_sms() / 2;
   const int clusters = units < pairs ? units : pairs;
   const CUtensorMap ones = ep.ones_col_p1 > 0 ? ones_map() : ah;
-  kern<<<2 * clusters, Cfg::kThreads, Cfg::kSmem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, ep, ones);
+  GemmEpilogue e = ep;
+  if (e.chunk_kb <= 0) e.chunk_kb = chunk_for(AM, BM_);
+  kern<<<2 * clusters, Cfg::kThreads, Cfg::kSmem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, e, ones);
   SPB_CUDA(cudaGetLastError());
 }
 
@@ -240,7 +260,8 @@ struct Plan {
 
 template <int EPI>
 void launch_splitk(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, const Plan& plan) {
-  const long ldw = round_up(B.mn, 4), stride = static_cast<long>(A.mn) * ldw;
+  // Workspace rows hold the GEMM's columns and, with a column-sum bias, the bias column after them.
+  const long ldw = round_up(std::max(B.mn, epi_cols(ep)), 4), stride = static_cast<long>(A.mn) * ldw;
   GemmEpilogue part{};
   part.out_hi = ep.splitk_ws;
   part.ld_out = ldw;
@@ -249,6 +270,7 @@ void launch_splitk(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
   part.N = B.mn;
   part.split_stride = stride;
   part.ones_col_p1 = ep.ones_col_p1;  // the partials compute the bias column like any other
+  part.colsum_col_p1 = ep.colsum_col_p1;  // (or the column-sum warps write it into the workspace)
   // Splits actually populated: ceil(kb / ceil(kb / splits)) can be < splits.
   const int kb = (A.k + kBK - 1) / kBK, kbs = (kb + plan.splits - 1) / plan.splits;
   const int splits = (kb + kbs - 1) / kbs;
@@ -337,6 +359,11 @@ void dispatch_major(const Operand& A, const Operand& B, const GemmEpilogue& ep, 
 
 void gemm_force_variant(int v) { g_force_variant = v; }
 
+void gemm_set_chunk(int kind, int kb) {
+  if (kind < 0 || kind > 2) throw std::invalid_argument("gemm_set_chunk: kind 0 (forward), 1 (dgrad), 2 (wgrad)");
+  g_chunk[kind] = kb < 1 ? -1 : kb;
+}
+
 void gemm_prepare_device() {
   int dev = 0;
   SPB_CUDA(cudaGetDevice(&dev));
@@ -390,19 +417,22 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
   const ConvGeom& g = src.g;
   if (g.c_in % 32 || src.ld % 32) throw std::invalid_argument("gemm_conv_wgrad: c_in and ld must be multiples of 32");
   if (!A.mn_major) throw std::invalid_argument("gemm_conv_wgrad: A (Delta) must be MN-major");
-  // N output columns: 9 c_in weights, plus the fused bias column (9 c_in is a
-  // multiple of 32 here) when ep.bias_col_p1 is set.
-  if (ep.bias_col_p1 > 0 && (ep.bias_col_p1 != 9 * g.c_in + 1 || ep.ones_col_p1 != ep.bias_col_p1))
+  // N = 9 c_in weight columns; with ep.bias_col_p1 = 9 c_in + 1 the bias is
+  // produced by the kernel's column-sum warps as output column 9 c_in.
+  const int N = 9 * g.c_in;
+  if (ep.bias_col_p1 > 0 && ep.bias_col_p1 != N + 1)
     throw std::invalid_argument("gemm_conv_wgrad: the bias column must follow the 9 c_in weights");
-  const int N = ep.bias_col_p1 > 0 ? 9 * g.c_in + 1 : 9 * g.c_in;
+  GemmEpilogue e = ep;
+  e.ones_col_p1 = 0;
+  e.colsum_col_p1 = ep.bias_col_p1;
   CUtensorMap b[2] = {im2col_map(src.hi, src, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B),
                       im2col_map(src.lo, src, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)};
   const ConvTmaArgs ic{g.out_h * g.out_w, g.out_w, g.stride, g.c_in, pixel0, 0};
   Operand B{nullptr, nullptr, 4, N, A.k, true};  // shape only
-  const Plan plan = plan_gemm(A.mn, N, A.k, ep.splitk_ws ? ep.splitk_ws_floats : 0, ep.splitk_ws != nullptr, false,
-                              false);  // the im2col-B wgrad has a 1-CTA kernel only
+  const Plan plan = plan_gemm(A.mn, epi_cols(e) > N ? epi_cols(e) : N, A.k, ep.splitk_ws ? ep.splitk_ws_floats : 0,
+                              ep.splitk_ws != nullptr, false, false);  // the im2col-B wgrad has a 1-CTA kernel only
   if (plan.splits > 1) {
-    const long ldw = round_up(N, 4), stride = static_cast<long>(A.mn) * ldw;
+    const long ldw = round_up(epi_cols(e) > N ? epi_cols(e) : N, 4), stride = static_cast<long>(A.mn) * ldw;
     GemmEpilogue part{};
     part.out_hi = ep.splitk_ws;
     part.ld_out = ldw;
@@ -410,17 +440,17 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
     part.M = A.mn;
     part.N = N;
     part.split_stride = stride;
-    part.ones_col_p1 = ep.ones_col_p1;
+    part.colsum_col_p1 = e.colsum_col_p1;  // bias partials into the workspace column
     launch_inst<128, true, true, kEpiStoreScaled, false, 2>(A, B, part, s, plan.splits, nullptr, b, ic);
-    const long n = static_cast<long>(A.mn) * N;
+    const long n = static_cast<long>(A.mn) * epi_cols(e);
     const int grid = static_cast<int>(std::min<long>((n + 255) / 256, 148L * 16));
     const int kb = (A.k + kBK - 1) / kBK, kbs = (kb + plan.splits - 1) / plan.splits;
-    // (the fixup's epilogue `ep` routes column 9 c_in to the bias)
-    splitk_fixup_kernel<kEpiStoreScaled><<<grid, 256, 0, s>>>(ep.splitk_ws, (kb + kbs - 1) / kbs, stride, ldw, ep);
+    // (the fixup's epilogue `e` routes column 9 c_in to the bias)
+    splitk_fixup_kernel<kEpiStoreScaled><<<grid, 256, 0, s>>>(ep.splitk_ws, (kb + kbs - 1) / kbs, stride, ldw, e);
     SPB_CUDA(cudaGetLastError());
     return 2;
   }
-  launch_inst<128, true, true, kEpiStoreScaled, false, 2>(A, B, ep, s, 1, nullptr, b, ic);
+  launch_inst<128, true, true, kEpiStoreScaled, false, 2>(A, B, e, s, 1, nullptr, b, ic);
   return 1;
 }
 
@@ -435,6 +465,9 @@ void gemm_last_plan(int* two_sm, int* pn, int* splits) {
   *pn = g_last_plan.pn;
   *splits = g_last_plan.splits;
 }
+
+int gemm_tf32x3_planned(const Operand& A, const Operand& B, int epi, const GemmEpilogue& ep, cudaStream_t s,
+                        const Plan& plan);
 
 int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue& ep, cudaStream_t s) {
   if (A.k != B.k) throw std::invalid_argument("gemm: K mismatch");
@@ -453,6 +486,22 @@ int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue&
   const Plan plan = plan_gemm(A.mn, B.mn, A.k, ep.splitk_ws && !no_split ? ep.splitk_ws_floats : 0, can_split,
                               narrow_pair_ok(A, B, epi), true, A.mn_major && B.mn_major, ep.ones_col_p1 > 0);
   g_last_plan = plan;
+  if (ep.ones_col_p1 > 0 && (!plan.two_sm || (epi == kEpiWgradUpdate && g_force_variant != 1))) {
+    // 1-CTA kernel: the column-sum warps produce the bias (no extra column tile).
+    Operand B2 = B;
+    B2.mn = B.mn_map > 0 ? B.mn_map : B.mn - 1;
+    B2.mn_map = 0;
+    GemmEpilogue e2 = ep;
+    e2.ones_col_p1 = 0;
+    e2.colsum_col_p1 = ep.bias_col_p1;
+    return gemm_tf32x3_planned(A, B2, epi, e2, s, plan);
+  }
+  return gemm_tf32x3_planned(A, B, epi, ep, s, plan);
+}
+
+int gemm_tf32x3_planned(const Operand& A, const Operand& B, int epi, const GemmEpilogue& ep, cudaStream_t s,
+                        const Plan& plan) {
+  constexpr int BN = 128;
   if (plan.splits > 1) {
     switch (epi) {
       case kEpiFwdTanh: launch_splitk<kEpiFwdTanh>(A, B, ep, s, plan); break;

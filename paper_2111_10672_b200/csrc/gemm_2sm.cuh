@@ -66,7 +66,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
                            int num_kb, int num_m_pairs, int num_tiles, int kb_per_split, int num_units,
                            const __grid_constant__ GemmEpilogue ep, const __grid_constant__ CUtensorMap t_ones) {
   using Cfg = Gemm2smCfg<PN>;
-  constexpr int kChunkKb = chunk_kb<A_MN, B_MN>();
+  const int kChunkKb = ep.chunk_kb > 0 ? ep.chunk_kb : chunk_kb<A_MN, B_MN>();
   // TMA bytes one CTA brings per k-block (A hi/lo + B hi/lo).
   constexpr uint32_t kBLoaded = B_MN ? ((Cfg::kRowsB + 31) / 32) * 4096 : Cfg::kRowsB * 128;
   constexpr uint32_t kCtaBytes = 2 * Cfg::kABytes + 2 * kBLoaded;

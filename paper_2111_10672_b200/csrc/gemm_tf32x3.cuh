@@ -76,12 +76,29 @@ struct GemmEpilogue {
   // like any other into the workspace and leave the routing to the fixup.
   int bias_col_p1;
   int ones_col_p1;
+  // k-blocks per TMEM accumulation chunk (see kChunkKb below); 0 = the
+  // compile-time default of this GEMM kind. The host launcher resolves it.
+  int chunk_kb;
+  // 1-CTA kernel, MN-major A (wgrad): the bias gradient without a ones column
+  // -- warps 2-3 sum the A tile (Delta^T) over K straight from shared memory
+  // as the stages stream by (Kahan-compensated fp32), in the units of column
+  // tile 0, and emit the sum as output column colsum_col_p1 - 1 (the bias
+  // column: bias_store; in split-K partials: the workspace column). Keeps the
+  // N tile count at n (no extra 128-wide tile for one column); the CTA-pair
+  // kernel uses the ones column instead (its CTA 1 cannot see the stage
+  // barrier, which lives on the leader).
+  int colsum_col_p1;
   float* gb_hi;
   float* gb_lo;
   float* gb_mom;
 };
 
 __host__ __device__ __forceinline__ int epi_bias_col(const GemmEpilogue& ep) { return ep.bias_col_p1 - 1; }
+// The bias column as a TILE column of the accumulator (the ones-column
+// scheme), or -1 when the column-sum warps produce it (colsum_col_p1).
+__host__ __device__ __forceinline__ int epi_tile_bias_col(const GemmEpilogue& ep) {
+  return ep.colsum_col_p1 > 0 ? -1 : ep.bias_col_p1 - 1;
+}
 // Output columns a GEMM with this epilogue computes (N, or up to the bias column).
 __host__ __device__ __forceinline__ int epi_cols(const GemmEpilogue& ep) {
   return ep.bias_col_p1 > 0 ? ep.bias_col_p1 : ep.N;
@@ -412,7 +429,7 @@ __global__ void __launch_bounds__(256, 1)
                        const __grid_constant__ CUtensorMap tw_lo, const __grid_constant__ CUtensorMap tw_mom,
                        const ConvTmaArgs ic, const __grid_constant__ CUtensorMap t_ones) {
   using Cfg = GemmCfg<BN, TMA_UPD>;
-  constexpr int kChunkKb = chunk_kb<A_MN, B_MN>();
+  const int kChunkKb = ep.chunk_kb > 0 ? ep.chunk_kb : chunk_kb<A_MN, B_MN>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
@@ -425,6 +442,7 @@ __global__ void __launch_bounds__(256, 1)
 
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31u;
+  const bool colsum = A_MN && IC != 1 && ep.colsum_col_p1 > 0;
   // Work unit u -> output tile u % num_tiles, K-split u / num_tiles.
   auto unit = [&](int u, int& m0, int& n0, int& kb0, int& kb1, int& split) {
     const int t = u % num_tiles;
@@ -444,7 +462,7 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 1 && elect_one()) {
     for (int s = 0; s < Cfg::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], colsum ? 3 : 1);  // the MMA commit (+ the two column-sum warps)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
@@ -542,6 +560,56 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
+  } else if (warp == 2 || warp == 3) {
+    if (colsum) {
+      // Column sums of A (MN-major: 32 x 32 boxes, K rows of 128 B, SW128 with
+      // 32 B atoms: the 8-float granule g of row k sits at g ^ (k & 3)).
+      // Warp 2 sums boxes 0-1 (m0 + [0, 64)), warp 3 boxes 2-3; lane = m.
+      const int box0 = static_cast<int>(warp - 2) * 2;
+      const int col = ep.colsum_col_p1 - 1;
+      int it = 0;
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        int m0, n0, kb0, kb1, split;
+        unit(u, m0, n0, kb0, kb1, split);
+        const bool mine = n0 == 0;  // column tile 0 carries the bias
+        float sum[2] = {0.f, 0.f}, cmp[2] = {0.f, 0.f};
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % Cfg::kStages;
+          const uint32_t ph = (it / Cfg::kStages) & 1u;
+          mbar_wait(&full_bar[s], ph);
+          if (mine) {
+            const uint8_t* base = smem + s * Cfg::kStageBytes;
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+              const uint8_t* hi = base + (box0 + b) * 4096;
+              const uint8_t* lo = hi + Cfg::kABytes;
+#pragma unroll 8
+              for (int k = 0; k < kBK; ++k) {
+                const uint32_t off = k * 128 + ((((lane >> 3) ^ (k & 3)) & 3) << 5) + (lane & 7) * 4;
+                const float v = *reinterpret_cast<const float*>(hi + off) + *reinterpret_cast<const float*>(lo + off);
+                const float y = v - cmp[b], t = sum[b] + y;  // Kahan
+                cmp[b] = (t - sum[b]) - y;
+                sum[b] = t;
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_bar[s]);
+        }
+        if (mine) {
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const int row = m0 + (box0 + b) * 32 + static_cast<int>(lane);
+            if (ep.bias_col_p1 > 0) {
+              bias_store<EPI>(ep, sum[b], row);
+            } else if (EPI == kEpiStoreScaled && row < ep.M) {  // split-K partial: the workspace column
+              const long out_shift = split * ep.split_stride;
+              ep.out_hi[out_shift + static_cast<long>(row) * ep.ld_out + col] = ep.alpha * sum[b];
+            }
+          }
+        }
+      }
+    }
   } else if (warp >= 4) {
     const uint32_t q = warp & 3u;
     const uint32_t lane_addr = (q * 32u) << 16;
@@ -634,8 +702,12 @@ __global__ void __launch_bounds__(256, 1)
           }
           __syncwarp();
         }
-        const int bc = epi_bias_col(ep) - n0;  // the fused bias column in this tile (its W box was out of bounds)
-        if (bc >= 0 && bc < BN) bias_store<EPI>(ep, acc[bc], row);
+        // The fused bias column in this tile (its W box was out of bounds);
+        // static indices only, so acc stays in registers.
+        const int tbc = epi_tile_bias_col(ep);
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 32)
+          if (n0 + c0 == tbc) bias_store<EPI>(ep, acc[c0], row);
       } else if (EPI == kEpiStoreScaled && ep.route_rows > 0) {
         // Rows routed to peer memory (multi-GPU push exchange): stage each
         // 32 x 32 block in shared memory so that one warp store writes four
@@ -646,7 +718,7 @@ __global__ void __launch_bounds__(256, 1)
         const int cc = 4 * static_cast<int>(lane & 7);
 #pragma unroll
         for (int c0 = 0; c0 < BN; c0 += 32) {
-          if (n0 + c0 == epi_bias_col(ep)) {
+          if (n0 + c0 == epi_tile_bias_col(ep)) {
             bias_store<EPI>(ep, acc[c0], row);  // the bias row stays local (it travels with the push signal)
           } else if (n0 + c0 < ep.N) {
 #pragma unroll
@@ -673,7 +745,7 @@ __global__ void __launch_bounds__(256, 1)
       } else {
 #pragma unroll
         for (int c0 = 0; c0 < BN; c0 += 32) {
-          if (n0 + c0 == epi_bias_col(ep)) bias_store<EPI>(ep, acc[c0], row);
+          if (n0 + c0 == epi_tile_bias_col(ep)) bias_store<EPI>(ep, acc[c0], row);
           else if (n0 + c0 < ep.N) epilogue_chunk<EPI>(ep, acc + c0, row, n0 + c0, out_shift);
         }
       }

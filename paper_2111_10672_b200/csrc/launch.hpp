@@ -63,6 +63,10 @@ int gemm_conv_dgrad(const ConvSrc& src, long pixel0, int rows, const Operand& B,
 // Per-device constants of the GEMMs (the fused-bias ones boxes); call once
 // per device before capturing any GEMM with a fused bias column.
 void gemm_prepare_device();
+// Tuning aid: TMEM accumulation chunk (k-blocks) of GEMM kind 0 (forward),
+// 1 (dgrad) or 2 (wgrad); kb < 1 restores the default. Captured graphs keep
+// the value they were captured with.
+void gemm_set_chunk(int kind, int kb);
 // Test hook: -1 automatic choice, 0 force 1-CTA, 1 force CTA pair.
 void gemm_force_variant(int v);
 // Tuning aid: force every GEMM onto one plan (two_sm: CTA-pair kernel of

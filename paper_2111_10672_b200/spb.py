@@ -90,6 +90,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "spb_partial_backprop": (i, [vp, ip, i, i, vp, C.POINTER(C.c_longlong), ip]),
         "spb_aggregate": (i, [vp, i, i, vp, ip, ip, vp]),
         "spb_aggregate64": (i, [i, i, i, vp, ip, ip, vp]),
+        "spb_layer_shard": (i, [C.c_longlong, i, C.POINTER(C.c_longlong)]),
+        "spb_set_gemm_chunk": (i, [i, i]),
         "spb_loss64": (i, [vp, vp, ip, i, C.POINTER(C.c_double)]),
         "spb_train_steps": (i, [vp, u64, i, i, i, fp]),
         "spb_step_host": (i, [vp, fp, fp, i, fp]),
@@ -127,7 +129,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 EXPORTED = [
     "spb_last_error", "spb_suffix_layers", "spb_chunk_coverage", "spb_chunk_layout", "spb_layer_chunks",
     "spb_draw_batch", "spb_rank_workers", "spb_create", "spb_destroy", "spb_set_dataset", "spb_set_params",
-    "spb_get_params", "spb_set_optimizer", "spb_partial_backprop", "spb_aggregate", "spb_aggregate64", "spb_loss64", "spb_train_steps",
+    "spb_get_params", "spb_set_optimizer", "spb_partial_backprop", "spb_aggregate", "spb_aggregate64", "spb_loss64", "spb_layer_shard", "spb_set_gemm_chunk", "spb_train_steps",
     "spb_step_host", "spb_loss", "spb_synchronize", "spb_stream", "spb_comm_unique_id", "spb_comm_init",
     "spb_last_batch", "spb_launches_per_step", "spb_make_random_chain_mlp",
     "spb_get_grads", "spb_profile_step", "spb_time_train_steps", "spb_bucket_plan", "spb_set_fused_update",
@@ -208,6 +210,13 @@ def bucket_plan(k: int, L: int, nranks: int, full_backprop: bool = False):
     mask = np.zeros(L, dtype=np.int32)
     _check(load_library().spb_bucket_plan(k, L, nranks, int(full_backprop), _ip(kind), _ip(root), _ip(mask)))
     return [(int(kind[l]), int(root[l]), [r for r in range(nranks) if (int(mask[l]) >> r) & 1]) for l in range(L)]
+
+
+def layer_shard(count: int, parts: int) -> int:
+    """The sub exchange mode's shard length (spb_layer_shard)."""
+    out = C.c_longlong()
+    _check(load_library().spb_layer_shard(count, parts, C.byref(out)))
+    return out.value
 
 
 def comm_unique_id() -> bytes:
@@ -478,10 +487,10 @@ class ChainMlp:
 
     @property
     def comm_mode(self):
-        """Multi-GPU aggregation mode: "rh", "push", "p2p", "rs", "nvls", "nccl" (None before comm_init)."""
+        """Multi-GPU aggregation mode: "rh", "push", "p2p", "sub", "nvls", "nccl" (None before comm_init)."""
         v = C.c_int()
         _check(load_library().spb_comm_mode(self._ctx, C.byref(v)), self._ctx)
-        return {0: "nccl", 1: "nvls", 2: "p2p", 3: "rs", 4: "push", 5: "rh"}.get(v.value)
+        return {0: "nccl", 1: "nvls", 2: "p2p", 3: "sub", 4: "push", 5: "rh"}.get(v.value)
 
     def comm_selftest(self) -> int:
         """Collective NVLS diagnostic; returns the mismatching element count."""

@@ -105,3 +105,88 @@ def test_bucket_plan_shapes():
         assert all(r == list(range(world)) for _, _, r in full)
     plan8 = spb.bucket_plan(8, L, 8)
     assert [len(r) for _, _, r in plan8] == [1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7, 8, 8]
+
+
+def _sub_worker(rank, world, port, out_dir, k):
+    """The sub exchange mode (engine.cu enqueue_sub_layer): per layer, the
+    contributing ranks reduce (a reduce-scatter, here all-reduce + own shard)
+    over their own group only, each updates its shard (spb_layer_shard), and
+    every member broadcasts its updated shard to all ranks."""
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from oracle.oracle import Oracle
+    from paper_2111_10672_b200 import spb
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Oracle()
+    L = len(WIDTHS) - 1
+    X, Y, W = orc.gen_chain_mlp(WIDTHS, N, DSEED)
+    chunks = spb.layer_chunks(k, L)
+    local = [np.zeros_like(b) for b in W]
+    for j in spb.rank_workers(k, L, rank, world):
+        g, cov = orc.partial_backprop(WIDTHS, X, Y, W, orc.draw_batch(SEED, 1, j, BW, N), spb.suffix_layers(j, k, L))
+        for l in range(cov, L + 1):
+            local[l - 1] += g[l - 1] / chunks[l - 1]
+    plan = spb.bucket_plan(k, L, world)
+    sets = sorted({tuple(r) for _, _, r in plan if len(r) > 1})
+    groups = {s: dist.new_group(list(s)) for s in sets}  # collectively, same order everywhere
+    P = [b.copy() for b in W]
+    moved = 0.0
+    for l in range(L, 0, -1):
+        _, _, ranks = plan[l - 1]
+        cnt = local[l - 1].size
+        sh = spb.layer_shard(cnt, len(ranks))
+        bounds = [(min(cnt, i * sh), min(cnt, (i + 1) * sh)) for i in range(len(ranks))]
+        if rank in ranks:
+            t = torch.from_numpy(local[l - 1].copy())
+            if len(ranks) > 1:
+                dist.all_reduce(t, group=groups[tuple(ranks)])
+                moved += t.numel()
+            a, b = bounds[ranks.index(rank)]
+            P[l - 1][a:b] = W[l - 1][a:b] - LR * t.numpy()[a:b]
+        for i, r in enumerate(ranks):
+            a, b = bounds[i]
+            if b > a:
+                t = torch.from_numpy(np.ascontiguousarray(P[l - 1][a:b]))
+                dist.broadcast(t, src=r)
+                P[l - 1][a:b] = t.numpy()
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), *P, np.array([moved]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k", [(2, 8), (4, 8), (8, 8), (2, 2), (4, 4)])
+def test_sub_protocol_matches_single_process_step(tmp_path, world, k, orc):
+    """Contributor sub-communicators (the engine's default at 8 ranks): the
+    weights after one step equal the single-process SPB step, on every rank;
+    with one worker per rank (k = world) ranks outside a layer's contributor
+    set move no gradient bytes for it."""
+    mp.start_processes(_sub_worker, args=(world, _free_port(), str(tmp_path), k), nprocs=world, start_method="spawn")
+    L = len(WIDTHS) - 1
+    X, Y, W = orc.gen_chain_mlp(WIDTHS, N, DSEED)
+    P = [b.copy() for b in W]
+    orc.spb_step(WIDTHS, X, Y, P, k, k * BW, LR, SEED, 1)
+    outs = [np.load(os.path.join(tmp_path, f"rank{r}.npz")) for r in range(world)]
+    for r in range(world):
+        for l in range(L):
+            got = outs[r][f"arr_{l}"]
+            np.testing.assert_allclose(got, P[l], rtol=1e-12, atol=1e-15)
+            assert np.array_equal(got, outs[0][f"arr_{l}"])  # rank-identical weights
+    if k == world:  # rank 0 (worker 1) contributes to the top layers only
+        from paper_2111_10672_b200 import spb
+
+        top = spb.suffix_layers(1, k, L)
+        dims = spb.block_dims(WIDTHS)
+        assert float(outs[0][f"arr_{L}"][0]) <= sum(dims[L - top:])
+
+
+def test_layer_shard_partition():
+    from paper_2111_10672_b200 import spb
+
+    for cnt in (1, 3, 4, 5, 97, 4096, 16781344):
+        for parts in range(1, 9):
+            sh = spb.layer_shard(cnt, parts)
+            assert sh % 4 == 0 and parts * sh >= cnt and (parts - 1) * sh < cnt + 4 * parts

@@ -3,8 +3,9 @@
 Each rank runs its balanced worker set on its own B200. Aggregation paths:
 p2p (copy-engine pulls of gradient shards, sharded update, pulls of the
 updated weights), rh (the same on a recursive-halving / -doubling schedule),
-push (gradient rows stored to their owners by the wgrad epilogue), rs (NCCL
-reduce-scatter / all-gather), NVLS (gradients reduced in the NVSwitch, each
+push (gradient rows stored to their owners by the wgrad epilogue), sub (NCCL
+reduce-scatter among each layer's contributing ranks only over contributor
+sub-communicators, sharded update, weight broadcast to every rank), NVLS (gradients reduced in the NVSwitch, each
 rank updates its shard and multicasts the new weights) and NCCL per-layer
 buckets (broadcast from a sole contributor, else all-reduce, then the same
 update on every rank).
@@ -83,7 +84,7 @@ def _rank(rank, world, port, out_dir, full, mode="p2p", mu=0.0, wd=0.0, chain=No
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["rh", "push", "p2p", "rs", "nvls", "nccl"])
+@pytest.mark.parametrize("mode", ["rh", "push", "p2p", "sub", "nvls", "nccl"])
 @pytest.mark.parametrize("full", [False, True])
 def test_multi_gpu_step_matches_oracle(tmp_path, orc, full, mode):
     world = min(_gpus(), 4)
@@ -124,7 +125,7 @@ def test_multi_gpu_momentum_sharded_matches_nccl(tmp_path):
         pytest.skip("needs >= 2 GPUs")
 
     res = {}
-    for mode in ("rh", "push", "p2p", "rs", "nvls", "nccl"):
+    for mode in ("rh", "push", "p2p", "sub", "nvls", "nccl"):
         d = tmp_path / mode
         d.mkdir()
         _launch(_rank_momentum, world, str(d), mode)
@@ -133,7 +134,7 @@ def test_multi_gpu_momentum_sharded_matches_nccl(tmp_path):
     for l in range(L):  # push and p2p sum the same contributions in the same order
         for r in range(world):
             assert np.array_equal(res["push"][r][f"arr_{l + 1}"], res["p2p"][r][f"arr_{l + 1}"])
-    for mode in ("rh", "push", "p2p", "rs", "nvls"):
+    for mode in ("rh", "push", "p2p", "sub", "nvls"):
         for l in range(L):
             a, b = res[mode][0][f"arr_{l + 1}"], res["nccl"][0][f"arr_{l + 1}"]
             assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-5
@@ -232,7 +233,7 @@ def _rank_conv(rank, world, port, out_dir, mode):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["rh", "p2p", "rs", "nvls", "nccl"])
+@pytest.mark.parametrize("mode", ["rh", "p2p", "sub", "nvls", "nccl"])
 def test_multi_gpu_convnet_matches_oracle(tmp_path, orc, mode):
     """The ConvNet (cfg4 shape family) on 2-4 GPUs: 3 SPB steps equal the
     single-process fp64 conv oracle (1e-4) and are bit-identical across ranks."""
@@ -255,3 +256,58 @@ def test_multi_gpu_convnet_matches_oracle(tmp_path, orc, mode):
         assert np.linalg.norm(got - B[l]) / np.linalg.norm(B[l]) <= 1e-4
         for r in range(world):
             assert np.array_equal(outs[r][f"arr_{l}"], got)
+
+
+def _rank_one_worker(rank, world, port, out_dir, mode):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+
+    from paper_2111_10672_b200 import spb
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["SPB_COMM"] = mode
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    X, Y, W = spb.gen_chain_mlp(WIDTHS, N, DSEED)
+    m = spb.ChainMlp(WIDTHS, X, Y, W, k=world, per_worker_batch=BW, device=rank)
+    m.comm_init_torch(dist, rank, world)
+    assert m.comm_mode == mode
+    m.set_optimizer(LR, 0.9, 1e-3)
+    m.train_steps(SEED, 1, 3)
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), *m.get_params())
+    dist.barrier()
+    m.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["sub", "p2p"])
+def test_multi_gpu_one_worker_per_gpu(tmp_path, orc, mode):
+    """north_star's layout at small scale: k = world workers, ONE per GPU, so a
+    layer's contributing ranks are a strict suffix of the ranks and the sub
+    mode reduces each layer over its own contributor sub-communicator. Weights
+    after 3 momentum + wd steps match the CPU oracle's restatement (1e-4) and
+    are rank-identical."""
+    world = min(_gpus(), 4)
+    if world < 2:
+        pytest.skip("needs >= 2 GPUs")
+    from oracle import batched
+    from paper_2111_10672_b200 import spb
+
+    _launch(_rank_one_worker, world, str(tmp_path), mode)
+    Xf, Yf, Wf = spb.gen_chain_mlp(WIDTHS, N, DSEED)
+    X, Y = Xf.astype(np.float64), Yf.astype(np.float64)
+    P = [b.astype(np.float64) for b in Wf]
+    bufs = [np.zeros_like(p) for p in P]
+    for s in range(1, 4):
+        rows = np.concatenate([orc.draw_batch(SEED, s, j, BW, N) for j in range(1, world + 1)])
+        g = batched.aggregate_step(WIDTHS, X[rows], Y[rows], P, world, BW)
+        batched.sgd_update(P, g, LR, 0.9, 1e-3, bufs)
+    outs = [np.load(os.path.join(tmp_path, f"r{r}.npz")) for r in range(world)]
+    for l in range(len(WIDTHS) - 1):
+        for r in range(world):
+            got = outs[r][f"arr_{l}"]
+            assert np.linalg.norm(got - P[l]) / np.linalg.norm(P[l]) <= 1e-4
+            assert np.array_equal(got, outs[0][f"arr_{l}"])
