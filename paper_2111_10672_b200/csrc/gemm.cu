@@ -483,8 +483,12 @@ int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue&
     if (!B.mn_major || oc % 32 || oc < (B.mn_map > 0 ? B.mn_map : B.mn) || B.mn != oc + 1)
       throw std::invalid_argument("gemm: bad fused-bias column");
   }
+  // Routed epilogues (the push exchange) stage rows through shared memory in
+  // the 1-CTA kernel only: the pair kernel would store 16-byte pieces row by
+  // row over NVLink.
   const Plan plan = plan_gemm(A.mn, B.mn, A.k, ep.splitk_ws && !no_split ? ep.splitk_ws_floats : 0, can_split,
-                              narrow_pair_ok(A, B, epi), true, A.mn_major && B.mn_major, ep.ones_col_p1 > 0);
+                              narrow_pair_ok(A, B, epi), ep.route_rows == 0, A.mn_major && B.mn_major,
+                              ep.ones_col_p1 > 0);
   g_last_plan = plan;
   if (ep.ones_col_p1 > 0 && (!plan.two_sm || (epi == kEpiWgradUpdate && g_force_variant != 1))) {
     // 1-CTA kernel: the column-sum warps produce the bias (no extra column tile).

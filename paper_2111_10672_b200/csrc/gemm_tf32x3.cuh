@@ -564,15 +564,22 @@ __global__ void __launch_bounds__(256, 1)
     if (colsum) {
       // Column sums of A (MN-major: 32 x 32 boxes, K rows of 128 B, SW128 with
       // 32 B atoms: the 8-float granule g of row k sits at g ^ (k & 3)).
-      // Warp 2 sums boxes 0-1 (m0 + [0, 64)), warp 3 boxes 2-3; lane = m.
+      // Warp 2 sums boxes 0-1 (m0 + [0, 64)), warp 3 boxes 2-3. Lane l reads
+      // the float4 p = l & 7 (m = 4p .. 4p + 3 of the box) of the rows
+      // k = 4 kk + (l >> 3): 16-byte loads, one fp32 partial per k-block,
+      // Kahan-compensated across k-blocks, the four row-phase lanes combined
+      // at the end. The unit of split s whose column tile is s mod (column
+      // tiles) carries the bias, so the work spreads over all column tiles.
       const int box0 = static_cast<int>(warp - 2) * 2;
       const int col = ep.colsum_col_p1 - 1;
+      const int num_n_tiles = num_tiles / num_m_tiles;
+      const int p = static_cast<int>(lane & 7u), r4 = static_cast<int>(lane >> 3);
       int it = 0;
       for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
         int m0, n0, kb0, kb1, split;
         unit(u, m0, n0, kb0, kb1, split);
-        const bool mine = n0 == 0;  // column tile 0 carries the bias
-        float sum[2] = {0.f, 0.f}, cmp[2] = {0.f, 0.f};
+        const bool mine = n0 / BN == split % num_n_tiles;
+        float sum[2][4] = {}, cmp[2][4] = {};
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % Cfg::kStages;
           const uint32_t ph = (it / Cfg::kStages) & 1u;
@@ -583,13 +590,21 @@ __global__ void __launch_bounds__(256, 1)
             for (int b = 0; b < 2; ++b) {
               const uint8_t* hi = base + (box0 + b) * 4096;
               const uint8_t* lo = hi + Cfg::kABytes;
-#pragma unroll 8
-              for (int k = 0; k < kBK; ++k) {
-                const uint32_t off = k * 128 + ((((lane >> 3) ^ (k & 3)) & 3) << 5) + (lane & 7) * 4;
-                const float v = *reinterpret_cast<const float*>(hi + off) + *reinterpret_cast<const float*>(lo + off);
-                const float y = v - cmp[b], t = sum[b] + y;  // Kahan
-                cmp[b] = (t - sum[b]) - y;
-                sum[b] = t;
+              float4 part = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int kk = 0; kk < kBK / 4; ++kk) {
+                const int k = kk * 4 + r4;
+                const uint32_t off = k * 128 + ((((p >> 1) ^ (k & 3)) & 3) << 5) + (p & 1) * 16;
+                const float4 vh = *reinterpret_cast<const float4*>(hi + off);
+                const float4 vl = *reinterpret_cast<const float4*>(lo + off);
+                part.x += vh.x + vl.x, part.y += vh.y + vl.y, part.z += vh.z + vl.z, part.w += vh.w + vl.w;
+              }
+              const float pv[4] = {part.x, part.y, part.z, part.w};
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {  // Kahan
+                const float y = pv[i] - cmp[b][i], t = sum[b][i] + y;
+                cmp[b][i] = (t - sum[b][i]) - y;
+                sum[b][i] = t;
               }
             }
           }
@@ -598,15 +613,20 @@ __global__ void __launch_bounds__(256, 1)
         }
         if (mine) {
 #pragma unroll
-          for (int b = 0; b < 2; ++b) {
-            const int row = m0 + (box0 + b) * 32 + static_cast<int>(lane);
-            if (ep.bias_col_p1 > 0) {
-              bias_store<EPI>(ep, sum[b], row);
-            } else if (EPI == kEpiStoreScaled && row < ep.M) {  // split-K partial: the workspace column
-              const long out_shift = split * ep.split_stride;
-              ep.out_hi[out_shift + static_cast<long>(row) * ep.ld_out + col] = ep.alpha * sum[b];
+          for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float v = sum[b][i] - cmp[b][i];
+              v += __shfl_xor_sync(0xffffffffu, v, 8);
+              v += __shfl_xor_sync(0xffffffffu, v, 16);
+              const int row = m0 + (box0 + b) * 32 + 4 * p + i;
+              if (r4 != 0) continue;
+              if (ep.bias_col_p1 > 0) {
+                bias_store<EPI>(ep, v, row);
+              } else if (EPI == kEpiStoreScaled && row < ep.M) {  // split-K partial: the workspace column
+                ep.out_hi[split * ep.split_stride + static_cast<long>(row) * ep.ld_out + col] = ep.alpha * v;
+              }
             }
-          }
         }
       }
     }

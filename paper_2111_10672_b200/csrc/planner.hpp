@@ -3,6 +3,7 @@
 // the multi-GPU worker placement. Everything here is pure integer work.
 #pragma once
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <numeric>
 #include <stdexcept>
@@ -91,12 +92,29 @@ inline int worker_stop(int j, int k, int L) { return L - suffix_layers(j, k, L) 
 // backward costs ~ s_j layers, so pairs (j, k+1-j) carry equal work; pairs are
 // dealt out snake-wise. Falls back to a count-balanced greedy (largest
 // suffix first to the least-loaded rank) when the pairing does not divide.
+// SPB_PLACEMENT=contiguous instead deals out consecutive workers (rank r gets
+// workers r*k/N+1 .. (r+1)*k/N): backward work is then unbalanced, but the
+// ranks hosting only low workers contribute to few layers, so the exchange
+// moves fewer gradient bytes (the saving SPB promises on the network).
+inline bool contiguous_placement() {
+  static const bool c = [] {
+    const char* p = std::getenv("SPB_PLACEMENT");
+    return p && std::string(p) == "contiguous";
+  }();
+  return c;
+}
+
 inline std::vector<int> rank_workers(int k, int L, int rank, int nranks) {
   if (k < 1 || nranks < 1 || rank < 0 || rank >= nranks) throw ArgumentError("rank_workers: bad arguments");
   if (nranks > k) throw ArgumentError("rank_workers: more ranks than workers");
   std::vector<std::vector<int>> owned(nranks);
   if (nranks == k) {
     for (int r = 0; r < nranks; ++r) owned[r] = {r + 1};
+  } else if (contiguous_placement()) {
+    for (int r = 0; r < nranks; ++r)
+      for (int j = static_cast<int>(static_cast<long long>(r) * k / nranks) + 1;
+           j <= static_cast<int>(static_cast<long long>(r + 1) * k / nranks); ++j)
+        owned[r].push_back(j);
   } else if (k % (2 * nranks) == 0) {
     const int pairs = k / 2;
     for (int p = 0; p < pairs; ++p) {
