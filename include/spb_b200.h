@@ -219,11 +219,12 @@ SPB_API void* spb_stream(spb_ctx* ctx);
  *    NVLink with the copy engines (CUDA IPC), applies the optimizer and the
  *    other ranks pull the updated fp32 shard back, synchronised by
  *    epoch-stamped device flags (no NCCL in the step);
- *  - "nvls": parameters and gradients in NVSwitch multicast memory; each rank
- *    reduces its shard in the switch, updates it and multicasts the weights;
- *  - "rs": NCCL reduce-scatter of each layer's gradient, the optimizer on
- *    this rank's shard, NCCL all-gather of the fp32 weights (a layer with one
- *    contributing rank: that rank updates it and broadcasts the weights);
+ *  - "sub" (default for other rank counts, e.g. 8 = one SPB worker per GPU):
+ *    NCCL over contributor sub-communicators (ncclCommSplit, one per distinct
+ *    contributor-rank set): a layer's gradient is reduce-scattered among the
+ *    ranks hosting one of its contributing workers ONLY, each of them updates
+ *    its shard, and every member broadcasts its updated fp32 shard to all
+ *    ranks (a sole contributor updates the whole layer);
  *  - "rh" (power-of-two rank counts; default for the ConvNet at 4 ranks): the p2p protocol's buffers with
  *    Rabenseifner's schedule -- recursive-halving reduce-scatter, the owner's
  *    update, recursive-doubling all-gather of the fp32 weights -- so every
@@ -234,12 +235,11 @@ SPB_API void* spb_stream(spb_ctx* ctx);
  *    stores through CUDA IPC, staged through shared memory into 128-byte row
  *    segments); the owner sums its rows and applies the optimizer; the peers
  *    pull the new fp32 rows (copy engines) and split them into (hi, lo);
- *  - "nccl" (default for other rank counts): per-layer NCCL buckets
- *    (broadcast / all-reduce), then the local optimizer update on every rank.
- * Ranks of one node only. */
+ * Ranks of one node only. SPB_PLACEMENT=contiguous deals consecutive workers
+ * to ranks instead of balanced pairs (spb_rank_workers): less exchange, less
+ * balanced backward work. */
 SPB_API spb_status spb_comm_unique_id(void* out128);
 SPB_API spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int nranks);
-/* Active aggregation mode: 0 nccl, 1 nvls, 2 p2p, 3 rs, 4 push, 5 rh (-1 before spb_comm_init). */
 /* Tuning aid (process-wide): k-blocks of K (32 each) the tensor cores
  * accumulate per TMEM chunk before the epilogue folds the chunk into fp32
  * registers, for GEMM kind 0 (forward), 1 (dgrad), 2 (wgrad); kblocks < 1
@@ -251,18 +251,12 @@ SPB_API spb_status spb_set_gemm_chunk(int kind, int kblocks);
  * member i of a layer's contributor set owns [i * shard, min(count, (i + 1) *
  * shard)); shard is a multiple of 4 floats and parts * shard >= count. */
 SPB_API spb_status spb_layer_shard(long long count, int parts, long long* shard);
+/* Active aggregation mode: 2 p2p, 3 sub, 4 push, 5 rh (-1 before spb_comm_init, 0 one rank). */
 SPB_API spb_status spb_comm_mode(spb_ctx* ctx, int* mode);
-/* Collective diagnostic of the NVLS path: multicast reduce + broadcast of a
- * known pattern over all ranks; *mismatches = wrong elements seen here. */
-SPB_API spb_status spb_comm_selftest(spb_ctx* ctx, long long* mismatches);
-/* Collective tuning aid of the NVLS path: times the switch reduce, the
- * multicast store and the fused reduce/update/store kernel over launch
- * shapes on an n_floats layer; rank 0 prints one line per variant. */
-SPB_API spb_status spb_comm_bench(spb_ctx* ctx, long long n_floats, int reps);
-/* The per-layer bucket protocol spb_comm_init sets up (host-only, no GPU):
- * for layer l (index l-1): kind 0 = all-reduce over all ranks (ranks without
- * contributor rows add zeros), 1 = broadcast from root (a single contributing
- * rank); rank_mask = bit r set when rank r hosts a contributor of layer l. */
+/* The per-layer contributor plan spb_comm_init sets up (host-only, no GPU):
+ * for layer l (index l-1) rank_mask has bit r set when rank r hosts a
+ * worker that backpropagates into l (the layer's contributing ranks); kind
+ * is 1 (root = that rank) when exactly one rank contributes, else 0. */
 SPB_API spb_status spb_bucket_plan(int k, int L, int nranks, int full_backprop, int* kind, int* root,
                                    int* rank_mask);
 

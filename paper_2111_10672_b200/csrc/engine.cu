@@ -36,7 +36,6 @@
 #include "gemm_tf32x3.cuh"
 #include "conv.hpp"
 #include "launch.hpp"
-#include "nvls.hpp"
 #include "p2p.hpp"
 #include "planner.hpp"
 
@@ -219,7 +218,7 @@ struct Engine {
   int fused_mode = 2;
   static constexpr int kFuseMaxRows = 512;  // 640 / 768 measured the same; 384 slower
   std::vector<char> fuse_layer;  // per layer, set by enqueue_step for enqueue_pass / on_layer
-  // Multi-GPU aggregation mode: 0 = NCCL buckets, 1 = NVLS multicast,
+  // Multi-GPU aggregation mode (0 = none selected yet):
   // 2 = peer-to-peer copy-engine pulls (p2p.cu), 3 = NCCL contributor
   // sub-communicators ("sub": reduce-scatter among the layer's contributing
   // ranks only, sharded update, weight broadcast to every rank).
@@ -268,16 +267,8 @@ struct Engine {
   }
   cudaStream_t s4 = nullptr;
   std::vector<cudaStream_t> gpull, wpull;  // per-peer copy streams (copy engines run concurrently)
-  // NVLS path (multi-GPU, NVSwitch multicast): p_hi / p_lo / grad live in
-  // multicast buffers; each layer's gradient is reduced in the switch and
-  // the optimizer runs once per element, on the rank owning its shard, which
-  // stores the new weights into every rank's copy (nvls.cu).
-  bool nvls = false;
-  McBuffer mc_hi, mc_lo, mc_grad, mc_flags;
-  int* epoch_dev = nullptr;  // completed NVLS steps (barrier targets)
+  int* epoch_dev = nullptr;  // completed steps of the flag-synchronised exchange modes
   float* bar_dev = nullptr;  // host-barrier scratch
-  std::string nvls_tag;      // socket-name prefix, identical on all ranks
-  int nvls_tests = 0;
   bool concurrent = true;          // side streams (off in spb_profile_step: clean per-kernel times)
 
   // Eager-mode instrumentation (spb_profile_step): CUDA events around every
@@ -376,11 +367,6 @@ struct Engine {
         if (q) cudaStreamDestroy(q);
       gpull.clear(), wpull.clear();
       comm_mode = 0;
-    }
-    if (nvls) {
-      nvls_free(mc_hi), nvls_free(mc_lo), nvls_free(mc_grad), nvls_free(mc_flags);
-      p_hi = p_lo = grad = nullptr;  // not cudaMalloc'd
-      nvls = false;
     }
     for (auto& kv : subcomms)
       if (kv.second) {
@@ -1019,59 +1005,6 @@ struct Engine {
     return evs[i];
   }
 
-  // Layer l's bucket collective on the comm stream, after the main stream has
-  // produced the layer's local gradient (grad[w_off[l] .. b_off[l] + n_l)).
-  int enqueue_bucket(int l, bool full, cudaStream_t s) {  // s: the stream that produced layer l's gradient
-    const Bucket* bk = nullptr;
-    for (auto& b : buckets[full])
-      if (b.l_lo <= l && l <= b.l_hi) bk = &b;
-    if (!bk) throw ConfigError("comm: no bucket for layer");
-    SPB_CUDA(cudaEventRecord(ev(kEvBucket + l), s));
-    SPB_CUDA(cudaStreamWaitEvent(cst, ev(kEvBucket + l), 0));
-    float* base = grad + w_off[l];
-    const size_t count = static_cast<size_t>(b_off[l] + w[l] - w_off[l]);
-    const bool mine = std::find(bk->ranks.begin(), bk->ranks.end(), rank) != bk->ranks.end();
-    pbeg(cst);
-    if (bk->kind == 1) {
-      nccl_check(nccl().Broadcast(base, base, count, ncclFloat32, bk->root, comm, cst));
-    } else {
-      if (!mine) SPB_CUDA(cudaMemsetAsync(base, 0, count * sizeof(float), cst));
-      nccl_check(nccl().AllReduce(base, base, count, ncclFloat32, ncclSum, comm, cst));
-    }
-    pend(kClsComm, static_cast<double>(count) * 4.0, cst);
-    return 0;
-  }
-
-  // NVLS: layer l's aggregate + optimizer + weight broadcast. On cst, after
-  // this rank's gradient of layer l is final (gs) and its dgrad_l, the last
-  // reader of W_l, is done (s): zero the gradient if this rank has no
-  // contributor rows, cross-rank barrier (every rank's gradient final and no
-  // rank still reading W_l), then the fused kernel over this rank's shard.
-  int enqueue_nvls_layer(int l, bool full, cudaStream_t gs, cudaStream_t s) {
-    const Bucket* bk = nullptr;
-    for (auto& b : buckets[full])
-      if (b.l_lo <= l && l <= b.l_hi) bk = &b;
-    if (!bk) throw ConfigError("comm: no bucket for layer");
-    SPB_CUDA(cudaEventRecord(ev(kEvBucket + l), gs));
-    SPB_CUDA(cudaStreamWaitEvent(cst, ev(kEvBucket + l), 0));
-    SPB_CUDA(cudaEventRecord(ev(kEvUpd + 2 * l), s));
-    SPB_CUDA(cudaStreamWaitEvent(cst, ev(kEvUpd + 2 * l), 0));
-    const long off = w_off[l], cnt = b_off[l] + round_up(w[l], 32) - w_off[l];
-    const bool mine = std::find(bk->ranks.begin(), bk->ranks.end(), rank) != bk->ranks.end();
-    int n = 2;
-    if (!mine) SPB_CUDA(cudaMemsetAsync(grad + off, 0, cnt * sizeof(float), cst));
-    int* fl_mc = reinterpret_cast<int*>(mc_flags.mcva);
-    const int* fl_uc = reinterpret_cast<const int*>(mc_flags.uc);
-    launch_nvls_barrier(fl_mc, fl_uc, l, nranks, epoch_dev, cst);
-    const long n4 = cnt / 4, a = n4 * rank / nranks * 4, b = n4 * (rank + 1) / nranks * 4;
-    auto mcp = [&](const McBuffer& m) { return reinterpret_cast<float*>(m.mcva) + off + a; };
-    pbeg(cst);
-    launch_fused_reduce_update(mcp(mc_grad), p_hi + off + a, p_lo + off + a, mcp(mc_hi), mcp(mc_lo),
-                               mom ? mom + off + a : nullptr, b - a, lr, mu, wd, cst);
-    pend(kClsComm, static_cast<double>(b - a) * 4.0 * (mom ? 7 : 5), cst);
-    return n;
-  }
-
   // p2p mode, layer l (see p2p.cu for the protocol). gs: the stream that
   // produced this rank's gradient of l; s: the main stream (dgrad_l, the last
   // local reader of W_l, was issued on it before this call).
@@ -1637,41 +1570,6 @@ struct Engine {
     SPB_CUDA(cudaStreamSynchronize(cst));
   }
 
-  // Collective over the ranks (spb_comm_init): move p_hi / p_lo / grad into
-  // multicast buffers. Returns false (nothing changed) unless every rank's
-  // GPU supports multicast.
-  bool setup_nvls(const std::string& tag) {
-    bar_dev = alloc<float>(1);
-    float ok = nvls_supported(dev) ? 1.f : 0.f;
-    SPB_CUDA(cudaMemcpy(bar_dev, &ok, 4, cudaMemcpyHostToDevice));
-    nccl_check(nccl().AllReduce(bar_dev, bar_dev, 1, ncclFloat32, ncclSum, comm, cst));
-    SPB_CUDA(cudaStreamSynchronize(cst));
-    SPB_CUDA(cudaMemcpy(&ok, bar_dev, 4, cudaMemcpyDeviceToHost));
-    if (ok != static_cast<float>(nranks)) return false;
-    nvls_tag = tag;
-    auto barrier = [&] { host_barrier(); };
-    const size_t bytes = static_cast<size_t>(nflat) * 4;
-    mc_hi = nvls_alloc(bytes, dev, rank, nranks, tag + "-hi", barrier);
-    mc_lo = nvls_alloc(bytes, dev, rank, nranks, tag + "-lo", barrier);
-    mc_grad = nvls_alloc(bytes, dev, rank, nranks, tag + "-g", barrier);
-    mc_flags = nvls_alloc(static_cast<size_t>(L + 1) * 4, dev, rank, nranks, tag + "-f", barrier);
-    SPB_CUDA(cudaDeviceSynchronize());
-    auto move = [&](float*& p, const McBuffer& m) {
-      float* np = reinterpret_cast<float*>(m.uc);
-      SPB_CUDA(cudaMemcpy(np, p, bytes, cudaMemcpyDeviceToDevice));
-      SPB_CUDA(cudaFree(p));
-      p = np;
-    };
-    move(p_hi, mc_hi);
-    move(p_lo, mc_lo);
-    move(grad, mc_grad);
-    epoch_dev = alloc<int>(1);
-    nvls = true;
-    invalidate_graphs();
-    host_barrier();
-    return true;
-  }
-
   // HBM bytes one update launch must move: read hi, lo, grad (+ mom), write
   // hi, lo (+ mom), 4 B each.
   double update_bytes() const { return static_cast<double>(nflat) * 4.0 * (mom ? 7 : 5); }
@@ -1730,7 +1628,12 @@ struct Engine {
     // the layer's gradient is final (wgrad on s2, or its NCCL bucket on cst)
     // and its last reader dgrad_l (on s) is done, so the HBM-bound update
     // runs beside the remaining backward GEMMs instead of after them.
-    const bool fused_ok = fused_mode != 0 && !conv_model && !comm;  // the conv pass has no fused epilogue
+    // Cross-rank exchange: the layer hooks of the active mode (a context that
+    // joined a 1-rank clique aggregates locally).
+    const bool xch = comm && nranks > 1;
+    if (xch && comm_mode != 2 && comm_mode != 3 && comm_mode != 4 && comm_mode != 5)
+      throw ConfigError("comm: no exchange mode selected");
+    const bool fused_ok = fused_mode != 0 && !conv_model && !xch;  // the conv pass has no fused epilogue
     fuse_layer.assign(L + 1, 0);
     bool any_unfused = !fused_ok;
     for (int l = 1; l <= L; ++l) {
@@ -1739,7 +1642,7 @@ struct Engine {
       fuse_layer[l] = fused_ok && l < L && row0[l] < rows && (fused_mode == 1 || rows - row0[l] <= kFuseMaxRows);
       if (!fuse_layer[l]) any_unfused = true;
     }
-    const bool per_layer = comm || any_unfused;
+    const bool per_layer = any_unfused;
     cudaStream_t us = concurrent ? s3 : s;
     auto fork = [&](cudaStream_t to, int e) {
       SPB_CUDA(cudaEventRecord(ev(e), s));
@@ -1749,7 +1652,7 @@ struct Engine {
       SPB_CUDA(cudaEventRecord(ev(e), from));
       SPB_CUDA(cudaStreamWaitEvent(s, ev(e), 0));
     };
-    if (comm && comm_mode == 3) {
+    if (xch && comm_mode == 3) {
       fork(cst, kEvStepFork);
       fork(s3, kEvUpdFork);
       n += enqueue_pass(rows, row0, alpha, s,
@@ -1760,7 +1663,7 @@ struct Engine {
       fwd_wait.assign(L + 1, -1);
       return n;
     }
-    if (comm && (comm_mode == 2 || comm_mode == 5)) {
+    if (xch && (comm_mode == 2 || comm_mode == 5)) {
       // Per layer (top down): G signal on the gradient stream, gradient and
       // weight pulls on per-peer copy streams, shard update on s3, split on
       // s4; all joined back into s, then the epoch advances. (5 = rh: the
@@ -1779,7 +1682,7 @@ struct Engine {
       launch_p2p_epoch(epoch_dev, nsub, s);
       return n + 1;
     }
-    if (comm && comm_mode == 4) {
+    if (xch && comm_mode == 4) {
       // Per layer (top down): gradient rows stored to their owners by the
       // wgrad epilogue, G signal on the gradient stream, owner update on s3,
       // weight pulls on per-peer copy streams, split on s4.
@@ -1802,29 +1705,11 @@ struct Engine {
       launch_p2p_epoch(epoch_dev, nsub, s);
       return n + 1;
     }
-    if (comm && nvls) {
-      // Per layer (top down) on cst: barrier + fused reduce/update/broadcast;
-      // then one closing barrier (every rank's weight stores have landed
-      // before anyone's next forward) and the epoch bump.
-      fork(cst, kEvStepFork);
-      n += enqueue_pass(rows, row0, alpha, s,
-                        [&](int l, cudaStream_t from) { return enqueue_nvls_layer(l, full, from, s); }, false,
-                        &ctl->step, nullptr);
-      launch_nvls_barrier(reinterpret_cast<int*>(mc_flags.mcva), reinterpret_cast<const int*>(mc_flags.uc), 0, nranks,
-                          epoch_dev, cst);
-      launch_nvls_epoch(epoch_dev, cst);
-      n += 2;
-      join(cst, kEvStepJoin);  // not pipelined across steps: joined every step
-      fwd_wait.assign(L + 1, -1);
-      return n;
-    }
-    if (comm) fork(cst, kEvStepFork);
     if (per_layer && concurrent) fork(s3, kEvUpdFork);
     auto on_layer = [&](int l, cudaStream_t grad_stream) {
       if (fuse_layer[l]) return;  // updated inside its wgrad epilogue
-      cudaStream_t src = comm ? cst : grad_stream;
       SPB_CUDA(cudaEventRecord(ev(kEvUpd + 2 * l), s));  // dgrad_l issued before this point on s
-      SPB_CUDA(cudaEventRecord(ev(kEvUpd + 2 * l + 1), src));
+      SPB_CUDA(cudaEventRecord(ev(kEvUpd + 2 * l + 1), grad_stream));
       SPB_CUDA(cudaStreamWaitEvent(us, ev(kEvUpd + 2 * l), 0));
       SPB_CUDA(cudaStreamWaitEvent(us, ev(kEvUpd + 2 * l + 1), 0));
       const long off = w_off[l], cnt = b_off[l] + round_up(w[l], 32) - w_off[l];
@@ -1840,14 +1725,8 @@ struct Engine {
         fwd_wait[l] = ev_ready(l);
       }
     };
-    if (comm) {
-      n += enqueue_pass(rows, row0, alpha, s, [&](int l, cudaStream_t from) { return enqueue_bucket(l, full, from); },
-                        false, &ctl->step, on_layer);
-      if (last) join(cst, kEvStepJoin);
-    } else {
-      n += enqueue_pass(rows, row0, alpha, s, nullptr, fused_ok, &ctl->step,
-                        per_layer ? std::function<void(int, cudaStream_t)>(on_layer) : nullptr);
-    }
+    n += enqueue_pass(rows, row0, alpha, s, nullptr, fused_ok, &ctl->step,
+                      per_layer ? std::function<void(int, cudaStream_t)>(on_layer) : nullptr);
     if (per_layer && concurrent && last) join(s3, kEvUpdJoin);
     return n;
   }
@@ -2453,7 +2332,7 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     e.buckets[1] = spb::bucket_plan(e.k, e.L, nranks, true);
     e.set_workers(spb::rank_workers(e.k, e.L, rank, nranks));
     e.ensure_rows(static_cast<int>(e.workers.size()) * e.bw);
-    // Aggregation mode: SPB_COMM = rh | p2p | sub | push | nccl | nvls.
+    // Aggregation mode: SPB_COMM = rh | p2p | sub | push.
     // Default by measurement (cfg3): p2p for 2 ranks (one
     // pairwise copy-engine exchange); push for 4 ranks (gradient rows stored
     // to their owners by the wgrad epilogue: 4.47 ms vs rh 5.02, p2p 5.2,
@@ -2463,12 +2342,12 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     const char* cm = std::getenv("SPB_COMM");
     const std::string mode =
         cm ? cm : (nranks == 2 ? "p2p" : (nranks == 4 ? (e.conv_model ? "rh" : "push") : "sub"));
-    if (mode != "p2p" && mode != "nccl" && mode != "nvls" && mode != "sub" && mode != "push" && mode != "rh")
-      throw spb::ArgumentError("comm: SPB_COMM must be rh, push, p2p, sub, nccl or nvls");
+    if (mode != "p2p" && mode != "sub" && mode != "push" && mode != "rh")
+      throw spb::ArgumentError("comm: SPB_COMM must be rh, push, p2p or sub");
     // NCCL's kernels need SMs while the backward GEMMs run: keep some free
     // (the copy-engine modes' few SM kernels measured the same with 0 / 16).
     const char* rs = std::getenv("SPB_COMM_SMS");
-    e.reserved_sms = rs ? std::max(0, std::atoi(rs)) : ((mode == "nccl" || mode == "sub" || mode == "nvls") ? 16 : 0);
+    e.reserved_sms = rs ? std::max(0, std::atoi(rs)) : (mode == "sub" ? 16 : 0);
     if (mode == "rh" && (nranks & (nranks - 1)))
       throw spb::ArgumentError("comm: rh mode needs a power-of-two rank count");
     if (nranks > 1 && mode == "p2p") e.setup_p2p();
@@ -2480,14 +2359,6 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     }
     if (nranks > 1 && mode == "push") e.setup_push();
     if (nranks > 1 && mode == "sub") e.setup_sub();
-    if (nranks > 1 && mode == "nvls") {
-      // Socket names derive from the unique id, shared by all ranks.
-      uint64_t h = 1469598103934665603ull;
-      for (size_t i = 0; i < sizeof id; ++i) h = (h ^ reinterpret_cast<const unsigned char*>(&id)[i]) * 1099511628211ull;
-      char tag[48];
-      std::snprintf(tag, sizeof tag, "spb-nvls-%016llx", static_cast<unsigned long long>(h));
-      if (e.setup_nvls(tag)) e.comm_mode = 1;
-    }
   });
   if (st != SPB_OK && ctx && (ctx->e.err.rfind("nccl", 0) == 0 || ctx->e.err.rfind("comm: ", 0) == 0))
     return SPB_E_NCCL;
@@ -2507,24 +2378,6 @@ spb_status spb_layer_shard(long long count, int parts, long long* shard) {
 
 spb_status spb_comm_mode(spb_ctx* ctx, int* mode) {
   return guard(ctx, [&] { *mode = ctx->e.comm ? ctx->e.comm_mode : -1; });
-}
-
-spb_status spb_comm_selftest(spb_ctx* ctx, long long* mismatches) {
-  return guard(ctx, [&] {
-    auto& e = ctx->e;
-    if (!e.nvls) throw spb::ConfigError("comm_selftest: NVLS is not enabled");
-    const std::string tag = e.nvls_tag + "-t" + std::to_string(e.nvls_tests++);
-    *mismatches = spb::nvls_selftest(e.dev, e.rank, e.nranks, tag, [&] { e.host_barrier(); });
-  });
-}
-
-spb_status spb_comm_bench(spb_ctx* ctx, long long n_floats, int reps) {
-  return guard(ctx, [&] {
-    auto& e = ctx->e;
-    if (!e.nvls) throw spb::ConfigError("comm_bench: NVLS is not enabled");
-    const std::string tag = e.nvls_tag + "-t" + std::to_string(e.nvls_tests++);
-    spb::nvls_bench(e.dev, e.rank, e.nranks, tag, [&] { e.host_barrier(); }, n_floats, reps);
-  });
 }
 
 spb_status spb_bucket_plan(int k, int L, int nranks, int full_backprop, int* kind, int* root, int* rank_mask) {

@@ -113,8 +113,6 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "spb_trace_steps": (i, [vp, u64, i, i, i, i, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong), ip, ip, ip,
                                 ip]),
         "spb_comm_mode": (i, [vp, ip]),
-        "spb_comm_selftest": (i, [vp, C.POINTER(C.c_longlong)]),
-        "spb_comm_bench": (i, [vp, C.c_longlong, i]),
         "spb_profile_task": (i, [vp, i, i, i, fp, fp, C.POINTER(C.c_double)]),
         "spb_empirical_variance": (i, [vp, i, i, i, u64, C.POINTER(C.c_double)]),
         "spb_create_conv": (i, [ip, i, i, i, i, i, C.POINTER(vp)]),
@@ -134,7 +132,7 @@ EXPORTED = [
     "spb_last_batch", "spb_launches_per_step", "spb_make_random_chain_mlp",
     "spb_get_grads", "spb_profile_step", "spb_time_train_steps", "spb_bucket_plan", "spb_set_fused_update",
     "spb_set_chain", "spb_trace_steps", "spb_step_host_async",
-    "spb_comm_mode", "spb_comm_selftest", "spb_comm_bench", "spb_profile_task",
+    "spb_comm_mode", "spb_profile_task",
     "spb_empirical_variance", "spb_create_conv",
 ]
 
@@ -487,16 +485,10 @@ class ChainMlp:
 
     @property
     def comm_mode(self):
-        """Multi-GPU aggregation mode: "rh", "push", "p2p", "sub", "nvls", "nccl" (None before comm_init)."""
+        """Multi-GPU aggregation mode: "rh", "push", "p2p", "sub" (None before comm_init; "local" for one rank)."""
         v = C.c_int()
         _check(load_library().spb_comm_mode(self._ctx, C.byref(v)), self._ctx)
-        return {0: "nccl", 1: "nvls", 2: "p2p", 3: "sub", 4: "push", 5: "rh"}.get(v.value)
-
-    def comm_selftest(self) -> int:
-        """Collective NVLS diagnostic; returns the mismatching element count."""
-        v = C.c_longlong()
-        _check(load_library().spb_comm_selftest(self._ctx, C.byref(v)), self._ctx)
-        return int(v.value)
+        return {0: "local", 2: "p2p", 3: "sub", 4: "push", 5: "rh"}.get(v.value)
 
     def profile_task(self, rows: int, suffix: int, reps: int = 10):
         """(forward_ms, backward_ms, peak_mem_gb) of one worker task that
@@ -506,10 +498,6 @@ class ChainMlp:
         mem = C.c_double()
         _check(load_library().spb_profile_task(self._ctx, rows, suffix, reps, _fp(f), _fp(b), C.byref(mem)), self._ctx)
         return float(f[0]), float(b[0]), float(mem.value)
-
-    def comm_bench(self, n_floats: int, reps: int = 20):
-        """Collective NVLS tuning aid (rank 0 prints the timings)."""
-        _check(load_library().spb_comm_bench(self._ctx, n_floats, reps), self._ctx)
 
     def last_batch(self, rows: int) -> np.ndarray:
         out = np.zeros(rows, dtype=np.int32)
