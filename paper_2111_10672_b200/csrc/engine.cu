@@ -170,6 +170,10 @@ struct Engine {
   float* splitk_ws = nullptr;  // split-K partials (forward / dgrad GEMMs, stream s only)
   static constexpr long kSplitkWsFloats = 16L << 20;
   float* splitk_ws2 = nullptr;  // split-K partials of the head wgrad (the gradient stream s2)
+  // Column-sum bias slices + counters of the 1-CTA wgrads (GemmEpilogue::
+  // colsum_ws): the wgrads run in stream order (s2, or s for the ConvNet).
+  float* colsum_ws = nullptr;
+  int* colsum_cnt = nullptr;
   static constexpr long kSplitkWs2Floats = 1L << 20;
   Ctl* ctl = nullptr;
   int* workers_dev = nullptr;
@@ -397,7 +401,7 @@ struct Engine {
       if (p) cudaFree(p);
     };
     f(splitk_ws);
-    f(splitk_ws2);
+    f(splitk_ws2), f(colsum_ws), f(colsum_cnt);
     f(p64);
     f(p_hi), f(p_lo), f(grad), f(mom), f(X), f(Y), f(delta), f(delta_lo), f(row_loss), f(ybatch), f(xin), f(idx),
         f(idx_in), f(loss_dev), f(tmp), f(ctl), f(workers_dev), f(epoch_dev), f(bar_dev), f(w32), f(flags),
@@ -527,6 +531,8 @@ struct Engine {
     tmp = alloc<float>(tmp_n);
     splitk_ws = alloc<float>(kSplitkWsFloats);
     splitk_ws2 = alloc<float>(kSplitkWs2Floats);
+    colsum_ws = alloc<float>(kColsumWsFloats);
+    colsum_cnt = alloc<int>(kColsumCounters);
     ctl = alloc<Ctl>(1);
     loss_dev = alloc<float>(kMaxChain);
     workers_dev = alloc<int>(k);
@@ -798,6 +804,7 @@ struct Engine {
         ep.N = fan[l];
         ep.bias_col_p1 = ep.ones_col_p1 = bc + 1;
         ep.gb_hi = grad + b_off[l];
+        ep.colsum_ws = colsum_ws, ep.colsum_cnt = colsum_cnt;
         ep.splitk_ws = splitk_ws;  // few output tiles, K = pixel rows: split K (single stream)
         ep.splitk_ws_floats = kSplitkWsFloats;
         pbeg(s);
@@ -939,6 +946,7 @@ struct Engine {
         ep.M = w[l];
         ep.N = w[l - 1];
         ep.bias_col_p1 = ep.ones_col_p1 = bc + 1;
+        ep.colsum_ws = colsum_ws, ep.colsum_cnt = colsum_cnt;
         if (lf(l)) {
           ep.out_hi = p_hi + w_off[l];
           ep.out_lo = p_lo + w_off[l];
@@ -991,6 +999,7 @@ struct Engine {
     ep.N = n_in;
     ep.bias_col_p1 = ep.ones_col_p1 = bc + 1;
     ep.gb_hi = grad + b_off[L];
+    ep.colsum_ws = colsum_ws, ep.colsum_cnt = colsum_cnt;
     ep.splitk_ws = ws;
     ep.splitk_ws_floats = ws_floats;
     return gemm_tf32x3(A, B, kEpiStoreScaled, ep, q);

@@ -128,6 +128,12 @@ CUtensorMap operand_map(const Operand& X, const float* base, int tile_rows) {
 // column), rows 32-63 zeros (its lo half), read as 32 x 32 MN-major boxes.
 // Allocated once per device by gemm_prepare_device (not capturable).
 const float* g_ones[64] = {};
+// Default column-sum slice scratch / counters (GemmEpilogue::colsum_ws /
+// colsum_cnt) for callers that pass none: one per device, so such callers
+// must not run colsum GEMMs on two streams at once (the engine passes its own).
+float* g_colsum_ws[64] = {};
+int* g_colsum_cnt[64] = {};
+
 
 const float* ones_buffer() {
   int dev = 0;
@@ -168,6 +174,15 @@ void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cud
   const CUtensorMap ones = ep.ones_col_p1 > 0 ? ones_map() : ah;
   GemmEpilogue e = ep;
   if (e.chunk_kb <= 0) e.chunk_kb = chunk_for(AM, BM_);
+  if (e.colsum_col_p1 > 0 && !e.colsum_ws) {  // the per-device default slice scratch
+    int dev = 0;
+    SPB_CUDA(cudaGetDevice(&dev));
+    e.colsum_ws = g_colsum_ws[dev];
+    e.colsum_cnt = g_colsum_cnt[dev];
+  }
+  if (e.colsum_col_p1 > 0 && (!e.colsum_ws || static_cast<long>(num_n) * num_m * kBM > kColsumWsFloats ||
+                              num_m > kColsumCounters))
+    throw std::invalid_argument("gemm: column-sum scratch missing or too small");
   kern<<<grid, 256, smem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, e, wh, wl, wm, ic, ones);
   SPB_CUDA(cudaGetLastError());
 }
@@ -250,6 +265,38 @@ __global__ void splitk_fixup_kernel(const float* __restrict__ ws, int splits, lo
   }
 }
 
+// The same for many splits and few outputs (the conv wgrads: K = up to ~1M
+// pixel rows over <= 296 splits, a few thousand outputs): one warp per output,
+// lanes strided over the splits, a fixed shuffle tree -- deterministic.
+template <int EPI>
+__global__ void splitk_fixup_wide_kernel(const float* __restrict__ ws, int splits, long stride, long ldw, GemmEpilogue ep) {
+  const int cols = epi_cols(ep);
+  const long n = static_cast<long>(ep.M) * cols;
+  const int lane = threadIdx.x & 31;
+  for (long i = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += (static_cast<long>(gridDim.x) * blockDim.x) >> 5) {
+    const int r = static_cast<int>(i / cols), c = static_cast<int>(i % cols);
+    float v = 0.f;
+    for (int sp = lane; sp < splits; sp += 32) v += ws[sp * stride + r * ldw + c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) epilogue_one<EPI>(ep, v, r, c);
+  }
+}
+
+template <int EPI>
+void launch_fixup(const float* ws, int splits, long stride, long ldw, const GemmEpilogue& ep, cudaStream_t s) {
+  const long n = static_cast<long>(ep.M) * epi_cols(ep);
+  if (splits >= 16) {
+    const int grid = static_cast<int>(std::min<long>((n * 32 + 255) / 256, 148L * 32));
+    splitk_fixup_wide_kernel<EPI><<<grid, 256, 0, s>>>(ws, splits, stride, ldw, ep);
+  } else {
+    const int grid = static_cast<int>(std::min<long>((n + 255) / 256, 148L * 16));
+    splitk_fixup_kernel<EPI><<<grid, 256, 0, s>>>(ws, splits, stride, ldw, ep);
+  }
+  SPB_CUDA(cudaGetLastError());
+}
+
 // Launch plan: the 1-CTA 128x128 kernel or the CTA-pair 256 x pn kernel,
 // with `splits` K-splits (fp32 partials + deterministic fixup) when > 1.
 struct Plan {
@@ -271,6 +318,7 @@ void launch_splitk(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
   part.split_stride = stride;
   part.ones_col_p1 = ep.ones_col_p1;  // the partials compute the bias column like any other
   part.colsum_col_p1 = ep.colsum_col_p1;  // (or the column-sum warps write it into the workspace)
+  part.colsum_ws = ep.colsum_ws, part.colsum_cnt = ep.colsum_cnt;
   // Splits actually populated: ceil(kb / ceil(kb / splits)) can be < splits.
   const int kb = (A.k + kBK - 1) / kBK, kbs = (kb + plan.splits - 1) / plan.splits;
   const int splits = (kb + kbs - 1) / kbs;
@@ -281,10 +329,7 @@ void launch_splitk(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
   else if (!A.mn_major && B.mn_major) launch_inst<128, false, true, kEpiStoreScaled>(A, B, part, s, splits);
   else if (A.mn_major && !B.mn_major) launch_inst<128, true, false, kEpiStoreScaled>(A, B, part, s, splits);
   else launch_inst<128, true, true, kEpiStoreScaled>(A, B, part, s, splits);
-  const long n = static_cast<long>(A.mn) * B.mn;
-  const int grid = static_cast<int>(std::min<long>((n + 255) / 256, 148L * 16));
-  splitk_fixup_kernel<EPI><<<grid, 256, 0, s>>>(ep.splitk_ws, splits, stride, ldw, ep);
-  SPB_CUDA(cudaGetLastError());
+  launch_fixup<EPI>(ep.splitk_ws, splits, stride, ldw, ep, s);
 }
 
 int g_force_variant = -1;  // -1 auto, 0 = 1-CTA 128x128, 1 = CTA pair
@@ -376,6 +421,10 @@ void gemm_prepare_device() {
   std::fill(h.begin(), h.begin() + 32 * 32, 1.f);
   SPB_CUDA(cudaMemcpy(p, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
   g_ones[dev] = p;
+  SPB_CUDA(cudaMalloc(&g_colsum_ws[dev], kColsumWsFloats * sizeof(float)));
+  SPB_CUDA(cudaMalloc(&g_colsum_cnt[dev], kColsumCounters * sizeof(int)));
+  SPB_CUDA(cudaMemset(g_colsum_cnt[dev], 0, kColsumCounters * sizeof(int)));
+  SPB_CUDA(cudaDeviceSynchronize());
 }
 
 void gemm_force_plan(int two_sm, int pn, int splits) { g_force_plan = {two_sm != 0, splits, pn}; }
@@ -441,13 +490,11 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
     part.N = N;
     part.split_stride = stride;
     part.colsum_col_p1 = e.colsum_col_p1;  // bias partials into the workspace column
+    part.colsum_ws = e.colsum_ws, part.colsum_cnt = e.colsum_cnt;
     launch_inst<128, true, true, kEpiStoreScaled, false, 2>(A, B, part, s, plan.splits, nullptr, b, ic);
-    const long n = static_cast<long>(A.mn) * epi_cols(e);
-    const int grid = static_cast<int>(std::min<long>((n + 255) / 256, 148L * 16));
     const int kb = (A.k + kBK - 1) / kBK, kbs = (kb + plan.splits - 1) / plan.splits;
     // (the fixup's epilogue `e` routes column 9 c_in to the bias)
-    splitk_fixup_kernel<kEpiStoreScaled><<<grid, 256, 0, s>>>(ep.splitk_ws, (kb + kbs - 1) / kbs, stride, ldw, e);
-    SPB_CUDA(cudaGetLastError());
+    launch_fixup<kEpiStoreScaled>(ep.splitk_ws, (kb + kbs - 1) / kbs, stride, ldw, e, s);
     return 2;
   }
   launch_inst<128, true, true, kEpiStoreScaled, false, 2>(A, B, e, s, 1, nullptr, b, ic);

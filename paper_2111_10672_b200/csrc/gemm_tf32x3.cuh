@@ -88,6 +88,13 @@ struct GemmEpilogue {
   // kernel uses the ones column instead (its CTA 1 cannot see the stage
   // barrier, which lives on the leader).
   int colsum_col_p1;
+  // Without K-splits every column tile of an m-tile sums a 1/(column tiles)
+  // slice of the k-blocks (so no CTA carries all of it); the slices meet in
+  // colsum_ws [column tiles x m-tiles*128] and the last tile to finish (per
+  // m-tile counter colsum_cnt, zero between launches) adds them in tile
+  // order -- deterministic.
+  float* colsum_ws;
+  int* colsum_cnt;
   float* gb_hi;
   float* gb_lo;
   float* gb_mom;
@@ -568,23 +575,27 @@ __global__ void __launch_bounds__(256, 1)
       // the float4 p = l & 7 (m = 4p .. 4p + 3 of the box) of the rows
       // k = 4 kk + (l >> 3): 16-byte loads, one fp32 partial per k-block,
       // Kahan-compensated across k-blocks, the four row-phase lanes combined
-      // at the end. The unit of split s whose column tile is s mod (column
-      // tiles) carries the bias, so the work spreads over all column tiles.
+      // at the end. With K-splits, the unit of split s whose column tile is
+      // s mod (column tiles) sums its whole k-range (the fixup adds the
+      // splits); without, column tile j sums the k-blocks kb = j mod (column
+      // tiles) and the per-m-tile counter combines the slices (colsum_ws).
       const int box0 = static_cast<int>(warp - 2) * 2;
       const int col = ep.colsum_col_p1 - 1;
       const int num_n_tiles = num_tiles / num_m_tiles;
+      const bool split_k = num_units > num_tiles;
       const int p = static_cast<int>(lane & 7u), r4 = static_cast<int>(lane >> 3);
       int it = 0;
       for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
         int m0, n0, kb0, kb1, split;
         unit(u, m0, n0, kb0, kb1, split);
-        const bool mine = n0 / BN == split % num_n_tiles;
+        const int nt = n0 / BN;
+        const bool mine = split_k ? nt == split % num_n_tiles : true;
         float sum[2][4] = {}, cmp[2][4] = {};
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % Cfg::kStages;
           const uint32_t ph = (it / Cfg::kStages) & 1u;
           mbar_wait(&full_bar[s], ph);
-          if (mine) {
+          if (mine && (split_k || (kb - kb0) % num_n_tiles == nt)) {
             const uint8_t* base = smem + s * Cfg::kStageBytes;
 #pragma unroll
             for (int b = 0; b < 2; ++b) {
@@ -611,23 +622,67 @@ __global__ void __launch_bounds__(256, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty_bar[s]);
         }
-        if (mine) {
+        if (!mine) continue;
+        float tot[2][4];
 #pragma unroll
-          for (int b = 0; b < 2; ++b)
+        for (int b = 0; b < 2; ++b)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              float v = sum[b][i] - cmp[b][i];
-              v += __shfl_xor_sync(0xffffffffu, v, 8);
-              v += __shfl_xor_sync(0xffffffffu, v, 16);
-              const int row = m0 + (box0 + b) * 32 + 4 * p + i;
-              if (r4 != 0) continue;
-              if (ep.bias_col_p1 > 0) {
-                bias_store<EPI>(ep, v, row);
-              } else if (EPI == kEpiStoreScaled && row < ep.M) {  // split-K partial: the workspace column
-                ep.out_hi[split * ep.split_stride + static_cast<long>(row) * ep.ld_out + col] = ep.alpha * v;
+          for (int i = 0; i < 4; ++i) {
+            float v = sum[b][i] - cmp[b][i];
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            tot[b][i] = v;
+          }
+        bool emit = true;
+        const long mpad = static_cast<long>(num_m_tiles) * kBM;
+        if (!split_k && num_n_tiles > 1) {
+          // Publish this tile's slice, count it; the last of the m-tile's
+          // column tiles adds all slices in tile order.
+          if (r4 == 0)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                ep.colsum_ws[nt * mpad + m0 + (box0 + b) * 32 + 4 * p + i] = tot[b][i];
+          __threadfence();
+          asm volatile("bar.sync 1, 64;" ::: "memory");  // both column-sum warps published
+          // Warp 2's lane 0 counts the slice and tells warp 3 through a
+          // barrier-ordered flag next to the TMEM slot (barrier page).
+          volatile int* flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+          if (warp == 2 && lane == 0) {
+            const int mt = m0 / kBM;
+            const bool last = atomicAdd(&ep.colsum_cnt[mt], 1) == num_n_tiles - 1;
+            if (last) ep.colsum_cnt[mt] = 0;  // ready for the next launch
+            *flag = last ? 1 : 0;
+          }
+          asm volatile("bar.sync 1, 64;" ::: "memory");
+          emit = *flag != 0;
+          if (emit) {
+            __threadfence();
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const long row = m0 + (box0 + b) * 32 + 4 * p + i;
+                float v = 0.f;
+                for (int j = 0; j < num_n_tiles; ++j) v += __ldcg(ep.colsum_ws + j * mpad + row);
+                tot[b][i] = v;
               }
-            }
+          }
+          asm volatile("bar.sync 1, 64;" ::: "memory");  // the flag slot is reused by the next unit
         }
+        if (!emit || r4 != 0) continue;
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int row = m0 + (box0 + b) * 32 + 4 * p + i;
+            if (ep.bias_col_p1 > 0) {
+              bias_store<EPI>(ep, tot[b][i], row);
+            } else if (EPI == kEpiStoreScaled && row < ep.M) {  // split-K partial: the workspace column
+              ep.out_hi[split * ep.split_stride + static_cast<long>(row) * ep.ld_out + col] = ep.alpha * tot[b][i];
+            }
+          }
       }
     }
   } else if (warp >= 4) {

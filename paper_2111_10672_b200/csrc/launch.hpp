@@ -60,6 +60,10 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
 // (kEpiDgradTanh), Wf = the spatially flipped, channel-transposed kernel
 // [c_below x 9 c_out] (launch_conv_flip). src.g describes Delta as input.
 int gemm_conv_dgrad(const ConvSrc& src, long pixel0, int rows, const Operand& B, const GemmEpilogue& ep, cudaStream_t s);
+// Column-sum bias scratch a caller passes in GemmEpilogue::colsum_ws /
+// colsum_cnt (floats / zeroed counters); gemm_prepare_device makes a default.
+constexpr long kColsumWsFloats = 4L << 20;
+constexpr int kColsumCounters = 4096;
 // Per-device constants of the GEMMs (the fused-bias ones boxes); call once
 // per device before capturing any GEMM with a fused bias column.
 void gemm_prepare_device();

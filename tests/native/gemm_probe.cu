@@ -207,7 +207,7 @@ static int run_shapes() {
       for (double& v : Rb) v *= alpha;
       float* gb;
       cudaMalloc(&gb, n * 4);
-      const struct { int two, pn, sp; } fp[] = {{-1, 0, 0}, {0, 128, 3}, {1, 192, 2}, {1, 256, 1}};
+      const struct { int two, pn, sp; } fp[] = {{-1, 0, 0}, {0, 128, 3}, {0, 128, 1}, {0, 128, 1}, {1, 192, 2}, {1, 256, 1}};
       for (const auto& f : fp) {
         if (f.two >= 0 && K != 1024) continue;
         if (f.two >= 0) gemm_force_plan(f.two, f.pn, f.sp);
