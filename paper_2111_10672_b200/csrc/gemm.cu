@@ -187,16 +187,18 @@ void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cud
   SPB_CUDA(cudaGetLastError());
 }
 
-template <bool AM, bool BM_, int EPI, int PN>
-void launch_2sm_pn(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, int splits = 1) {
+template <bool AM, bool BM_, int EPI, int PN, int IC = 0>
+void launch_2sm_pn(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, int splits = 1,
+                   const CUtensorMap* ic_a = nullptr, ConvTmaArgs ic = {}) {
   using Cfg = Gemm2smCfg<PN>;
-  auto kern = gemm_tf32x3_2sm_kernel<AM, BM_, EPI, PN>;
+  auto kern = gemm_tf32x3_2sm_kernel<AM, BM_, EPI, PN, IC>;
   static bool configured = false;
   if (!configured) {
     SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
     configured = true;
   }
-  CUtensorMap ah = operand_map(A, A.hi, Cfg::kRowsA), al = operand_map(A, A.lo, Cfg::kRowsA);
+  CUtensorMap ah = IC == 1 ? ic_a[0] : operand_map(A, A.hi, Cfg::kRowsA);
+  CUtensorMap al = IC == 1 ? ic_a[1] : operand_map(A, A.lo, Cfg::kRowsA);
   CUtensorMap bh = operand_map(B, B.hi, Cfg::kRowsB), bl = operand_map(B, B.lo, Cfg::kRowsB);
   const int num_kb = (A.k + kBK - 1) / kBK;
   const int num_m = (A.mn + 255) / 256, num_n = (B.mn + Cfg::kPairN - 1) / Cfg::kPairN;
@@ -209,7 +211,7 @@ void launch_2sm_pn(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
   const CUtensorMap ones = ep.ones_col_p1 > 0 ? ones_map() : ah;
   GemmEpilogue e = ep;
   if (e.chunk_kb <= 0) e.chunk_kb = chunk_for(AM, BM_);
-  kern<<<2 * clusters, Cfg::kThreads, Cfg::kSmem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, e, ones);
+  kern<<<2 * clusters, Cfg::kThreads, Cfg::kSmem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, e, ones, ic);
   SPB_CUDA(cudaGetLastError());
 }
 
@@ -429,6 +431,30 @@ void gemm_prepare_device() {
 
 void gemm_force_plan(int two_sm, int pn, int splits) { g_force_plan = {two_sm != 0, splits, pn}; }
 
+// Implicit-GEMM convolution (forward / stride-1 dgrad) on the 1-CTA kernel,
+// or -- output channels >= 128 and >= 2 pixel-row tiles -- on the CTA pair
+// (256 pixels x 128 / 256 channels per SM pair: half the shared-memory bytes
+// per FLOP of the 1-CTA tile, which is smem-bandwidth bound at 45 % tensor
+// activity on these shapes). SPB_CONV_PAIR=0 keeps the 1-CTA kernel (A/B).
+template <int EPI>
+int launch_conv_implicit(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s,
+                         const CUtensorMap* a, const ConvTmaArgs& ic) {
+  static const bool pair_off = [] {
+    const char* v = std::getenv("SPB_CONV_PAIR");
+    return v && std::atoi(v) == 0;
+  }();
+  if (!pair_off && B.mn >= 128 && A.mn >= 256) {
+    if (B.mn <= 128) launch_2sm_pn<false, false, EPI, 128, 1>(A, B, ep, s, 1, a, ic);
+    else launch_2sm_pn<false, false, EPI, 256, 1>(A, B, ep, s, 1, a, ic);
+    return 1;
+  }
+  if (B.mn <= 64)
+    launch_inst<64, false, false, EPI, false, 1>(A, B, ep, s, 1, a, nullptr, ic);
+  else
+    launch_inst<128, false, false, EPI, false, 1>(A, B, ep, s, 1, a, nullptr, ic);
+  return 1;
+}
+
 int gemm_conv_fwd(const ConvSrc& src, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
   const ConvGeom& g = src.g;
   if (g.c_in % 32 || src.ld % 32) throw std::invalid_argument("gemm_conv_fwd: c_in and ld must be multiples of 32");
@@ -438,11 +464,7 @@ int gemm_conv_fwd(const ConvSrc& src, const Operand& B, const GemmEpilogue& ep, 
                       im2col_map(src.lo, src, kBM, CU_TENSOR_MAP_SWIZZLE_128B)};
   const ConvTmaArgs ic{g.out_h * g.out_w, g.out_w, g.stride, g.c_in, 0, 0};
   Operand A{nullptr, nullptr, 4, M, K, false};  // shape only: tiles come from the im2col maps
-  if (B.mn <= 64)
-    launch_inst<64, false, false, kEpiFwdTanh, false, 1>(A, B, ep, s, 1, a, nullptr, ic);
-  else
-    launch_inst<128, false, false, kEpiFwdTanh, false, 1>(A, B, ep, s, 1, a, nullptr, ic);
-  return 1;
+  return launch_conv_implicit<kEpiFwdTanh>(A, B, ep, s, a, ic);
 }
 
 int gemm_conv_dgrad(const ConvSrc& src, long pixel0, int rows, const Operand& B, const GemmEpilogue& ep, cudaStream_t s) {
@@ -455,11 +477,7 @@ int gemm_conv_dgrad(const ConvSrc& src, long pixel0, int rows, const Operand& B,
                       im2col_map(src.lo, src, kBM, CU_TENSOR_MAP_SWIZZLE_128B)};
   const ConvTmaArgs ic{g.out_h * g.out_w, g.out_w, 1, g.c_in, 0, pixel0};
   Operand A{nullptr, nullptr, 4, rows, K, false};
-  if (B.mn <= 64)
-    launch_inst<64, false, false, kEpiDgradTanh, false, 1>(A, B, ep, s, 1, a, nullptr, ic);
-  else
-    launch_inst<128, false, false, kEpiDgradTanh, false, 1>(A, B, ep, s, 1, a, nullptr, ic);
-  return 1;
+  return launch_conv_implicit<kEpiDgradTanh>(A, B, ep, s, a, ic);
 }
 
 int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const GemmEpilogue& ep, cudaStream_t s) {

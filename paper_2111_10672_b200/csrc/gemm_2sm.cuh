@@ -59,12 +59,16 @@ __device__ __forceinline__ void load_operand_2sm(uint8_t* dst, const CUtensorMap
   }
 }
 
-template <bool A_MN, bool B_MN, int EPI, int PN = 256>
+// IC == 1: A is the implicit im2col operand of a 3x3 convolution (forward or
+// stride-1 dgrad), loaded through TMA im2col maps exactly as in the 1-CTA
+// kernel (gemm_tf32x3.cuh, ConvTmaArgs), each CTA its own 128 output pixels.
+template <bool A_MN, bool B_MN, int EPI, int PN = 256, int IC = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
     gemm_tf32x3_2sm_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                            const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                            int num_kb, int num_m_pairs, int num_tiles, int kb_per_split, int num_units,
-                           const __grid_constant__ GemmEpilogue ep, const __grid_constant__ CUtensorMap t_ones) {
+                           const __grid_constant__ GemmEpilogue ep, const __grid_constant__ CUtensorMap t_ones,
+                           const ConvTmaArgs ic) {
   using Cfg = Gemm2smCfg<PN>;
   const int kChunkKb = ep.chunk_kb > 0 ? ep.chunk_kb : chunk_kb<A_MN, B_MN>();
   // TMA bytes one CTA brings per k-block (A hi/lo + B hi/lo).
@@ -139,8 +143,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
             mbar_wait(&empty_bar[s], ph ^ 1u);
             if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * kCtaBytes);
             uint8_t* base = smem + s * Cfg::kStageBytes;
-            load_operand_2sm<A_MN, Cfg::kRowsA>(base, &ta_hi, &full_bar[s], m0, kb * kBK);
-            load_operand_2sm<A_MN, Cfg::kRowsA>(base + Cfg::kABytes, &ta_lo, &full_bar[s], m0, kb * kBK);
+            if constexpr (IC == 1) {
+              const int k = kb * kBK, tap = k / ic.c_in, c = k - tap * ic.c_in;
+              int w, h, n;
+              conv_origin(ic, ic.m_base + m0, w, h, n);
+              const uint16_t ox = static_cast<uint16_t>(tap % 3), oy = static_cast<uint16_t>(tap / 3);
+              tma_load_im2col_4d_2sm(base, &ta_hi, &full_bar[s], c, w, h, n, ox, oy);
+              tma_load_im2col_4d_2sm(base + Cfg::kABytes, &ta_lo, &full_bar[s], c, w, h, n, ox, oy);
+            } else {
+              load_operand_2sm<A_MN, Cfg::kRowsA>(base, &ta_hi, &full_bar[s], m0, kb * kBK);
+              load_operand_2sm<A_MN, Cfg::kRowsA>(base + Cfg::kABytes, &ta_lo, &full_bar[s], m0, kb * kBK);
+            }
             load_operand_2sm<B_MN, Cfg::kRowsB>(base + 2 * Cfg::kABytes, &tb_hi, &full_bar[s], n0, kb * kBK, &t_ones,
                                                 ones_col, 0);
             load_operand_2sm<B_MN, Cfg::kRowsB>(base + 2 * Cfg::kABytes + Cfg::kBBytes, &tb_lo, &full_bar[s], n0,
