@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include <algorithm>
@@ -334,6 +335,16 @@ void launch_splitk(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
   launch_fixup<EPI>(ep.splitk_ws, splits, stride, ldw, ep, s);
 }
 
+// A/B knob: SPB_BIAS=ones keeps the virtual ones column in the 1-CTA kernels
+// too (an extra column tile) instead of the column-sum warps.
+bool bias_by_ones() {
+  static const bool v = [] {
+    const char* e = std::getenv("SPB_BIAS");
+    return e && std::string(e) == "ones";
+  }();
+  return v;
+}
+
 int g_force_variant = -1;  // -1 auto, 0 = 1-CTA 128x128, 1 = CTA pair
 Plan g_force_plan{false, 0, 0};  // splits == 0: not forced
 Plan g_last_plan{false, 1, 128};  // the plan of the last gemm_tf32x3 launch (test hook)
@@ -486,12 +497,14 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
   if (!A.mn_major) throw std::invalid_argument("gemm_conv_wgrad: A (Delta) must be MN-major");
   // N = 9 c_in weight columns; with ep.bias_col_p1 = 9 c_in + 1 the bias is
   // produced by the kernel's column-sum warps as output column 9 c_in.
-  const int N = 9 * g.c_in;
-  if (ep.bias_col_p1 > 0 && ep.bias_col_p1 != N + 1)
+  const int Nw = 9 * g.c_in;
+  if (ep.bias_col_p1 > 0 && ep.bias_col_p1 != Nw + 1)
     throw std::invalid_argument("gemm_conv_wgrad: the bias column must follow the 9 c_in weights");
   GemmEpilogue e = ep;
-  e.ones_col_p1 = 0;
-  e.colsum_col_p1 = ep.bias_col_p1;
+  const bool ones = ep.bias_col_p1 > 0 && bias_by_ones();
+  const int N = ones ? Nw + 1 : Nw;  // the ones column (A/B knob) is one more GEMM column
+  e.ones_col_p1 = ones ? ep.bias_col_p1 : 0;
+  e.colsum_col_p1 = ones ? 0 : ep.bias_col_p1;
   CUtensorMap b[2] = {im2col_map(src.hi, src, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B),
                       im2col_map(src.lo, src, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)};
   const ConvTmaArgs ic{g.out_h * g.out_w, g.out_w, g.stride, g.c_in, pixel0, 0};
@@ -555,7 +568,7 @@ int gemm_tf32x3(const Operand& A, const Operand& B, int epi, const GemmEpilogue&
                               narrow_pair_ok(A, B, epi), ep.route_rows == 0, A.mn_major && B.mn_major,
                               ep.ones_col_p1 > 0);
   g_last_plan = plan;
-  if (ep.ones_col_p1 > 0 && (!plan.two_sm || (epi == kEpiWgradUpdate && g_force_variant != 1))) {
+  if (ep.ones_col_p1 > 0 && !bias_by_ones() && (!plan.two_sm || (epi == kEpiWgradUpdate && g_force_variant != 1))) {
     // 1-CTA kernel: the column-sum warps produce the bias (no extra column tile).
     Operand B2 = B;
     B2.mn = B.mn_map > 0 ? B.mn_map : B.mn - 1;

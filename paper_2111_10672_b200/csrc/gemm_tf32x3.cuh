@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(256, 1)
       const int num_n_tiles = num_tiles / num_m_tiles;
       const bool split_k = num_units > num_tiles;
       const int p = static_cast<int>(lane & 7u), r4 = static_cast<int>(lane >> 3);
-      int it = 0;
+      int it = 0, uflip = 0;
       for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
         int m0, n0, kb0, kb1, split;
         unit(u, m0, n0, kb0, kb1, split);
@@ -644,21 +644,25 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
               for (int i = 0; i < 4; ++i)
                 ep.colsum_ws[nt * mpad + m0 + (box0 + b) * 32 + 4 * p + i] = tot[b][i];
-          __threadfence();
-          asm volatile("bar.sync 1, 64;" ::: "memory");  // both column-sum warps published
-          // Warp 2's lane 0 counts the slice and tells warp 3 through a
-          // barrier-ordered flag next to the TMEM slot (barrier page).
-          volatile int* flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+          // bar.sync then ONE gpu-scope acq_rel atomic by warp 2's lane 0
+          // publishes every lane's slice (the barrier orders the 64 threads'
+          // stores before the release) -- no per-thread fences -- and tells
+          // warp 3 through a barrier-ordered flag (two slots, alternating by
+          // unit, next to the TMEM slot in the barrier page).
+          asm volatile("bar.sync 1, 64;" ::: "memory");
+          volatile int* flag = reinterpret_cast<volatile int*>(tmem_slot + 1 + (uflip & 1));
           if (warp == 2 && lane == 0) {
             const int mt = m0 / kBM;
-            const bool last = atomicAdd(&ep.colsum_cnt[mt], 1) == num_n_tiles - 1;
+            int old;
+            asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(ep.colsum_cnt + mt) : "memory");
+            const bool last = old == num_n_tiles - 1;
             if (last) ep.colsum_cnt[mt] = 0;  // ready for the next launch
             *flag = last ? 1 : 0;
           }
           asm volatile("bar.sync 1, 64;" ::: "memory");
           emit = *flag != 0;
+          ++uflip;
           if (emit) {
-            __threadfence();
 #pragma unroll
             for (int b = 0; b < 2; ++b)
 #pragma unroll
@@ -669,7 +673,6 @@ __global__ void __launch_bounds__(256, 1)
                 tot[b][i] = v;
               }
           }
-          asm volatile("bar.sync 1, 64;" ::: "memory");  // the flag slot is reused by the next unit
         }
         if (!emit || r4 != 0) continue;
 #pragma unroll
