@@ -451,3 +451,41 @@ def test_step_host_rejects_bad_host_arrays():
             m.step_host_async(bad_x, bad_y, np.zeros(1, np.float32))
     m.step_host(x, y)
     m.close()
+
+
+def test_k1_spb_equals_plain_sgd_bitwise_50_iterations():
+    """verify.cpp:274-301 through the DEVICE step: with k = 1 the single worker
+    backpropagates every layer, so 50 SPB-SGD iterations are bit-identical to
+    50 plain SGD (full-backprop) iterations on the same draws."""
+    widths = [64, 48, 32, 1]
+    a, *_ = make(widths, 256, 3, k=1, bw=16)
+    b, *_ = make(widths, 256, 3, k=1, bw=16)
+    a.set_optimizer(1e-2)
+    b.set_optimizer(1e-2)
+    la = a.train_steps(5, 1, 50, losses=True)
+    lb = b.train_steps(5, 1, 50, full_backprop=True, losses=True)
+    assert np.array_equal(la, lb)
+    for x, y in zip(a.get_params(), b.get_params()):
+        assert np.array_equal(x, y)
+
+
+def test_aggregation_unbiased_through_device_step():
+    """verify.cpp:303-341 through the DEVICE step: the mean of many SPB
+    aggregates (each from fresh worker draws, k = 4) converges to the full
+    gradient -- every layer's deviation within 3 standard errors."""
+    widths, N, k, bw, trials = [12, 10, 8, 6, 1], 96, 4, 2, 3000
+    m, X, Y, W = make(widths, N, 9, k=k, bw=bw)
+    L = len(widths) - 1
+    full = spb.partial_backprop(m, None, np.arange(N, dtype=np.int32), L).blocks  # full_gradient
+    m.set_optimizer(0.0)
+    m.set_fused_update(0)
+    est = []
+    for t in range(1, trials + 1):
+        m.train_steps(77, t, 1)
+        est.append([g.astype(np.float64) for g in m.get_grads()])
+    for l in range(L):
+        e = np.stack([x[l] for x in est])
+        mean = e.mean(axis=0)
+        se = np.sqrt(((e - mean) ** 2).sum() / trials / (trials - 1))
+        dev = np.linalg.norm(mean - full[l])
+        assert dev <= 3.0 * se, (l, dev / se)
