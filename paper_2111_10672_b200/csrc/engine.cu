@@ -219,7 +219,11 @@ struct Engine {
   // wgrads over <= kFuseMaxRows contributor rows, where it is cheaper than a
   // separate update pass (measured: the fused epilogue costs the same as
   // wgrad + update at 1024 rows and saves ~20 us per layer at <= 512).
-  int fused_mode = 2;
+  int fused_mode = default_fused_mode();
+  static int default_fused_mode() {  // SPB_FUSED_MODE: A/B experiments (spb_set_fused_update sets it per context)
+    const char* v = std::getenv("SPB_FUSED_MODE");
+    return v ? std::max(0, std::min(2, std::atoi(v))) : 2;
+  }
   static constexpr int kFuseMaxRows = 512;  // 640 / 768 measured the same; 384 slower
   std::vector<char> fuse_layer;  // per layer, set by enqueue_step for enqueue_pass / on_layer
   // Multi-GPU aggregation mode (0 = none selected yet):

@@ -116,6 +116,33 @@ int chunk_for(bool a_mn, bool b_mn) {
   return g_chunk[kind];
 }
 
+// Launch with programmatic stream serialization (SPB_PDL=1, default on): the
+// GEMM's prologue (barrier init, TMEM allocation, tensor-map prefetch) may
+// start while the previous kernel in the stream drains; the kernels execute
+// griddepcontrol.wait before touching any data (gemm_tf32x3.cuh).
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("SPB_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
+  return v;
+}
+
+template <class Kern, class... Args>
+void launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  SPB_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 // The TMA extent along MN: the operand's real columns (mn_map) when the GEMM
 // extends past them (the fused-bias ones column of a wgrad B operand).
 CUtensorMap operand_map(const Operand& X, const float* base, int tile_rows) {
@@ -184,7 +211,8 @@ void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cud
   if (e.colsum_col_p1 > 0 && (!e.colsum_ws || static_cast<long>(num_n) * num_m * kBM > kColsumWsFloats ||
                               num_m > kColsumCounters))
     throw std::invalid_argument("gemm: column-sum scratch missing or too small");
-  kern<<<grid, 256, smem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, e, wh, wl, wm, ic, ones);
+  launch_pdl(kern, dim3(grid), dim3(256), smem, s, ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, e, wh, wl, wm, ic,
+             ones);
   SPB_CUDA(cudaGetLastError());
 }
 
@@ -212,7 +240,8 @@ void launch_2sm_pn(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
   const CUtensorMap ones = ep.ones_col_p1 > 0 ? ones_map() : ah;
   GemmEpilogue e = ep;
   if (e.chunk_kb <= 0) e.chunk_kb = chunk_for(AM, BM_);
-  kern<<<2 * clusters, Cfg::kThreads, Cfg::kSmem, s>>>(ah, al, bh, bl, num_kb, num_m, tiles, kbs, units, e, ones, ic);
+  launch_pdl(kern, dim3(2 * clusters), dim3(Cfg::kThreads), Cfg::kSmem, s, ah, al, bh, bl, num_kb, num_m, tiles, kbs,
+             units, e, ones, ic);
   SPB_CUDA(cudaGetLastError());
 }
 

@@ -126,6 +126,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Programmatic dependent launch (see gemm_tf32x3.cuh).
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp < 4) {
     if (warp == 0) {
