@@ -364,12 +364,16 @@ void launch_splitk(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
   launch_fixup<EPI>(ep.splitk_ws, splits, stride, ldw, ep, s);
 }
 
-// A/B knob: SPB_BIAS=ones keeps the virtual ones column in the 1-CTA kernels
-// too (an extra column tile) instead of the column-sum warps.
+// How the 1-CTA kernels produce the fused bias column: the virtual ones column
+// (default: one more column tile when n is a multiple of 128) or, with
+// SPB_BIAS=colsum, the column-sum warps. Same-box A/B (tools/ab_env.py, 3
+// rounds each): cfg3 SPB step 5.95-6.00 ms with the ones column vs 6.06-6.12
+// with the column sums (their per-k-block barrier traffic and extra smem reads
+// in the smem-bound 1-CTA kernel cost more than the 33rd tile); cfg4 equal.
 bool bias_by_ones() {
   static const bool v = [] {
     const char* e = std::getenv("SPB_BIAS");
-    return e && std::string(e) == "ones";
+    return !(e && std::string(e) == "colsum");
   }();
   return v;
 }

@@ -45,3 +45,7 @@ def test_gemm_probe_benchmark_shapes():
     # the plans the 1-GPU cfg3 step ships (profiles/r01_launches_cfg3_summary_v2.json)
     assert re.search(r"shape forward \(tanh epilogue\)\s+M=1024 N=4096 K=4096 plan=2sm/pn240/sp1", r.stdout)
     assert re.search(r"shape wgrad \(alpha epilogue\)\s+M=4096 N=4096 K=1024 plan=2sm/pn192/sp1", r.stdout)
+    # the same shapes with the 1-CTA kernels' column-sum bias warps (SPB_BIAS=colsum)
+    r = subprocess.run([_build_probe(), "shapes"], capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, SPB_BIAS="colsum"))
+    assert r.returncode == 0 and "GEMM SHAPES OK" in r.stdout, r.stdout + r.stderr
