@@ -116,14 +116,16 @@ int chunk_for(bool a_mn, bool b_mn) {
   return g_chunk[kind];
 }
 
-// Launch with programmatic stream serialization (SPB_PDL=1, default on): the
+// Launch with programmatic stream serialization (SPB_PDL=1; default off): the
 // GEMM's prologue (barrier init, TMEM allocation, tensor-map prefetch) may
 // start while the previous kernel in the stream drains; the kernels execute
-// griddepcontrol.wait before touching any data (gemm_tf32x3.cuh).
+// griddepcontrol.wait before touching any data (gemm_tf32x3.cuh). Same-box
+// A/B (tools/ab_env.py, 3 rounds): cfg3 SPB 6.04 vs 6.02 ms, full backprop
+// 8.54 vs 8.35 ms, cfg4 equal -- no gain, so off.
 bool pdl_enabled() {
   static const bool v = [] {
     const char* e = std::getenv("SPB_PDL");
-    return !e || std::atoi(e) != 0;
+    return e && std::atoi(e) != 0;
   }();
   return v;
 }
@@ -553,7 +555,8 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
     part.M = A.mn;
     part.N = N;
     part.split_stride = stride;
-    part.colsum_col_p1 = e.colsum_col_p1;  // bias partials into the workspace column
+    part.ones_col_p1 = e.ones_col_p1;      // the partials compute the bias column like any other,
+    part.colsum_col_p1 = e.colsum_col_p1;  // or the column-sum warps write it into the workspace
     part.colsum_ws = e.colsum_ws, part.colsum_cnt = e.colsum_cnt;
     launch_inst<128, true, true, kEpiStoreScaled, false, 2>(A, B, part, s, plan.splits, nullptr, b, ic);
     const int kb = (A.k + kBK - 1) / kBK, kbs = (kb + plan.splits - 1) / plan.splits;
