@@ -161,3 +161,27 @@ def test_cfg4_resnet18_widths_match_conv_oracle(orc):
     for l in range(o.L):
         assert rel_err(after[l], B[l]) <= WEIGHT_TOL
         assert delta_ok(after[l], W0[l], B[l]), l
+
+
+@pytest.mark.parametrize("width", [1024, 2048, 8192])
+def test_cfg5_widths_match_batched_oracle(orc, width):
+    """cfg5 (BASELINE configs[4]: the width sweep 1k-8k, k = 8, B_w = 128) at
+    depth 4: the step-1 aggregate of every layer against oracle/batched.py
+    (1e-5), SPB, on the GEMM plans those widths select."""
+    from paper_2111_10672_b200 import spb
+
+    widths, k, bw, N, seed = [width] * 4 + [1], 8, 128, 2048, 11
+    X, Y, W = spb.gen_chain_mlp(widths, N, 7)
+    m = spb.ChainMlp(widths, X, Y, W, k=k, per_worker_batch=bw)
+    try:
+        m.set_optimizer(0.0)
+        m.set_fused_update(0)
+        m.train_steps(seed, 1, 1)
+        grads = m.get_grads()
+    finally:
+        m.close()
+    rows = _rows(orc, seed, 1, k, bw, N)
+    g = batched.aggregate_step(widths, X[rows].astype(np.float64), Y[rows].astype(np.float64),
+                               [b.astype(np.float64) for b in W], k, bw)
+    for l, (a, b) in enumerate(zip(grads, g)):
+        assert rel_err(a, b) <= GRAD_TOL, (width, l, rel_err(a, b))
