@@ -69,8 +69,11 @@ SPB_API spb_status spb_layer_chunks(int k, int L, int* out);
  * (spb.cpp:176,187,141): count sample indices in [0, dataset_size). */
 SPB_API spb_status spb_draw_batch(uint64_t seed, int step, int worker, int count, int dataset_size, int* out);
 /* Worker placement for multi-GPU runs: the workers (1-based, ascending) that
- * rank `rank` of `nranks` hosts, balanced so every rank carries the same
- * backward work (pairs j, k+1-j). Writes *count entries to out (size >= k). */
+ * rank `rank` of `nranks` hosts: one each when nranks == k; below 4 ranks
+ * balanced pairs (j, k+1-j), so every rank carries the same backward work;
+ * from 4 ranks contiguous blocks (fewer contributing ranks per layer, fewer
+ * exchange bytes; measured faster there). SPB_PLACEMENT=balanced|contiguous
+ * overrides. Writes *count entries to out (size >= k). */
 SPB_API spb_status spb_rank_workers(int k, int L, int rank, int nranks, int* out, int* count);
 
 /* make_random_chain_mlp (model.hpp:240-241, model.cpp:208-231): the
@@ -235,9 +238,7 @@ SPB_API void* spb_stream(spb_ctx* ctx);
  *    stores through CUDA IPC, staged through shared memory into 128-byte row
  *    segments); the owner sums its rows and applies the optimizer; the peers
  *    pull the new fp32 rows (copy engines) and split them into (hi, lo);
- * Ranks of one node only. SPB_PLACEMENT=contiguous deals consecutive workers
- * to ranks instead of balanced pairs (spb_rank_workers): less exchange, less
- * balanced backward work. */
+ * Ranks of one node only. The placement of workers on ranks: spb_rank_workers. */
 SPB_API spb_status spb_comm_unique_id(void* out128);
 SPB_API spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int nranks);
 /* Tuning aid (process-wide): k-blocks of K (32 each) the tensor cores

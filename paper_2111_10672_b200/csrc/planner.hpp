@@ -92,16 +92,20 @@ inline int worker_stop(int j, int k, int L) { return L - suffix_layers(j, k, L) 
 // backward costs ~ s_j layers, so pairs (j, k+1-j) carry equal work; pairs are
 // dealt out snake-wise. Falls back to a count-balanced greedy (largest
 // suffix first to the least-loaded rank) when the pairing does not divide.
-// SPB_PLACEMENT=contiguous instead deals out consecutive workers (rank r gets
+// Contiguous placement instead deals out consecutive workers (rank r gets
 // workers r*k/N+1 .. (r+1)*k/N): backward work is then unbalanced, but the
 // ranks hosting only low workers contribute to few layers, so the exchange
-// moves fewer gradient bytes (the saving SPB promises on the network).
-inline bool contiguous_placement() {
-  static const bool c = [] {
+// moves fewer gradient bytes -- the saving SPB promises on the network. It is
+// the default from 4 ranks on (measured, cfg3 at 4 B200s: push 232.3 k vs
+// 224.7 k samples/s, rh 208.0 k vs 199.2 k; at 2 ranks it loses: p2p 210.4 k
+// vs 227.5 k); SPB_PLACEMENT=balanced | contiguous overrides.
+inline bool contiguous_placement(int nranks) {
+  static const int forced = [] {
     const char* p = std::getenv("SPB_PLACEMENT");
-    return p && std::string(p) == "contiguous";
+    if (!p) return -1;
+    return std::string(p) == "contiguous" ? 1 : (std::string(p) == "balanced" ? 0 : -1);
   }();
-  return c;
+  return forced >= 0 ? forced == 1 : nranks >= 4;
 }
 
 inline std::vector<int> rank_workers(int k, int L, int rank, int nranks) {
@@ -110,7 +114,7 @@ inline std::vector<int> rank_workers(int k, int L, int rank, int nranks) {
   std::vector<std::vector<int>> owned(nranks);
   if (nranks == k) {
     for (int r = 0; r < nranks; ++r) owned[r] = {r + 1};
-  } else if (contiguous_placement()) {
+  } else if (contiguous_placement(nranks)) {
     for (int r = 0; r < nranks; ++r)
       for (int j = static_cast<int>(static_cast<long long>(r) * k / nranks) + 1;
            j <= static_cast<int>(static_cast<long long>(r + 1) * k / nranks); ++j)

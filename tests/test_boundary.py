@@ -93,7 +93,11 @@ def test_rank_workers_partition(k, L, nr):
     assert max(sizes) - min(sizes) <= 1
     for o in owned:
         assert o == sorted(o)
-    if k % (2 * nr) == 0:
+    if nr == k:
+        assert owned == [[j] for j in range(1, k + 1)]  # one worker per rank
+    elif nr >= 4:  # default from 4 ranks: contiguous blocks of workers (fewer exchange bytes)
+        assert sum(owned, []) == list(range(1, k + 1))
+    elif k % (2 * nr) == 0:  # balanced pairs (j, k+1-j): equal backward work
         loads = [sum(spb.suffix_layers(j, k, L) for j in o) for o in owned]
         assert max(loads) - min(loads) <= 2
 
