@@ -1,7 +1,8 @@
 // Non-GEMM kernels of the SPB step: dataset gather with the on-device
-// counter-based Rng, the fused output head, deterministic column reductions
-// (bias / head gradients), the fused optimizer update, and the per-layer
-// contributor average used by the aggregator entry point.
+// counter-based Rng, the fused output head, the optimizer update, and the
+// per-layer contributor averages of the aggregator entry points (fp32, and
+// fp64 with the reference's exact operation order). The bias / head gradient
+// reductions of round 1 now live inside the wgrad GEMMs (gemm_tf32x3.cuh).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -162,75 +163,6 @@ __global__ void head_kernel(const float* __restrict__ h_hi, const float* __restr
   }
 }
 
-constexpr int kColThreads = 256;
-// Rows per partial-sum split: 32, growing for very tall inputs (conv pixel
-// rows) so pass 2 sums at most ~1024 partials per column.
-inline int rows_per_split(int rows) { return std::max(32, static_cast<int>(round_up((rows + 1023) / 1024, 32))); }
-
-// Pass 1: partial[split][o][c] = sum over this split's rows.
-__global__ void colreduce_partial_kernel(const float* __restrict__ hi, const float* __restrict__ lo, long ld, int r0,
-                                         int r1, int ncols, const float* __restrict__ rowvec, int nvec, long ldv,
-                                         float* __restrict__ partial, int rps) {
-  const int c = blockIdx.x * kColThreads + threadIdx.x;
-  const int split = blockIdx.y;
-  const int ra = r0 + split * rps;
-  const int rb = min(r1, ra + rps);
-  if (c >= ncols) return;
-  float acc[kMaxOut];
-#pragma unroll
-  for (int o = 0; o < kMaxOut; ++o) acc[o] = 0.f;
-#pragma unroll 8
-  for (int r = ra; r < rb; ++r) {
-    float v = hi[static_cast<long>(r) * ld + c];
-    if (lo) v += lo[static_cast<long>(r) * ld + c];
-    if (!rowvec) {
-      acc[0] += v;
-    } else {
-#pragma unroll
-      for (int o = 0; o < kMaxOut; ++o)
-        if (o < nvec) acc[o] = fmaf(rowvec[r * ldv + o], v, acc[o]);
-    }
-  }
-  for (int o = 0; o < nvec; ++o) partial[(static_cast<long>(split) * nvec + o) * ncols + c] = acc[o];
-}
-
-// Pass 2: g = alpha * sum over splits (warp per output, fixed order); either stored to
-// out, or (upd != nullptr) applied as the optimizer step to the split pair
-// out/out_lo in place (single-GPU fused update of biases and the head).
-struct UpdArgs {
-  float* lo;
-  float* mom;
-  float lr, mu, wd;
-};
-__global__ void colreduce_final_kernel(const float* __restrict__ partial, int nsplit, int nvec, int ncols, float alpha,
-                                       float* __restrict__ out, long ld_out, UpdArgs upd, int update) {
-  // One warp per output (o, c): lane i sums splits i, i + 32, ... in order,
-  // then a fixed xor-shuffle tree -- deterministic, and parallel even when a
-  // tall input (conv pixel rows) leaves ~1000 partials per column.
-  const long t = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= static_cast<long>(nvec) * ncols) return;
-  const int o = static_cast<int>(t / ncols), c = static_cast<int>(t % ncols);
-  float s = 0.f;
-  for (int sp = lane; sp < nsplit; sp += 32) s += partial[(static_cast<long>(sp) * nvec + o) * ncols + c];
-#pragma unroll
-  for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
-  if (lane) return;
-  const long at = o * ld_out + c;
-  if (!update) {
-    out[at] = alpha * s;
-    return;
-  }
-  float g = fmaf(upd.wd, out[at] + upd.lo[at], alpha * s);
-  if (upd.mom) {
-    upd.mom[at] = fmaf(upd.mu, upd.mom[at], g);
-    g = upd.mom[at];
-  }
-  const float w = (out[at] + upd.lo[at]) - upd.lr * g;
-  const float wh = tf32_rna(w);
-  out[at] = wh;
-  upd.lo[at] = w - wh;
-}
 
 // Fused optimizer over the flat parameter pair, float4-vectorised, grid-stride:
 //   w = hi + lo; g' = g + wd*w; buf = mu*buf + g' (when mu != 0); w -= lr*buf
@@ -365,31 +297,6 @@ void launch_head(const float* h_hi, const float* h_lo, long ldh, int rows, int n
                                                                 b_hi, b_lo, y, delta, delta_lo, ldq, row_loss, dn_hi,
                                                                 dn_lo, ldd,
                                                                 cont_row0, tanh_out ? 1 : 0, dn_act ? 1 : 0);
-  SPB_CUDA(cudaGetLastError());
-}
-
-long colreduce_scratch(int rows, int ncols, int nvec) {
-  const int rps = rows_per_split(rows);
-  const long nsplit = (rows + rps - 1) / rps;
-  return (nsplit < 1 ? 1 : nsplit) * nvec * static_cast<long>(ncols);
-}
-
-void launch_colreduce(const float* hi, const float* lo, long ld, int r0, int r1, int ncols, const float* rowvec,
-                      int nvec, long ldv, float alpha, float* out, long ld_out, float* scratch, cudaStream_t s,
-                      const ColUpdate* upd) {
-  if (nvec > kMaxOut) throw std::invalid_argument("colreduce: nvec > 16");
-  const int rows = r1 - r0;
-  if (rows <= 0 || ncols <= 0) return;
-  const int rps = rows_per_split(rows);
-  const int nsplit = (rows + rps - 1) / rps;
-  dim3 g1((ncols + kColThreads - 1) / kColThreads, nsplit);
-  colreduce_partial_kernel<<<g1, kColThreads, 0, s>>>(hi, lo, ld, r0, r1, ncols, rowvec, nvec, ldv, scratch, rps);
-  SPB_CUDA(cudaGetLastError());
-  const long tot = static_cast<long>(nvec) * ncols;
-  UpdArgs u{nullptr, nullptr, 0.f, 0.f, 0.f};
-  if (upd) u = UpdArgs{upd->lo, upd->mom, upd->lr, upd->mu, upd->wd};
-  colreduce_final_kernel<<<static_cast<int>((tot * 32 + 255) / 256), 256, 0, s>>>(scratch, nsplit, nvec, ncols, alpha,
-                                                                                  out, ld_out, u, upd ? 1 : 0);
   SPB_CUDA(cudaGetLastError());
 }
 

@@ -108,20 +108,6 @@ void launch_head(const float* h_hi, const float* h_lo, long ldh, int rows, int n
                  const float* w_lo, long ldw, const float* b_hi, const float* b_lo, const float* y,
                  float* delta, float* delta_lo, long ldq, float* row_loss, float* dn_hi, float* dn_lo, long ldd,
                  int cont_row0, bool tanh_out, cudaStream_t s, bool dn_act = true);
-// out[o * ld_out + c] = alpha * sum_{r in [r0,r1)} vec(r,o) * (hi + lo)[r, c]
-// (vec = 1 when rowvec == nullptr, nvec = 1), deterministic two-pass column
-// reduction. scratch must hold colreduce_scratch(...) floats.
-long colreduce_scratch(int rows, int ncols, int nvec);
-// When upd is given, the reduced gradient is applied in place as the
-// optimizer step to the split pair (out = hi, upd->lo) instead of stored.
-struct ColUpdate {
-  float* lo;
-  float* mom;
-  float lr, mu, wd;
-};
-void launch_colreduce(const float* hi, const float* lo, long ld, int r0, int r1, int ncols, const float* rowvec,
-                      int nvec, long ldv, float alpha, float* out, long ld_out, float* scratch, cudaStream_t s,
-                      const ColUpdate* upd = nullptr);
 // Optimizer over the flat parameter pair (see engine.cu).
 // ctas > 0 fixes the grid (measurement tools); 0 sizes it to the SM count.
 void launch_sgd_update(float* p_hi, float* p_lo, const float* grad, float* mom, long n, float lr, float momentum,
