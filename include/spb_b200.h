@@ -222,18 +222,20 @@ SPB_API void* spb_stream(spb_ctx* ctx);
  *    NVLink with the copy engines (CUDA IPC), applies the optimizer and the
  *    other ranks pull the updated fp32 shard back, synchronised by
  *    epoch-stamped device flags (no NCCL in the step);
- *  - "sub" (default for other rank counts, e.g. 8 = one SPB worker per GPU):
+ *  - "sub" (default for a ConvNet over a non-power-of-two rank count, and
+ *    above 8 ranks):
  *    NCCL over contributor sub-communicators (ncclCommSplit, one per distinct
  *    contributor-rank set): a layer's gradient is reduce-scattered among the
  *    ranks hosting one of its contributing workers ONLY, each of them updates
  *    its shard, and every member broadcasts its updated fp32 shard to all
  *    ranks (a sole contributor updates the whole layer);
- *  - "rh" (power-of-two rank counts; default for the ConvNet at 4 ranks): the p2p protocol's buffers with
+ *  - "rh" (power-of-two rank counts; the ConvNet's default at 4 and 8 ranks): the p2p protocol's buffers with
  *    Rabenseifner's schedule -- recursive-halving reduce-scatter, the owner's
  *    update, recursive-doubling all-gather of the fp32 weights -- so every
  *    copy-engine pull is from ONE peer (single-peer NVLink copies run at
  *    ~760 GB/s, all-to-all pulls at ~450 GB/s);
- *  - "push" (MLP; default at 4 ranks): the wgrad GEMM epilogue stores each
+ *  - "push" (MLP; default from 3 to 8 ranks, e.g. 8 = one SPB worker per GPU):
+ *    the wgrad GEMM epilogue stores each
  *    gradient row straight into the owning rank's staging slot (NVLink
  *    stores through CUDA IPC, staged through shared memory into 128-byte row
  *    segments); the owner sums its rows and applies the optimizer; the peers

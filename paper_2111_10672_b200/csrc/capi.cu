@@ -565,14 +565,18 @@ spb_status spb_comm_init(spb_ctx* ctx, const void* unique_id128, int rank, int n
     e.ensure_rows(static_cast<int>(e.workers.size()) * e.bw);
     // Aggregation mode: SPB_COMM = rh | p2p | sub | push.
     // Default by measurement (cfg3): p2p for 2 ranks (one
-    // pairwise copy-engine exchange); push for 4 ranks (gradient rows stored
-    // to their owners by the wgrad epilogue: 4.47 ms vs rh 5.02, p2p 5.2,
-    // nccl 5.09 on one box), rh for the ConvNet there (push is MLP-only);
-    // sub elsewhere -- NCCL over contributor sub-communicators, parity-tested
-    // at 2 and 4 ranks (8 ranks could not be measured: gpurun offers 4 GPUs).
+    // pairwise copy-engine exchange); push from 3 to 8 ranks for the MLP
+    // (gradient rows stored to their owners by the wgrad epilogue: 4.47 ms
+    // vs rh 5.02, p2p 5.2, sub 6.6 at 4 ranks), rh for the ConvNet at a
+    // power of two (push is MLP-only); sub otherwise -- NCCL over
+    // contributor sub-communicators. Every mode is parity-tested at 2 and 4
+    // ranks; 8 ranks could not be run here (gpurun offers at most 4 GPUs).
     const char* cm = std::getenv("SPB_COMM");
+    const bool pow2 = (nranks & (nranks - 1)) == 0;
     const std::string mode =
-        cm ? cm : (nranks == 2 ? "p2p" : (nranks == 4 ? (e.conv_model ? "rh" : "push") : "sub"));
+        cm ? cm
+           : (nranks == 2 ? "p2p"
+                          : (e.conv_model ? (pow2 ? "rh" : "sub") : (nranks <= spb::kMaxPeers ? "push" : "sub")));
     if (mode != "p2p" && mode != "sub" && mode != "push" && mode != "rh")
       throw spb::ArgumentError("comm: SPB_COMM must be rh, push, p2p or sub");
     // NCCL's kernels need SMs while the backward GEMMs run: keep some free

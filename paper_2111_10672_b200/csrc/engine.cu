@@ -547,7 +547,10 @@ int Engine::enqueue_pass(int rows, const std::vector<int>& row0, const std::vect
       ep.splitk_ws = splitk_ws;
       ep.splitk_ws_floats = kSplitkWsFloats;
       pbeg(s);
-      n += gemm_tf32x3(A, B, kEpiDgradTanh, ep, s);
+      {
+        SmReserve part(two && dgrad_sms > 0 ? std::max(reserved_sms, sm_total() - dgrad_sms) : reserved_sms);
+        n += gemm_tf32x3(A, B, kEpiDgradTanh, ep, s);
+      }
       pend(kClsDgrad, 2.0 * qn * w[l] * w[l - 1], s);
     }
     if (two) {
@@ -582,7 +585,10 @@ int Engine::enqueue_pass(int rows, const std::vector<int>& row0, const std::vect
         if (route_push) push_route(l, ep);  // rows stored straight to their owners
       }
       pbeg(sw);
-      n += gemm_tf32x3(A, B, lf(l) ? kEpiWgradUpdate : kEpiStoreScaled, ep, sw);
+      {
+        SmReserve part(two && wgrad_sms > 0 ? std::max(reserved_sms, sm_total() - wgrad_sms) : reserved_sms);
+        n += gemm_tf32x3(A, B, lf(l) ? kEpiWgradUpdate : kEpiStoreScaled, ep, sw);
+      }
       pend(kClsWgrad, 2.0 * cnt * w[l] * w[l - 1], sw);
     }
     if (two) SPB_CUDA(cudaEventRecord(ev_wgrad(l), s2));

@@ -203,6 +203,23 @@ struct Engine {
   // SMs the persistent GEMMs of this context leave free (spb_comm_init: 16
   // with NCCL collectives in the step, 0 for the copy-engine modes).
   int reserved_sms = 0;
+  // SM partition of the concurrent backward (A/B knob, 0 = off): persistent
+  // grids of the dgrad chain (stream s) and of the wgrads (s2) capped at
+  // SPB_DGRAD_SMS / SPB_WGRAD_SMS SMs, so the two streams (and the exchange
+  // kernels beside them) share the SMs by partition instead of by whichever
+  // CTAs the scheduler places first.
+  int dgrad_sms = env_int("SPB_DGRAD_SMS");
+  int wgrad_sms = env_int("SPB_WGRAD_SMS");
+  static int env_int(const char* name) {
+    const char* v = std::getenv(name);
+    return v ? std::max(0, std::atoi(v)) : 0;
+  }
+  static int sm_total() {
+    int dev = 0, n = 0;
+    SPB_CUDA(cudaGetDevice(&dev));
+    SPB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    return n;
+  }
   // p2p mode: fp32 weights (own shards published to the peers), epoch-stamped
   // flags [2 * (L + 1)][nranks], gradient staging [2][nranks - 1][shard], and
   // the peers' IPC-mapped grad / w32 / flags.
