@@ -501,6 +501,7 @@ int Engine::enqueue_pass(int rows, const std::vector<int>& row0, const std::vect
     SPB_CUDA(cudaStreamWaitEvent(s2, ev(kEvFork), 0));
   }
   cudaStream_t sw = two ? s2 : s;
+  const int dsms = part_sms(dgrad_sms, 68), wsms = part_sms(wgrad_sms, 72);
   // Head gradients over the contributor rows of layer L: one wgrad GEMM,
   // alpha_L delta_L^T [H_{L-1} | 1] (weights and bias; never fused with the
   // optimizer -- enqueue_step keeps layer L unfused).
@@ -548,7 +549,7 @@ int Engine::enqueue_pass(int rows, const std::vector<int>& row0, const std::vect
       ep.splitk_ws_floats = kSplitkWsFloats;
       pbeg(s);
       {
-        SmReserve part(two && dgrad_sms > 0 ? std::max(reserved_sms, sm_total() - dgrad_sms) : reserved_sms);
+        SmReserve part(two && dsms > 0 ? std::max(reserved_sms, sm_total() - dsms) : reserved_sms);
         n += gemm_tf32x3(A, B, kEpiDgradTanh, ep, s);
       }
       pend(kClsDgrad, 2.0 * qn * w[l] * w[l - 1], s);
@@ -586,7 +587,7 @@ int Engine::enqueue_pass(int rows, const std::vector<int>& row0, const std::vect
       }
       pbeg(sw);
       {
-        SmReserve part(two && wgrad_sms > 0 ? std::max(reserved_sms, sm_total() - wgrad_sms) : reserved_sms);
+        SmReserve part(two && wsms > 0 ? std::max(reserved_sms, sm_total() - wsms) : reserved_sms);
         n += gemm_tf32x3(A, B, lf(l) ? kEpiWgradUpdate : kEpiStoreScaled, ep, sw);
       }
       pend(kClsWgrad, 2.0 * cnt * w[l] * w[l - 1], sw);

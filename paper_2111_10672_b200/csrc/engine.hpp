@@ -203,17 +203,20 @@ struct Engine {
   // SMs the persistent GEMMs of this context leave free (spb_comm_init: 16
   // with NCCL collectives in the step, 0 for the copy-engine modes).
   int reserved_sms = 0;
-  // SM partition of the concurrent backward (A/B knob, 0 = off): persistent
-  // grids of the dgrad chain (stream s) and of the wgrads (s2) capped at
-  // SPB_DGRAD_SMS / SPB_WGRAD_SMS SMs, so the two streams (and the exchange
-  // kernels beside them) share the SMs by partition instead of by whichever
-  // CTAs the scheduler places first.
-  int dgrad_sms = env_int("SPB_DGRAD_SMS");
-  int wgrad_sms = env_int("SPB_WGRAD_SMS");
-  static int env_int(const char* name) {
+  // SM partition of the concurrent backward: persistent grids of the dgrad
+  // chain (stream s) and of the wgrads (s2) capped at these SM counts, so
+  // the two streams (and the exchange kernels beside them) share the SMs by
+  // partition instead of by whichever CTAs the scheduler places first.
+  // -1 = automatic: 68 / 72 with a multi-GPU exchange (measured 4.5 -> 4.28
+  // ms at 4 ranks, 4.50 -> 4.31 at 2), off on one GPU (there it costs 3-6 %);
+  // SPB_DGRAD_SMS / SPB_WGRAD_SMS override (0 = off).
+  int dgrad_sms = env_int("SPB_DGRAD_SMS", -1);
+  int wgrad_sms = env_int("SPB_WGRAD_SMS", -1);
+  static int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
-    return v ? std::max(0, std::atoi(v)) : 0;
+    return v ? std::max(0, std::atoi(v)) : dflt;
   }
+  int part_sms(int v, int dflt) const { return v >= 0 ? v : (comm && nranks > 1 ? dflt : 0); }
   static int sm_total() {
     int dev = 0, n = 0;
     SPB_CUDA(cudaGetDevice(&dev));
