@@ -169,6 +169,116 @@ __global__ void conv_flip_kernel(const float* __restrict__ w_hi, const float* __
   }
 }
 
+// Direct 3x3 convolution of a narrow input (c_in <= 4, stored 4-wide: the RGB
+// layer), the forward of a layer whose im2col GEMM would have K = 27: one
+// thread per output pixel computes all c_out (<= kDirectMaxOut) channels in
+// fp32 FMAs over the 9 taps x c_in inputs, with x = hi + lo and w = hi + lo
+// (both exact), then bias + tanh + split like the GEMM's forward epilogue.
+// The 9 taps are loaded up front (18 independent 16-byte loads); the weights
+// sit in shared memory tap-major ([9 * 4][c_out]) and are read as warp-wide
+// broadcasts; each warp stages its 32 output rows in shared memory so the
+// stores are contiguous 512-byte runs. Memory-bound on the split output
+// (8 B per output element), where the im2col GEMM wrote 9 c_in columns first
+// and then ran a K = 32 GEMM at a few % of the tensor peak.
+constexpr int kDirectMaxOut = 64;
+constexpr int kDirectThreads = 128;
+constexpr int kDirectPad = kDirectMaxOut + 4;  // staging row stride (floats)
+
+template <int CIN>
+__global__ void __launch_bounds__(kDirectThreads, 3) conv_direct_fwd_kernel(
+    const float* __restrict__ in_hi, const float* __restrict__ in_lo, long ldin, ConvGeom g, long rows,
+    const float* __restrict__ w_hi, const float* __restrict__ w_lo, long ldw, const float* __restrict__ b_hi,
+    const float* __restrict__ b_lo, float* __restrict__ o_hi, float* __restrict__ o_lo, long ldo) {
+  // [36][kDirectMaxOut] weights (tap * 4 + c; zero for c >= c_in), [kDirectMaxOut] bias,
+  // then per warp a [32][kDirectPad] staging tile.
+  extern __shared__ __align__(16) float ws[];
+  float* bias = ws + 36 * kDirectMaxOut;
+  const int C = g.c_out;
+  for (int i = threadIdx.x; i < 36 * kDirectMaxOut; i += blockDim.x) {
+    const int k = i / kDirectMaxOut, co = i - k * kDirectMaxOut;
+    const int tap = k >> 2, c = k & 3;
+    const long at = static_cast<long>(co) * ldw + tap * g.c_in + c;
+    ws[i] = (co < C && c < g.c_in) ? w_hi[at] + w_lo[at] : 0.f;
+  }
+  for (int co = threadIdx.x; co < kDirectMaxOut; co += blockDim.x) bias[co] = co < C ? b_hi[co] + b_lo[co] : 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* stage = bias + kDirectMaxOut + warp * 32 * kDirectPad;
+  const int opix = g.out_h * g.out_w;
+  const long step = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long base = static_cast<long>(blockIdx.x) * blockDim.x + warp * 32; base < rows; base += step) {
+    const long r = base + lane;
+    const bool live = r < rows;
+    float x[9 * CIN];
+    {
+      const long s = live ? r / opix : 0;
+      const int rem = live ? static_cast<int>(r - s * opix) : 0;
+      const int oy = rem / g.out_w, ox = rem - oy * g.out_w;
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap) {
+        const int iy = oy * g.stride + tap / 3 - 1, ix = ox * g.stride + tap % 3 - 1;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (live && iy >= 0 && iy < g.in_h && ix >= 0 && ix < g.in_w) {  // else zero padding
+          const long src = ((s * g.in_h + iy) * g.in_w + ix) * ldin;
+          const float4 h = *reinterpret_cast<const float4*>(in_hi + src);
+          const float4 l = *reinterpret_cast<const float4*>(in_lo + src);
+          v = make_float4(h.x + l.x, h.y + l.y, h.z + l.z, h.w + l.w);
+        }
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int c = 0; c < CIN; ++c) x[tap * CIN + c] = vv[c];
+      }
+    }
+    float acc[kDirectMaxOut];
+#pragma unroll
+    for (int j = 0; j < kDirectMaxOut; ++j) acc[j] = bias[j];
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap) {
+#pragma unroll
+      for (int c = 0; c < CIN; ++c) {  // the 4th (padding) channel of an RGB input is skipped
+        const float xc = x[tap * CIN + c];
+        const float* wk = ws + (tap * 4 + c) * kDirectMaxOut;
+#pragma unroll
+        for (int j = 0; j < kDirectMaxOut; j += 4) {
+          const float4 w4 = *reinterpret_cast<const float4*>(wk + j);
+          acc[j] = fmaf(xc, w4.x, acc[j]);
+          acc[j + 1] = fmaf(xc, w4.y, acc[j + 1]);
+          acc[j + 2] = fmaf(xc, w4.z, acc[j + 2]);
+          acc[j + 3] = fmaf(xc, w4.w, acc[j + 3]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kDirectMaxOut; ++j) acc[j] = tanhf(acc[j]);
+    // hi then lo through the staging tile: lane-row writes, then the warp
+    // stores its 32 rows x C channels as contiguous float4 runs.
+    const int n = static_cast<int>(rows - base < 32 ? rows - base : 32);
+    const int cv = C / 4;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+#pragma unroll
+      for (int j = 0; j < kDirectMaxOut; j += 4) {
+        float4 v;
+        float* vp = &v.x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float h = tf32r(acc[j + q]);
+          vp[q] = half == 0 ? h : acc[j + q] - h;
+        }
+        *reinterpret_cast<float4*>(stage + lane * kDirectPad + j) = v;
+      }
+      __syncwarp();
+      float* out = half == 0 ? o_hi : o_lo;
+      for (int e = lane; e < n * cv; e += 32) {
+        const int row = e / cv, q = e - row * cv;
+        *reinterpret_cast<float4*>(out + (base + row) * ldo + 4 * q) =
+            *reinterpret_cast<const float4*>(stage + row * kDirectPad + 4 * q);
+      }
+      __syncwarp();
+    }
+  }
+}
+
 int flat_grid(long total) { return static_cast<int>(std::max<long>(1, std::min<long>((total + 255) / 256, 148L * 16))); }
 
 // pooled[s, c] = mean over the pix pixel rows of sample s (split pair out).
@@ -229,6 +339,27 @@ void launch_im2col(const float* in_hi, const float* in_lo, long ldin, const Conv
   else
     im2col_kernel<1><<<flat_grid(static_cast<long>(rows) * 9 * g.c_in), 256, 0, s>>>(in_hi, in_lo, ldin, g, row0, rows,
                                                                                    col_hi, col_lo, ldk);
+  SPB_CUDA(cudaGetLastError());
+}
+
+bool conv_direct_ok(const ConvGeom& g, long ldin, long ldo) {
+  return g.c_in <= 4 && ldin == 4 && g.c_out <= kDirectMaxOut && g.c_out % 4 == 0 && ldo % 4 == 0;
+}
+
+void launch_conv_direct_fwd(const float* in_hi, const float* in_lo, long ldin, const ConvGeom& g, long rows,
+                            const float* w_hi, const float* w_lo, long ldw, const float* b_hi, const float* b_lo,
+                            float* o_hi, float* o_lo, long ldo, cudaStream_t s) {
+  if (rows <= 0) return;
+  if (!conv_direct_ok(g, ldin, ldo)) throw std::invalid_argument("conv_direct_fwd: unsupported geometry");
+  const int smem = static_cast<int>((37 * kDirectMaxOut + (kDirectThreads / 32) * 32 * kDirectPad) * sizeof(float));
+  static_assert((37 * kDirectMaxOut + (kDirectThreads / 32) * 32 * kDirectPad) * sizeof(float) <= 48 * 1024,
+                "conv_direct_fwd: static shared-memory budget");
+  const int grid = static_cast<int>(std::max<long>(1, std::min<long>((rows + kDirectThreads - 1) / kDirectThreads,
+                                                                     148L * 3)));
+  auto kern = g.c_in == 3 ? conv_direct_fwd_kernel<3>
+                          : (g.c_in == 4 ? conv_direct_fwd_kernel<4>
+                                         : (g.c_in == 2 ? conv_direct_fwd_kernel<2> : conv_direct_fwd_kernel<1>));
+  kern<<<grid, kDirectThreads, smem, s>>>(in_hi, in_lo, ldin, g, rows, w_hi, w_lo, ldw, b_hi, b_lo, o_hi, o_lo, ldo);
   SPB_CUDA(cudaGetLastError());
 }
 

@@ -20,6 +20,12 @@ void launch_conv_gather(const float* X, long ldx, const float* Y, int pix, int c
 // col rows [row0, row0 + rows) (output pixels) from the input split pair.
 void launch_im2col(const float* in_hi, const float* in_lo, long ldin, const ConvGeom& g, int row0, int rows,
                    float* col_hi, float* col_lo, long ldk, cudaStream_t s);
+// Direct forward (bias + tanh + split) of a narrow-input convolution (the RGB
+// layer): output pixel rows [0, rows). conv_direct_ok: the geometries it takes.
+bool conv_direct_ok(const ConvGeom& g, long ldin, long ldo);
+void launch_conv_direct_fwd(const float* in_hi, const float* in_lo, long ldin, const ConvGeom& g, long rows,
+                            const float* w_hi, const float* w_lo, long ldw, const float* b_hi, const float* b_lo,
+                            float* o_hi, float* o_lo, long ldo, cudaStream_t s);
 // Delta of the layer below for input pixel rows [row0, row0 + rows).
 void launch_col2im_tanh(const float* dcol, long ldk, const ConvGeom& g, int row0, int rows, const float* h_hi,
                         const float* h_lo, long ldh, float* d_hi, float* d_lo, long ldd, cudaStream_t s);

@@ -104,7 +104,7 @@ void Engine::release() {
     if (p) cudaFree(p);
   };
   f(splitk_ws);
-  f(splitk_ws2), f(colsum_ws), f(colsum_cnt);
+  f(splitk_ws2), f(splitk_ws3), f(colsum_ws), f(colsum_cnt);
   f(p64);
   f(p_hi), f(p_lo), f(grad), f(mom), f(X), f(Y), f(delta), f(delta_lo), f(row_loss), f(ybatch), f(xin), f(idx),
       f(idx_in), f(loss_dev), f(tmp), f(ctl), f(workers_dev), f(epoch_dev), f(bar_dev), f(w32), f(flags),
@@ -219,6 +219,7 @@ void Engine::allocate_params() {
   tmp = alloc<float>(tmp_n);
   splitk_ws = alloc<float>(kSplitkWsFloats);
   splitk_ws2 = alloc<float>(kSplitkWs2Floats);
+  if (conv_model) splitk_ws3 = alloc<float>(kConvWsFloats);  // the conv wgrads' split-K (gradient stream)
   colsum_ws = alloc<float>(kColsumWsFloats);
   colsum_cnt = alloc<int>(kColsumCounters);
   ctl = alloc<Ctl>(1);
@@ -323,6 +324,14 @@ int Engine::enqueue_pass_conv(int samples, const std::vector<int>& row0, const s
     fwd_gate(l, s);
     const int M = static_cast<int>(samples * pix[l]);
     const bool tma = conv_tma(l);
+    if (conv_direct(l)) {
+      pbeg(s);
+      launch_conv_direct_fwd(Hh[l - 1], Hl[l - 1], ld[l - 1], cg[l], M, p_hi + w_off[l], p_lo + w_off[l], ldf[l],
+                             p_hi + b_off[l], p_lo + b_off[l], Hh[l], Hl[l], ld[l], s);
+      pend(kClsFwd, 2.0 * M * w[l] * fan[l], s);
+      ++n;
+      continue;
+    }
     if (!tma) {
       pbeg(s);
       launch_im2col(Hh[l - 1], Hl[l - 1], ld[l - 1], cg[l], 0, M, Ch[l], Cl[l], ldf[l], s);
@@ -372,11 +381,23 @@ int Engine::enqueue_pass_conv(int samples, const std::vector<int>& row0, const s
                        Dh[Lc % kDbuf], Dl[Lc % kDbuf], ld[Lc], s);
     ++n;
   }
+  // Two streams, as in the MLP pass: the Delta chain (dgrads) on s, the
+  // wgrads (+ the RGB layer's column gather) on s2 with their own split-K
+  // workspace; Delta is triple-buffered, so dgrad_l waits for wgrad_{l+2}.
+  const bool two = concurrent;
+  cudaStream_t sw = two ? s2 : s;
+  float* wws = splitk_ws3;  // (used by the wgrads only, on whichever stream they run)
+  // SM partition of the two streams: off by default for the ConvNet (A/B knob).
+  const int dsms = part_sms(dgrad_sms, 0), wsms = part_sms(wgrad_sms, 0);
+  auto ev_delta = [&](int q) { return ev(kEvLayer + 2 * q); };     // Delta_q ready (on s)
+  auto ev_wgrad = [&](int q) { return ev(kEvLayer + 2 * q + 1); }; // wgrad_q done (on s2)
+  if (two) SPB_CUDA(cudaEventRecord(ev_delta(Lc), s));
   int l = Lc;
   for (; l >= 1; --l) {
     if (row0[l] >= samples) break;
     const int b = l % kDbuf, bn = (l - 1) % kDbuf;
     const long r0 = row0[l] * pix[l], cnt = (samples - row0[l]) * pix[l];
+    if (two && l > 1 && row0[l - 1] < samples && l + 2 <= Lc) SPB_CUDA(cudaStreamWaitEvent(s, ev_wgrad(l + 2), 0));
     if (l > 1 && row0[l - 1] < samples && conv_tma_dgrad(l)) {
       // Delta_{l-1} = conv(Delta_l, flipped W_l) * (1 - H_{l-1}^2), rows of the continuing samples.
       const long q0 = row0[l - 1] * pix[l - 1], qn = (samples - row0[l - 1]) * pix[l - 1];
@@ -395,6 +416,7 @@ int Engine::enqueue_pass_conv(int samples, const std::vector<int>& row0, const s
       ep.ld_h = ld[l - 1];
       ep.M = static_cast<int>(qn);
       ep.N = w[l - 1];
+      SmReserve part(two && dsms > 0 ? std::max(reserved_sms, sm_total() - dsms) : reserved_sms);
       n += 1 + gemm_conv_dgrad(src, q0, static_cast<int>(qn), B, ep, s);
       pend(kClsDgrad, 2.0 * qn * w[l] * fan[l], s);
     } else if (l > 1 && row0[l - 1] < samples) {  // dgrad into columns, then col2im * (1 - H^2)
@@ -410,13 +432,27 @@ int Engine::enqueue_pass_conv(int samples, const std::vector<int>& row0, const s
       ep.splitk_ws = splitk_ws;
       ep.splitk_ws_floats = kSplitkWsFloats;
       pbeg(s);
-      n += gemm_tf32x3(A, B, kEpiStoreScaled, ep, s);
+      {
+        SmReserve part(two && dsms > 0 ? std::max(reserved_sms, sm_total() - dsms) : reserved_sms);
+        n += gemm_tf32x3(A, B, kEpiStoreScaled, ep, s);
+      }
       pend(kClsDgrad, 2.0 * qn * w[l] * fan[l], s);
       pbeg(s);
       launch_col2im_tanh(dcol, ldf[l], cg[l], static_cast<int>(row0[l - 1] * pix[l - 1]),
                          static_cast<int>((samples - row0[l - 1]) * pix[l - 1]), Hh[l - 1], Hl[l - 1], ld[l - 1],
                          Dh[bn], Dl[bn], ld[l - 1], s);
       pend(kClsDgrad, 0, s);  // the gather half of the stride-2 dgrad
+      ++n;
+    }
+    if (two) {  // Delta_{l-1} ready / dgrad_l (last reader of W_l) done; wgrad_l needs Delta_l
+      SPB_CUDA(cudaEventRecord(ev_delta(l - 1), s));
+      SPB_CUDA(cudaStreamWaitEvent(s2, ev_delta(l), 0));
+    }
+    if (conv_direct(l)) {  // the direct forward left no columns: those of the contributor samples
+      pbeg(sw);
+      launch_im2col(Hh[l - 1], Hl[l - 1], ld[l - 1], cg[l], static_cast<int>(r0), static_cast<int>(cnt), Ch[l], Cl[l],
+                    ldf[l], sw);
+      pend(kClsGather, 0, sw);
       ++n;
     }
     {  // wgrad + bias: [dW_l | db_l] = alpha_l * Delta_l[r0:]^T [col_l[r0:] | 1]
@@ -434,19 +470,25 @@ int Engine::enqueue_pass_conv(int samples, const std::vector<int>& row0, const s
       ep.bias_col_p1 = ep.ones_col_p1 = bc + 1;
       ep.gb_hi = grad + b_off[l];
       ep.colsum_ws = colsum_ws, ep.colsum_cnt = colsum_cnt;
-      ep.splitk_ws = splitk_ws;  // few output tiles, K = pixel rows: split K (single stream)
-      ep.splitk_ws_floats = kSplitkWsFloats;
-      pbeg(s);
+      ep.splitk_ws = wws;  // few output tiles, K = pixel rows: split K
+      ep.splitk_ws_floats = kConvWsFloats;
+      pbeg(sw);
+      SmReserve part(two && wsms > 0 ? std::max(reserved_sms, sm_total() - wsms) : reserved_sms);
       if (tma) {
         ConvSrc src{Hh[l - 1], Hl[l - 1], ld[l - 1], samples, cg[l]};
-        n += gemm_conv_wgrad(A, src, r0, ep, s);
+        n += gemm_conv_wgrad(A, src, r0, ep, sw);
       } else {
-        n += gemm_tf32x3(A, B, kEpiStoreScaled, ep, s);
+        n += gemm_tf32x3(A, B, kEpiStoreScaled, ep, sw);
       }
-      pend(kClsWgrad, 2.0 * cnt * w[l] * fan[l], s);
+      pend(kClsWgrad, 2.0 * cnt * w[l] * fan[l], sw);
     }
-    if (on_grad) n += on_grad(l, s);
-    if (on_layer) on_layer(l, s);
+    if (two) SPB_CUDA(cudaEventRecord(ev_wgrad(l), s2));
+    if (on_grad) n += on_grad(l, sw);
+    if (on_layer) on_layer(l, sw);  // grad of layer l final on sw; dgrad_l (last W_l reader) done on s
+  }
+  if (two) {  // join the gradient stream
+    SPB_CUDA(cudaEventRecord(ev(kEvJoin), s2));
+    SPB_CUDA(cudaStreamWaitEvent(s, ev(kEvJoin), 0));
   }
   for (; l >= 1 && on_grad; --l) {
     n += on_grad(l, s);

@@ -135,6 +135,9 @@ struct Engine {
   long tmp_n = 0;
   float* splitk_ws = nullptr;  // split-K partials (forward / dgrad GEMMs, stream s only)
   static constexpr long kSplitkWsFloats = 16L << 20;
+  float* splitk_ws3 = nullptr;  // ConvNet: split-K partials of the wgrads (gradient stream s2)
+  // 256 MB: room for ~30-60 K-splits of the widest conv wgrads (M = 512, N = 4609)
+  static constexpr long kConvWsFloats = 64L << 20;
   float* splitk_ws2 = nullptr;  // split-K partials of the head wgrad (the gradient stream s2)
   // Column-sum bias slices + counters of the 1-CTA wgrads (GemmEpilogue::
   // colsum_ws): the wgrads run in stream order (s2, or s for the ConvNet).
@@ -395,6 +398,17 @@ struct Engine {
   bool conv_tma(int l) const {
     static const bool off = std::getenv("SPB_CONV_IM2COL") != nullptr;  // A/B experiments: materialise columns
     return !off && cg[l].c_in % 32 == 0 && ld[l - 1] % 32 == 0;
+  }
+
+  // Forward of convolution l as a direct fp32 kernel (the RGB layer: c_in <=
+  // 4); its wgrad materialises the im2col columns of the contributor samples
+  // only, in the backward. SPB_CONV_DIRECT=0: the im2col GEMM forward (A/B).
+  bool conv_direct(int l) const {
+    static const bool off = [] {
+      const char* v = std::getenv("SPB_CONV_DIRECT");
+      return v && std::string(v) == "0";
+    }();
+    return !off && !conv_tma(l) && conv_direct_ok(cg[l], ld[l - 1], ld[l]);
   }
 
   // Gathers `rows` samples (ChainMlp: rows; ConvNet: pixel rows of the

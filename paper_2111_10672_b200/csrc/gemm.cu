@@ -413,13 +413,25 @@ Plan plan_gemm(int M, int N, int K, long ws_floats, bool can_split, bool narrow_
   // Split counts: up to 8 for the MLP shapes; far more for the few-tile,
   // huge-K wgrad GEMMs of the conv model (K = pixel rows, up to ~1M).
   static const int kSplits[] = {1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 32, 48, 64, 96, 128, 148, 192, 256, 296};
-  for (int sp : kSplits) {
-    if (!split_ok(sp)) break;
+  auto try_split = [&](int sp) {
     const int kbs = (kb + sp - 1) / sp, eff = (kb + kbs - 1) / kbs;
     const long units = t1 * eff;
     const double t =
         static_cast<double>((units + sms - 1) / sms) * ((N <= 64 && sp == 1 ? 0.31 : 0.638) * kbs + 1.41) + fixup(eff);
     if (t < best_t) best_t = t, best = {false, sp, 256};
+  };
+  // Few output tiles over a huge K (the conv wgrads: K = pixel rows): every
+  // split count, so that tiles x splits can land just under a whole number
+  // of waves (38 tiles: 35 splits = 8.99 waves, where the list's 32 / 48 fill
+  // 8.2 / 12.3); the MLP shapes keep the fitted list.
+  const bool fine = t1 < sms / 2 && kb >= 512;
+  for (int sp : kSplits) {
+    if (!split_ok(sp)) break;
+    try_split(sp);
+  }
+  for (int sp = 9; fine && sp <= 296; ++sp) {
+    if (!split_ok(sp)) break;
+    try_split(sp);
   }
   const int pairs = sms / 2;
   for (int pn : kPairNs) {
