@@ -381,10 +381,13 @@ int Engine::enqueue_pass_conv(int samples, const std::vector<int>& row0, const s
                        Dh[Lc % kDbuf], Dl[Lc % kDbuf], ld[Lc], s);
     ++n;
   }
-  // Two streams, as in the MLP pass: the Delta chain (dgrads) on s, the
-  // wgrads (+ the RGB layer's column gather) on s2 with their own split-K
-  // workspace; Delta is triple-buffered, so dgrad_l waits for wgrad_{l+2}.
-  const bool two = concurrent;
+  // Two streams on one GPU, as in the MLP pass: the Delta chain (dgrads) on
+  // s, the wgrads (+ the RGB layer's column gather) on s2 with their own
+  // split-K workspace; Delta is triple-buffered, so dgrad_l waits for
+  // wgrad_{l+2}. With a multi-GPU exchange the conv backward stays on one
+  // stream: the exchange's flag-wait kernels beside two persistent GEMM grids
+  // whose CTAs fill an SM's register file can starve a grid of its last CTA.
+  const bool two = concurrent && !(comm && nranks > 1);
   cudaStream_t sw = two ? s2 : s;
   float* wws = splitk_ws3;  // (used by the wgrads only, on whichever stream they run)
   // SM partition of the two streams: off by default for the ConvNet (A/B knob).
