@@ -644,6 +644,10 @@ spb_status spb_profile_step(spb_ctx* ctx, uint64_t seed, int step, int full_back
     SPB_CUDA(cudaEventCreate(&b));
     e.prof = &recs;
     e.concurrent = false;  // serialise so each launch's events time it alone
+    // 5 ms head start: the whole step is enqueued before the GPU reaches it
+    // (the step enqueues in ~1 ms), so no launch's events include a wait for
+    // the host to submit it.
+    spb::launch_spin(5'000'000, e.st);
     SPB_CUDA(cudaEventRecord(a, e.st));
     try {
       e.enqueue_step(full_backprop != 0, false, e.st);

@@ -377,6 +377,21 @@ void launch_stamp(unsigned long long* slot, cudaStream_t s) {
   SPB_CUDA(cudaGetLastError());
 }
 
+// One thread idles on the stream for ns nanoseconds (%globaltimer).
+__global__ void spin_kernel(long long ns) {
+  long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(2000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+void launch_spin(long long ns, cudaStream_t s) {
+  spin_kernel<<<1, 1, 0, s>>>(ns);
+  SPB_CUDA(cudaGetLastError());
+}
+
 void launch_sum_loss(const float* row_loss, int rows, float scale, float* out, int* step_dev, cudaStream_t s) {
   sum_loss_kernel<<<1, 1024, 0, s>>>(row_loss, rows, scale, out, step_dev);
   SPB_CUDA(cudaGetLastError());

@@ -130,5 +130,9 @@ void launch_loss64(const float* X, long ldx, const float* Y, const int* idx, int
                    double* row_loss, cudaStream_t s);
 // One thread writes %globaltimer (ns) to *slot (timeline tracing).
 void launch_stamp(unsigned long long* slot, cudaStream_t s);
+// One thread idles the stream for ns nanoseconds: gives the host a head start
+// to enqueue a whole eager step before the GPU reaches it (spb_profile_step),
+// so per-launch event timings carry no host-submission gaps.
+void launch_spin(long long ns, cudaStream_t s);
 
 }  // namespace spb
