@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -176,16 +177,28 @@ CUtensorMap ones_map() {
   return tmap2d(ones_buffer(), 32, 64, 32, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
+// The dynamic shared-memory opt-in of a kernel, once per (kernel, device):
+// a function attribute belongs to the device's context, so a process driving
+// contexts on several GPUs must set it on each.
+template <class K>
+void configure_smem(K* kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  SPB_CUDA(cudaGetDevice(&dev));
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(key)) return;
+  SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert(key);
+}
+
 template <int BN, bool AM, bool BM_, int EPI, bool TMA_UPD = false, int IC = 0>
 void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, int splits = 1,
                  const CUtensorMap* ic_a = nullptr, const CUtensorMap* ic_b = nullptr, ConvTmaArgs ic = {}) {
   auto kern = gemm_tf32x3_kernel<BN, AM, BM_, EPI, TMA_UPD, IC>;
   constexpr int smem = GemmCfg<BN, TMA_UPD>::kSmem;
-  static bool configured = false;
-  if (!configured) {
-    SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
+  configure_smem(kern, smem);
   // IC == 1: A comes from ic_a[0..1] (im2col hi / lo); IC == 2: B from ic_b.
   CUtensorMap ah = IC == 1 ? ic_a[0] : operand_map(A, A.hi, kBM), al = IC == 1 ? ic_a[1] : operand_map(A, A.lo, kBM);
   CUtensorMap bh = IC == 2 ? ic_b[0] : operand_map(B, B.hi, BN), bl = IC == 2 ? ic_b[1] : operand_map(B, B.lo, BN);
@@ -223,11 +236,7 @@ void launch_2sm_pn(const Operand& A, const Operand& B, const GemmEpilogue& ep, c
                    const CUtensorMap* ic_a = nullptr, ConvTmaArgs ic = {}) {
   using Cfg = Gemm2smCfg<PN>;
   auto kern = gemm_tf32x3_2sm_kernel<AM, BM_, EPI, PN, IC>;
-  static bool configured = false;
-  if (!configured) {
-    SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
-    configured = true;
-  }
+  configure_smem(kern, Cfg::kSmem);
   CUtensorMap ah = IC == 1 ? ic_a[0] : operand_map(A, A.hi, Cfg::kRowsA);
   CUtensorMap al = IC == 1 ? ic_a[1] : operand_map(A, A.lo, Cfg::kRowsA);
   CUtensorMap bh = operand_map(B, B.hi, Cfg::kRowsB), bl = operand_map(B, B.lo, Cfg::kRowsB);

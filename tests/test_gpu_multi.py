@@ -274,3 +274,32 @@ def test_multi_gpu_one_worker_per_gpu(tmp_path, orc, mode):
             got = outs[r][f"arr_{l}"]
             assert np.linalg.norm(got - P[l]) / np.linalg.norm(P[l]) <= 1e-4
             assert np.array_equal(got, outs[0][f"arr_{l}"])
+
+
+def test_contexts_on_two_devices_in_one_process(orc):
+    """One process driving contexts on two GPUs (the reference's threads
+    each own a model; the drop-in binds a context to the caller's device):
+    per-device kernel attributes and the ones box are set up on each device,
+    and the same SPB steps give bit-identical weights on both, equal to the
+    CPU oracle (1e-4)."""
+    if _gpus() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    from paper_2111_10672_b200 import spb
+
+    X, Y, W = spb.gen_chain_mlp(WIDTHS, N, DSEED)
+    outs = []
+    for dev in (1, 0):  # device 1 first: its kernels are configured before device 0's
+        m = spb.ChainMlp(WIDTHS, X, Y, W, k=K, per_worker_batch=BW, device=dev)
+        try:
+            m.set_optimizer(LR)
+            m.train_steps(SEED, 1, 3)
+            outs.append(m.get_params())
+        finally:
+            m.close()
+    X64, Y64 = X.astype(np.float64), Y.astype(np.float64)
+    P = [b.astype(np.float64) for b in W]
+    for s in range(1, 4):
+        orc.spb_step(WIDTHS, X64, Y64, P, K, K * BW, LR, SEED, s)
+    for l in range(len(WIDTHS) - 1):
+        assert np.array_equal(outs[0][l], outs[1][l])
+        assert np.linalg.norm(outs[0][l] - P[l]) / np.linalg.norm(P[l]) <= 1e-4
