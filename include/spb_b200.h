@@ -132,7 +132,8 @@ SPB_API spb_status spb_set_chain(spb_ctx* ctx, int steps);
  * graph (diagnostic; no reference counterpart): a %globaltimer stamp kernel
  * on the op's stream before and after every op (GEMMs, reductions, updates,
  * exchanges, p2p flag waits). Per op (up to cap): begin / end ns, class
- * (0 fwd, 1 wgrad, 2 dgrad, 3 head, 4 colreduce, 5 update, 6 gather, 7 comm,
+ * (0 fwd, 1 wgrad, 2 dgrad, 3 head, 4 colreduce (unused since the bias joined
+ * the wgrad GEMM), 5 update, 6 gather, 7 comm,
  * 100 wait), stream (0 main, 1 wgrad, 2 update, 3 split, 4 collectives,
  * 10+p / 20+p gradient / weight pulls from peer p), step index in the chain.
  * Parameters advance by `steps` iterations twice (warm-up replay + traced). */
