@@ -381,20 +381,25 @@ int Engine::enqueue_pass_conv(int samples, const std::vector<int>& row0, const s
                        Dh[Lc % kDbuf], Dl[Lc % kDbuf], ld[Lc], s);
     ++n;
   }
-  // Two streams on one GPU, as in the MLP pass: the Delta chain (dgrads) on
-  // s, the wgrads (+ the RGB layer's column gather) on s2 with their own
-  // split-K workspace; Delta is triple-buffered, so dgrad_l waits for
-  // wgrad_{l+2}. With a multi-GPU exchange the conv backward stays on one
-  // stream: the exchange's flag-wait kernels beside two persistent GEMM grids
-  // whose CTAs fill an SM's register file can starve a grid of its last CTA.
-  const bool two = concurrent && !(comm && nranks > 1);
+  // Two streams, as in the MLP pass: the Delta chain (dgrads) on s, the
+  // wgrads (+ the RGB layer's column gather) on s2 with their own split-K
+  // workspace; Delta is triple-buffered, so dgrad_l waits for wgrad_{l+2}.
+  // (SPB_CONV_TWO_STREAM=0: one stream, for A/B.)
+  static const bool one = [] {
+    const char* v = std::getenv("SPB_CONV_TWO_STREAM");
+    return v && std::string(v) == "0";
+  }();
+  const bool two = concurrent && !one;
   cudaStream_t sw = two ? s2 : s;
   float* wws = splitk_ws3;  // (used by the wgrads only, on whichever stream they run)
   // SM partition of the two streams: off by default for the ConvNet (A/B knob).
   const int dsms = part_sms(dgrad_sms, 0), wsms = part_sms(wgrad_sms, 0);
   auto ev_delta = [&](int q) { return ev(kEvLayer + 2 * q); };     // Delta_q ready (on s)
   auto ev_wgrad = [&](int q) { return ev(kEvLayer + 2 * q + 1); }; // wgrad_q done (on s2)
-  if (two) SPB_CUDA(cudaEventRecord(ev_delta(Lc), s));
+  if (two) {  // fork the gradient stream (also when this rank has no rows below the head)
+    SPB_CUDA(cudaEventRecord(ev_delta(Lc), s));
+    SPB_CUDA(cudaStreamWaitEvent(s2, ev_delta(Lc), 0));
+  }
   int l = Lc;
   for (; l >= 1; --l) {
     if (row0[l] >= samples) break;
