@@ -4,7 +4,7 @@ environment set, joins the exchange, and times SPB and full-backprop graph
 steps (CUDA events, max over ranks). Knobs read once per process
 (SPB_PLACEMENT, SPB_COMM_SMS read at comm_init is fine) must not be varied.
 
-    torchrun --nproc-per-node 4 tools/ab_multi.py ROUNDS name=ENV:VAL,ENV:VAL [name=...]
+    torchrun --nproc-per-node 4 tools/ab_multi.py [--conv] ROUNDS name=ENV:VAL,ENV:VAL [name=...]
 """
 import json
 import os
@@ -24,19 +24,30 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
-    rounds = int(sys.argv[1])
+    args = sys.argv[1:]
+    conv = args[0] == "--conv"  # cfg4 (the ConvNet) instead of cfg3
+    if conv:
+        args = args[1:]
+    rounds = int(args[0])
     variants = []
-    for spec in sys.argv[2:]:
+    for spec in args[1:]:
         name, _, envs = spec.partition("=")
         variants.append((name, dict(e.split(":", 1) for e in envs.split(",") if e)))
     widths, k, bw = [4096] * 16 + [1], 8, 128
-    X, Y, W = spb.gen_chain_mlp(widths, 8192, 7)
+    shape, convs = (32, 32, 3), [(64, 1), (64, 1), (128, 2), (128, 1), (256, 2), (256, 1), (512, 2), (512, 1)]
+    if conv:
+        X, Y, W = spb.gen_convnet(shape, convs, 10, 8192, 7)
+    else:
+        X, Y, W = spb.gen_chain_mlp(widths, 8192, 7)
     res = {}
     for r in range(rounds):
         for name, env in variants:
             saved = {key: os.environ.get(key) for key in env}
             os.environ.update(env)
-            m = spb.ChainMlp(widths, X, Y, W, k=k, per_worker_batch=bw, device=local)
+            if conv:
+                m = spb.ConvNet(shape, convs, 10, X, Y, W, k=k, per_worker_batch=bw, device=local)
+            else:
+                m = spb.ChainMlp(widths, X, Y, W, k=k, per_worker_batch=bw, device=local)
             m.comm_init_torch(dist, rank, world)
             m.set_optimizer(0.01, 0.9, 1e-4)
             out = {}
