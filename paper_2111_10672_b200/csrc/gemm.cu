@@ -233,13 +233,14 @@ void launch_inst(const Operand& A, const Operand& B, const GemmEpilogue& ep, cud
 
 template <bool AM, bool BM_, int EPI, int PN, int IC = 0>
 void launch_2sm_pn(const Operand& A, const Operand& B, const GemmEpilogue& ep, cudaStream_t s, int splits = 1,
-                   const CUtensorMap* ic_a = nullptr, ConvTmaArgs ic = {}) {
+                   const CUtensorMap* ic_a = nullptr, ConvTmaArgs ic = {}, const CUtensorMap* ic_b = nullptr) {
   using Cfg = Gemm2smCfg<PN>;
   auto kern = gemm_tf32x3_2sm_kernel<AM, BM_, EPI, PN, IC>;
   configure_smem(kern, Cfg::kSmem);
   CUtensorMap ah = IC == 1 ? ic_a[0] : operand_map(A, A.hi, Cfg::kRowsA);
   CUtensorMap al = IC == 1 ? ic_a[1] : operand_map(A, A.lo, Cfg::kRowsA);
-  CUtensorMap bh = operand_map(B, B.hi, Cfg::kRowsB), bl = operand_map(B, B.lo, Cfg::kRowsB);
+  CUtensorMap bh = IC == 2 ? ic_b[0] : operand_map(B, B.hi, Cfg::kRowsB);
+  CUtensorMap bl = IC == 2 ? ic_b[1] : operand_map(B, B.lo, Cfg::kRowsB);
   const int num_kb = (A.k + kBK - 1) / kBK;
   const int num_m = (A.mn + 255) / 256, num_n = (B.mn + Cfg::kPairN - 1) / Cfg::kPairN;
   const int tiles = num_m * num_n;
@@ -547,6 +548,18 @@ int gemm_conv_dgrad(const ConvSrc& src, long pixel0, int rows, const Operand& B,
   return launch_conv_implicit<kEpiDgradTanh>(A, B, ep, s, a, ic);
 }
 
+// The conv wgrads with >= 256 output channels run on the CTA pair (each CTA
+// loads half of the im2col B columns, the pair shares the 256-row A tile):
+// cfg4 SPB 6.35 -> 5.92 ms, wgrad phase 2.28 -> 1.72 ms on one B200 against
+// the 1-CTA 128 x 128 kernel. SPB_CONV_WGRAD_PAIR=0: the 1-CTA kernel (A/B).
+bool conv_wgrad_pair() {
+  static const bool on = [] {
+    const char* v = std::getenv("SPB_CONV_WGRAD_PAIR");
+    return !(v && std::string(v) == "0");
+  }();
+  return on;
+}
+
 int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const GemmEpilogue& ep, cudaStream_t s) {
   const ConvGeom& g = src.g;
   if (g.c_in % 32 || src.ld % 32) throw std::invalid_argument("gemm_conv_wgrad: c_in and ld must be multiples of 32");
@@ -565,6 +578,42 @@ int gemm_conv_wgrad(const Operand& A, const ConvSrc& src, long pixel0, const Gem
                       im2col_map(src.lo, src, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)};
   const ConvTmaArgs ic{g.out_h * g.out_w, g.out_w, g.stride, g.c_in, pixel0, 0};
   Operand B{nullptr, nullptr, 4, N, A.k, true};  // shape only
+  if (conv_wgrad_pair() && A.mn >= 256 && ep.splitk_ws) {
+    // CTA pair, 256 x 256 tiles (each CTA half of B's columns): over the
+    // huge K the split count is chosen so pair tiles x splits fill whole
+    // waves of the SM pairs (same cost model as plan_gemm's pair branch).
+    const int pairs = num_sms() / 2, kb = (A.k + kBK - 1) / kBK;
+    const int cols = epi_cols(e) > N ? epi_cols(e) : N;
+    const long tiles = static_cast<long>((A.mn + 255) / 256) * ((cols + 255) / 256);
+    const long ldw = round_up(cols, 4), stride = static_cast<long>(A.mn) * ldw;
+    int best_sp = 1;
+    double best_t = 1e300;
+    for (int sp = 1; sp <= 128; ++sp) {
+      if (sp > 1 && (static_cast<long>(sp) * stride > ep.splitk_ws_floats || kb < 8 * sp)) break;
+      const int kbs = (kb + sp - 1) / sp, eff = (kb + kbs - 1) / kbs;
+      const long units = tiles * eff;
+      const double t = static_cast<double>((units + pairs - 1) / pairs) * (1.01 * kbs + 1.01 + 4.24) +
+                       (eff > 1 ? 3.0 + (eff + 2.0) * A.mn * static_cast<double>(cols) * 4.0 / 3.17e6 : 0.0);
+      if (t < best_t) best_t = t, best_sp = sp;
+    }
+    const int kbs = (kb + best_sp - 1) / best_sp, eff = (kb + kbs - 1) / kbs;
+    if (eff > 1) {
+      GemmEpilogue part{};
+      part.out_hi = ep.splitk_ws;
+      part.ld_out = ldw;
+      part.alpha = 1.0f;
+      part.M = A.mn;
+      part.N = N;
+      part.split_stride = stride;
+      part.ones_col_p1 = e.ones_col_p1;
+      part.colsum_col_p1 = 0;
+      launch_2sm_pn<true, true, kEpiStoreScaled, 256, 2>(A, B, part, s, eff, nullptr, ic, b);
+      launch_fixup<kEpiStoreScaled>(ep.splitk_ws, eff, stride, ldw, e, s);
+      return 2;
+    }
+    launch_2sm_pn<true, true, kEpiStoreScaled, 256, 2>(A, B, e, s, 1, nullptr, ic, b);
+    return 1;
+  }
   const Plan plan = plan_gemm(A.mn, epi_cols(e) > N ? epi_cols(e) : N, A.k, ep.splitk_ws ? ep.splitk_ws_floats : 0,
                               ep.splitk_ws != nullptr, false, false);  // the im2col-B wgrad has a 1-CTA kernel only
   if (plan.splits > 1) {

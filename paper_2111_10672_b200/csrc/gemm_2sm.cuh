@@ -62,6 +62,7 @@ __device__ __forceinline__ void load_operand_2sm(uint8_t* dst, const CUtensorMap
 // IC == 1: A is the implicit im2col operand of a 3x3 convolution (forward or
 // stride-1 dgrad), loaded through TMA im2col maps exactly as in the 1-CTA
 // kernel (gemm_tf32x3.cuh, ConvTmaArgs), each CTA its own 128 output pixels.
+// IC == 2: B is (the conv wgrad), each CTA its own PN / 2 columns.
 template <bool A_MN, bool B_MN, int EPI, int PN = 256, int IC = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
     gemm_tf32x3_2sm_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
@@ -157,10 +158,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
               load_operand_2sm<A_MN, Cfg::kRowsA>(base, &ta_hi, &full_bar[s], m0, kb * kBK);
               load_operand_2sm<A_MN, Cfg::kRowsA>(base + Cfg::kABytes, &ta_lo, &full_bar[s], m0, kb * kBK);
             }
-            load_operand_2sm<B_MN, Cfg::kRowsB>(base + 2 * Cfg::kABytes, &tb_hi, &full_bar[s], n0, kb * kBK, &t_ones,
-                                                ones_col, 0);
-            load_operand_2sm<B_MN, Cfg::kRowsB>(base + 2 * Cfg::kABytes + Cfg::kBBytes, &tb_lo, &full_bar[s], n0,
-                                                kb * kBK, &t_ones, ones_col, 32);
+            if constexpr (IC == 2) {
+              // B = im2col columns (conv wgrad, MN-major): this CTA's kRowsB
+              // columns as 32-channel x 32-pixel boxes (N = tap * c_in + ci),
+              // as in the 1-CTA kernel; the fused bias column loads ones.
+              int w, h, n;
+              conv_origin(ic, ic.k_base + kb * kBK, w, h, n);
+#pragma unroll
+              for (int cc = 0; cc < (Cfg::kRowsB + 31) / 32; ++cc) {
+                const int col = n0 + cc * 32, tap = col / ic.c_in, c = col - tap * ic.c_in;
+                uint8_t* dh = base + 2 * Cfg::kABytes + cc * 4096;
+                if (col == ones_col) {
+                  tma_load_2d_2sm(dh, &t_ones, &full_bar[s], 0, 0);
+                  tma_load_2d_2sm(dh + Cfg::kBBytes, &t_ones, &full_bar[s], 0, 32);
+                  continue;
+                }
+                const uint16_t ox = static_cast<uint16_t>(tap % 3), oy = static_cast<uint16_t>(tap / 3);
+                tma_load_im2col_4d_2sm(dh, &tb_hi, &full_bar[s], c, w, h, n, ox, oy);
+                tma_load_im2col_4d_2sm(dh + Cfg::kBBytes, &tb_lo, &full_bar[s], c, w, h, n, ox, oy);
+              }
+            } else {
+              load_operand_2sm<B_MN, Cfg::kRowsB>(base + 2 * Cfg::kABytes, &tb_hi, &full_bar[s], n0, kb * kBK,
+                                                  &t_ones, ones_col, 0);
+              load_operand_2sm<B_MN, Cfg::kRowsB>(base + 2 * Cfg::kABytes + Cfg::kBBytes, &tb_lo, &full_bar[s], n0,
+                                                  kb * kBK, &t_ones, ones_col, 32);
+            }
           }
         }
       }
