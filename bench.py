@@ -374,7 +374,7 @@ def run_cfg4(world, rank, local, dist, K, W_):
     m.set_optimizer(c["lr"], c["momentum"], c["weight_decay"])
     out = {"workload": c["workload"], "params": int(sum(spb.convnet_block_dims(c["shape"], c["convs"], c["nout"]))),
            "data": "synthetic (numpy uniform images/targets, seed 7)",
-           "lowering": "implicit GEMM via TMA im2col (c_in % 32 == 0) on tcgen05 3xTF32; the RGB layer's forward as a direct fp32 kernel (its wgrad over im2col columns of the contributor samples); dgrad / wgrad on two streams"}
+           "lowering": "implicit GEMM via TMA im2col (c_in % 32 == 0) on tcgen05 3xTF32; the RGB layer's forward as a direct fp32 kernel (its wgrad over im2col columns of the contributor samples); dgrad / wgrad on two streams; wgrads of >= 256 output channels on the CTA pair"}
     _measure_sub(m, c, out, world, dist, K, W_)
     barrier(dist)
     m.close()
